@@ -1,0 +1,187 @@
+"""ctypes wrapper of the fp64 CPU oracle (oracle/glassnet_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  The product package
+(paper_2405_19056_b200) never imports it and shares no code with it.
+
+Parity status per function:
+  og_conv3x3  pinned (P2 Toeplitz, P7 identity, P8 stride, torch conv2d)
+  og_up2      pinned (P9 constant / ramp closed form / torch interpolate)
+  og_T_pixel  pinned (P1 hand-expanded golden, P3 permutation, P4 garbage, P5 empty, P6 duplicate)
+  og_forward  pinned (P10 torch-fp64 composition, P11 homogeneity, P13 tiles, P14 shift)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "glassnet_oracle.c")
+_LIB = os.path.join(_HERE, "libglassnet_oracle.so")
+_lib = None
+
+
+def build(force=False):
+    """gcc -O2, no fast-math, no FP contraction."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+                               "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("K", ctypes.c_int), ("L", ctypes.c_int),
+                ("c", ctypes.c_int * 4), ("h", ctypes.c_int), ("pool", ctypes.c_int),
+                ("r_takes_ld", ctypes.c_int), ("input_norm", ctypes.c_int)]
+
+
+_P = ctypes.POINTER(ctypes.c_double)
+
+
+class Dump(ctypes.Structure):
+    _fields_ = [("x", _P), ("e", _P * 4), ("tau", _P), ("phi", _P), ("y", _P * 4),
+                ("d", _P * 4), ("logits", _P)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_LIB)
+        _lib.og_weight_count.restype = ctypes.c_size_t
+        _lib.og_weight_count.argtypes = [ctypes.POINTER(Dims)]
+        _lib.og_forward.restype = ctypes.c_int
+        _lib.og_conv3x3.restype = None
+        _lib.og_up2.restype = None
+        _lib.og_T_pixel.restype = None
+    return _lib
+
+
+def make_dims(H, W, K, widths, t_hidden, levels=None, pool="sum", r_takes_ld=True,
+              input_norm=True) -> Dims:
+    levels = len(widths) if levels is None else levels
+    c = (ctypes.c_int * 4)(*(list(widths) + [0] * (4 - len(widths))))
+    return Dims(H, W, K, levels, c, t_hidden, 1 if pool == "mean" else 0,
+                1 if r_takes_ld else 0, 1 if input_norm else 0)
+
+
+def dims_from_cfg(cfg, H=None, W=None, **kw) -> Dims:
+    return make_dims(cfg.height if H is None else H, cfg.width if W is None else W,
+                     cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool, **kw)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_P)
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def weight_count(d: Dims) -> int:
+    return int(lib().og_weight_count(ctypes.byref(d)))
+
+
+def lvl(n, l):
+    for _ in range(l):
+        n = (n + 1) // 2
+    return n
+
+
+def forward(d: Dims, weights, gbuf, direct, tbuf, tcount, dump=False):
+    """One frame (arrays without batch dim), or a batch (leading dim) -> out fp64."""
+    gbuf = np.asarray(gbuf)
+    if gbuf.ndim == 4:
+        res = [forward(d, weights, gbuf[b], direct[b], tbuf[b], tcount[b], dump)
+               for b in range(gbuf.shape[0])]
+        if dump:
+            return np.stack([r[0] for r in res]), [r[1] for r in res]
+        return np.stack(res)
+    H, W, L, h = d.H, d.W, d.L, d.h
+    w = _c64(weights)
+    assert w.size == weight_count(d), (w.size, weight_count(d))
+    g, dr, t = _c64(gbuf), _c64(direct), _c64(tbuf)
+    n = np.ascontiguousarray(tcount, dtype=np.uint8)
+    assert g.shape == (H, W, 12) and dr.shape == (H, W, 3) and t.shape == (H, W, d.K, 11)
+    out = np.zeros((H, W, 3), np.float64)
+    dm = None
+    arrays = {}
+    if dump:
+        c = list(d.c)
+        arrays["x"] = np.zeros((H, W, 15))
+        arrays["e"] = [np.zeros((lvl(H, l), lvl(W, l), c[l])) for l in range(L)]
+        arrays["tau"] = np.zeros((H, W, h + 1))
+        arrays["phi"] = np.zeros((H, W, c[0]))
+        arrays["y"] = [None] + [np.zeros((lvl(H, l), lvl(W, l), c[l - 1])) for l in range(1, L)]
+        arrays["d"] = [np.zeros((lvl(H, l), lvl(W, l), c[l])) for l in range(L - 1)]
+        arrays["logits"] = np.zeros((H, W, 3))
+        dm = Dump()
+        dm.x, dm.tau, dm.phi, dm.logits = (_ptr(arrays[k]) for k in ("x", "tau", "phi", "logits"))
+        for l in range(L):
+            dm.e[l] = _ptr(arrays["e"][l])
+        for l in range(1, L):
+            dm.y[l] = _ptr(arrays["y"][l])
+        for l in range(L - 1):
+            dm.d[l] = _ptr(arrays["d"][l])
+    rc = lib().og_forward(ctypes.byref(d), _ptr(w), _ptr(g), _ptr(dr), _ptr(t),
+                          n.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), _ptr(out),
+                          ctypes.byref(dm) if dm is not None else None)
+    if rc != 0:
+        raise RuntimeError(f"og_forward failed rc={rc}")
+    return (out, arrays) if dump else out
+
+
+def conv3x3(x, Wt, b, stride=1, relu=True):
+    x, Wt, b = _c64(x), _c64(Wt), _c64(b)
+    H, W, Cin = x.shape
+    Cout = Wt.shape[0]
+    assert Wt.shape == (Cout, 3, 3, Cin)
+    out = np.zeros(((H + stride - 1) // stride, (W + stride - 1) // stride, Cout))
+    lib().og_conv3x3(_ptr(x), H, W, Cin, _ptr(Wt), _ptr(b), Cout, stride, int(relu), _ptr(out))
+    return out
+
+
+def up2(v, H2, W2):
+    v = _c64(v)
+    h, w, C = v.shape
+    out = np.zeros((H2, W2, C))
+    lib().og_up2(_ptr(v), h, w, C, H2, W2, _ptr(out))
+    return out
+
+
+def T_pixel(d: Dims, W1, b1, W2, b2, records, n):
+    rec = _c64(records)
+    assert rec.shape == (d.K, 11)
+    W1, b1, W2, b2 = _c64(W1), _c64(b1), _c64(W2), _c64(b2)
+    tau = np.zeros(d.h + 1)
+    lib().og_T_pixel(ctypes.byref(d), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(rec),
+                     int(n), _ptr(tau))
+    return tau
+
+
+def split_weights(d: Dims, weights):
+    """Blob -> dict of fp64 arrays (same documented order the library parses)."""
+    w = _c64(weights)
+    h, L, c = d.h, d.L, list(d.c)
+    out, p = {}, 0
+
+    def take(name, shape):
+        nonlocal p
+        n = int(np.prod(shape))
+        out[name] = w[p:p + n].reshape(shape)
+        p += n
+
+    take("T1.W", (h, 11)); take("T1.b", (h,)); take("T2.W", (h, h)); take("T2.b", (h,))
+    cin = 15
+    for l in range(L):
+        take(f"F{l}.W", (c[l], 3, 3, cin)); take(f"F{l}.b", (c[l],)); cin = c[l]
+    take("B.W", (c[0], c[0] + h + 1)); take("B.b", (c[0],))
+    for l in range(L - 1, 0, -1):
+        take(f"R{l}.W", (c[l - 1], 3, 3, c[l])); take(f"R{l}.b", (c[l - 1],))
+    nO = c[0] + (3 if d.r_takes_ld else 0)
+    take("O.W", (3, nO)); take("O.b", (3,))
+    assert p == w.size
+    return out
