@@ -1,0 +1,285 @@
+"""bench.py -- GlassNet forward throughput on B200 (BASELINE.json metric, configs[3]).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+One step = one forward pass of the whole hot path (T, F, B, R; all §8(a) rows) over one
+batch of 32 synthetic 1920x1080 K=8 frames per GPU (weak scaling: each rank owns its own
+32 frames, no data-path collective).  Inputs (13.7 GB per rank) are larger than L2, so
+no flush is needed between steps.  Timing: CUDA events on the launching stream, barrier
++ synchronize on both sides, max over ranks.  Prints ONE JSON line on rank 0.
+
+--impl reference times the fp64 CPU oracle (oracle/, the reference arm of this tier) on
+a bounded row band of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "GlassNet frames/sec at 1920x1080 K=8 (configs[3], batch 32 frames per GPU)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--family", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def alg_flops_per_frame(cfg, mean_n):
+    """Algorithmic FLOPs per frame (valid fragments only, unpadded)."""
+    H, W = cfg.height, cfg.width
+    c, h, L = cfg.widths, cfg.t_hidden, cfg.levels
+    P = H * W
+    macs = {}
+    macs["T"] = P * mean_n * (11 * h + h * h)
+    macs["F0"] = P * 9 * 15 * c[0]
+    for l in range(1, L):
+        macs[f"F{l}"] = (P >> (2 * l)) * 9 * c[l - 1] * c[l]
+    macs["B"] = P * (c[0] + h + 1) * c[0]
+    for l in range(L - 1, 0, -1):
+        macs[f"R{l}"] = (P >> (2 * l)) * 9 * c[l] * c[l - 1]
+    macs["O"] = P * (c[0] + 3) * 3
+    return {k: 2 * v for k, v in macs.items()}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_oracle_band(cfg, rows=(0, 272), frame=0):
+    """Oracle (single thread, fp64) on a row band of one frame; returns (seconds, fraction of frame)."""
+    import oracle
+    fr = synth.gen_frames(cfg, seed=1, frame0=frame, nframes=1, rows=rows)
+    g, d, t, n = fr.as64()
+    w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=cfg.precision == "bf16")
+    dims = oracle.make_dims(rows[1] - rows[0], cfg.width, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels,
+                            pool=cfg.pool)
+    w64 = w.astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.forward(dims, w64, g[0], d[0], t[0], n[0])
+    return time.perf_counter() - t0, (rows[1] - rows[0]) / cfg.height
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    band = (0, 64)
+    for _ in range(args.warmup):
+        cpu_oracle_band(cfg, band)
+    times = []
+    for _ in range(args.steps):
+        s, frac = cpu_oracle_band(cfg, band)
+        times.append(s)
+    tot = sum(times)
+    value = args.steps * frac / tot
+    sample = (f"frame 0 rows [{band[0]},{band[1]}) of {cfg.height} x {cfg.width} px, K={cfg.k_slots} "
+              f"({frac * 100:.1f}% of one frame) per step; fp64 C oracle, 1 thread; frames/s = fraction/time")
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+                      "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": cfg.name, "height": cfg.height, "width": cfg.width,
+                                 "k_slots": cfg.k_slots, "sample_rows": list(band)},
+                      "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                                       "sample": sample},
+                      "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}))
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_19056_b200 import GlassNet, make_dims
+    from synth import device as sdev
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[args.config]
+    B = cfg.batch
+    H, W, K = cfg.height, cfg.width, cfg.k_slots
+    w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True)
+    net = GlassNet(w, make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, precision=cfg.precision,
+                                max_batch=B, pool=cfg.pool))
+    net.set_kernel_family(args.family == "tc")
+    # inputs resident in HBM: this rank's own 32 frames (weak scaling)
+    g, d, t, n = sdev.alloc_and_fill(cfg, nframes=B, seed=1, frame0=rank * B)
+    out = torch.empty((B, H, W, 3), dtype=torch.float32, device="cuda")
+    mean_n = float(n.float().mean().item())
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        net.forward(g, d, t, n, out)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            net.forward(g, d, t, n, out)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    tmax = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = float(tmax.item())
+    value = world * B * args.steps / (ms / 1000.0)
+
+    # per-stage times (events after every launch, same stream; a second pass of K steps)
+    launches = net.launches_per_forward(B)
+    net.profile_begin(launches * args.steps + 2)
+    for _ in range(args.steps):
+        net.forward(g, d, t, n, out)
+    stages = net.profile_end()
+    torch.cuda.synchronize()
+    flops = alg_flops_per_frame(cfg, mean_n)
+    step_ms = sum(v[0] for v in stages.values()) / args.steps
+    # dominant kernel
+    top = max(stages.items(), key=lambda kv: kv[1][0])
+    top_name, (top_ms, top_cnt) = top
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    stage_flops = {"T_B_psi": flops["T"] + flops["B"], "conv_F0": flops["F0"], "conv_F1": flops["F1"],
+                   "conv_F2": flops["F2"], "conv_F3": flops["F3"], "conv_R3": flops["R3"], "conv_R2": flops["R2"],
+                   "conv_R1": flops["R1"] + 2 * (cfg.height * cfg.width // 4) * cfg.widths[0] * 3}
+    if top_name in stage_flops:
+        achieved = stage_flops[top_name] * B / (top_ms / top_cnt / 1000.0) / 1e12
+        roof = {"kernel": top_name, "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
+    else:
+        roof = {"kernel": top_name, "bound": "hbm", "achieved": None, "peak": peaks.get("hbm_gbs"),
+                "unit": "GB/s", "frac": None, "traffic": None}
+    stage_report = {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / args.steps / step_ms} for k, v in
+                    stages.items()}
+    total_alg = sum(flops.values()) * B
+    whole = {"alg_tflops_per_step": total_alg / 1e12,
+             "achieved_tflops": total_alg / (ms / args.steps / 1000.0) / 1e12,
+             "frac_of_peak": total_alg / (ms / args.steps / 1000.0) / 1e12 / peak_tf}
+
+    # end to end: public C-ABI call with pinned HOST buffers (H2D + forward + D2H inside)
+    e2e = None
+    if args.e2e_steps > 0:
+        hg, hd, ht, hn = (x.cpu().pin_memory() for x in (g, d, t, n))
+        hout = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        net.forward_host(hg, hd, ht, hn, hout)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            net.forward_host(hg, hd, ht, hn, hout)
+        e1.record(stream)
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        bi = sum(x.numel() * x.element_size() for x in (hg, hd, ht, hn))
+        e2e = {"value": world * B * args.e2e_steps / (float(ems.item()) / 1000.0), "unit": "frames/s",
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": hout.numel() * 4, "steps": args.e2e_steps}
+        del hg, hd, ht, hn, hout
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, frac = cpu_oracle_band(cfg, (0, 272))
+        cpu = {"value": frac / s, "unit": "frames/s", "cores": 1, "kind": "oracle",
+               "sample": f"frame 0 rows [0,272) of 1080 ({frac * 100:.1f}% of one 1920x1080 K=8 frame), "
+                         f"fp64 C oracle single-threaded, {s:.1f} s; value = fraction/time"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: {W}x{H}, K={K}, {B} frames per GPU, n~U{{0..{K}}}",
+                           "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world} (frames)",
+                           "kernel_family": args.family, "l2": "inputs (13.7 GB/rank) larger than L2; no flush",
+                           "mean_valid_fragments": mean_n},
+                "roofline": roof, "whole_step": whole, "stages": stage_report,
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "gpu_launches": launches * args.steps}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,150 @@
+/*
+ * glassnet.h -- C ABI of the B200-native GlassNet inference forward pass
+ * (arXiv 2405.19056; PAPER.md = /root/reference/PAPER.md, "P:n" = its line n).
+ *
+ * The operation (one frame; §3.4 "Rendering Model", and
+ * Eq. eq:SymmetricNN; widths from BASELINE.json configs[0]/[1] since the
+ * paper gives none; every reading is listed in DESIGN.md "Readings"):
+ *
+ *   x      = [G', L_d]                     G' = G with position*2^-3, depth*2^-7 (R9)
+ *   e_0    = ReLU(conv3x3_s1(x))            scene encoder F
+ *   e_l    = ReLU(conv3x3_s2(e_{l-1}))      l = 1..L-1
+ *   tau    = [ sum_{k < min(n,K)} h(b_k), n ]   T, Eq. eq:SymmetricNN; h = ReLU MLP 11->h->h
+ *   phi    = ReLU(W_B [e_0; tau] + b_B)     blending network B
+ *   d_{L-1}= e_{L-1};  y_l = ReLU(conv3x3_s1(d_l));  d_{l-1} = up2(y_l) + skip_{l-1}
+ *            (skip_0 = phi, else e_{l-1})   rendering network R
+ *   out    = sigmoid(W_O [d_0; L_d] + b_O)  fp32 RGB in [0,1]
+ *
+ * Every stage runs in this library's own sm_100a CUDA kernels.  There is no CPU
+ * fallback: a missing device or an unsupported shape is an error.
+ *
+ * Tensors (all dense, NHWC, caller-owned, >= 16-byte aligned device pointers unless a
+ * function says "host"):
+ *   gbuf   [B][H][W][12]   pos xyz, normal xyz, albedo rgb, roughness, metallic, depth
+ *   direct [B][H][W][3]    L_d (raw, un-normalised)
+ *   tbuf   [B][H][W][K][11] per slot: normal xyz, colour rgb, alpha, depth, direct rgb;
+ *                          UNSORTED; slots k >= tcount may hold any bits (NaN/Inf ok)
+ *   tcount [B][H][W] uint8 valid slots per pixel; values > K are clamped to K
+ *   out    [B][H][W][3] fp32
+ * gbuf/direct/tbuf element type = dims.precision (GLASSNET_BF16: bfloat16 bits,
+ * GLASSNET_FP32: float).
+ *
+ * Weights: one little-endian fp32 host blob, in this order (conv weights OHWI,
+ * cross-correlation, tap (ky,kx) reads offset (ky-1,kx-1)):
+ *   T1.W[h][11] T1.b[h] T2.W[h][h] T2.b[h]
+ *   F0.W[c0][3][3][15] F0.b ... F_{L-1}.W[c_{L-1}][3][3][c_{L-2}] F_{L-1}.b
+ *   B.W[c0][c0+h+1] B.b[c0]                 concat order [e0, tau_sum, n]
+ *   R_{L-1}.W[c_{L-2}][3][3][c_{L-1}] R_{L-1}.b ... R_1.W[c0][3][3][c1] R_1.b
+ *   O.W[3][c0+3] O.b[3]                     concat order [d0, L_d]
+ * In GLASSNET_BF16 mode the W tensors are rounded RNE to bf16; biases stay fp32.
+ *
+ * Errors: every function returns GLASSNET_OK (0) or an error code; the message
+ * (naming the violated invariant) is in glassnet_last_error() (thread-local).
+ * Validation is synchronous and happens before anything is enqueued.  Asynchronous
+ * device faults surface as GLASSNET_ERR_CUDA on a later call or at the caller's sync.
+ */
+#ifndef GLASSNET_H_
+#define GLASSNET_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GLASSNET_ABI_VERSION 1
+
+enum { GLASSNET_OK = 0, GLASSNET_ERR_INVALID_ARGUMENT = 1, GLASSNET_ERR_UNSUPPORTED = 2,
+       GLASSNET_ERR_CUDA = 3, GLASSNET_ERR_NCCL = 4, GLASSNET_ERR_OUT_OF_MEMORY = 5 };
+enum { GLASSNET_BF16 = 0, GLASSNET_FP32 = 1 };          /* storage + math mode         */
+enum { GLASSNET_POOL_SUM = 0, GLASSNET_POOL_MEAN = 1 };  /* g of Eq. eq:SymmetricNN     */
+enum { GLASSNET_FLAG_R_TAKES_LD = 1u << 0,               /* reading R15, default on     */
+       GLASSNET_FLAG_INPUT_NORM = 1u << 1 };             /* reading R9, default on      */
+
+typedef struct glassnet* glassnet_t;
+typedef struct glassnet_comm* glassnet_comm_t;
+typedef void* glassnet_stream_t;                         /* a cudaStream_t (0 = legacy) */
+
+typedef struct {
+  int32_t abi_version;   /* = GLASSNET_ABI_VERSION                                  */
+  int32_t height, width; /* full frame; multiples of 2^(levels-1)                   */
+  int32_t max_batch;     /* workspace is sized for this many frames                 */
+  int32_t k_slots;       /* K, 1..16                                                */
+  int32_t levels;        /* L, 2..4                                                 */
+  int32_t widths[4];     /* c_0..c_{L-1}, multiples of 16, <= 256                   */
+  int32_t t_hidden;      /* h, multiple of 16, <= 64                                */
+  int32_t precision;     /* GLASSNET_BF16 | GLASSNET_FP32                           */
+  int32_t pool;          /* GLASSNET_POOL_*                                         */
+  uint32_t flags;        /* GLASSNET_FLAG_*                                         */
+} glassnet_dims;
+
+/* Number of fp32 values in the weight blob for these dims (0 if dims are invalid). */
+size_t glassnet_weight_count(const glassnet_dims* dims);
+
+/* Create a handle on CUDA device `device`: validates dims, copies + repacks the host
+ * weight blob (n_weights fp32 values, caller keeps ownership) into device memory and
+ * allocates the workspace for dims->max_batch frames.  The workspace size does not
+ * depend on K (the transparency stage streams fragments). */
+int glassnet_create(const float* weights, size_t n_weights, const glassnet_dims* dims,
+                    int device, glassnet_t* out);
+
+/* Enqueue one forward pass of `batch` frames (1..max_batch) on `stream`.  All pointers
+ * are device pointers with the layouts above.  No host sync, no allocation.  A handle
+ * must not run two forwards concurrently. */
+int glassnet_forward(glassnet_t net, const void* gbuf, const void* direct, const void* tbuf,
+                     const uint8_t* tcount, float* out, int32_t batch, glassnet_stream_t stream);
+
+/* Same as glassnet_forward but with HOST buffers (pinned for best speed): copies the
+ * inputs host->device on `stream`, runs the forward, copies `out` back and
+ * synchronises the stream before returning (the end-to-end user call). */
+int glassnet_forward_host(glassnet_t net, const void* gbuf, const void* direct,
+                          const void* tbuf, const uint8_t* tcount, float* out, int32_t batch,
+                          glassnet_stream_t stream);
+
+/* Device bytes owned by the handle: workspace (activations) and repacked weights. */
+size_t glassnet_workspace_bytes(glassnet_t net);
+size_t glassnet_weight_bytes(glassnet_t net);
+
+/* Number of kernel launches one glassnet_forward of `batch` frames enqueues. */
+int glassnet_launches_per_forward(glassnet_t net, int32_t batch);
+
+/* Select the kernel family for bf16 mode: 1 = tcgen05 tensor-core kernels (default
+ * when built for sm_100a), 0 = SIMT FFMA kernels (the fp32-check-mode kernels run on
+ * bf16 storage).  Both are this library's CUDA; used by tests to cross-check. */
+int glassnet_set_kernel_family(glassnet_t net, int tensor_cores);
+
+/* Per-stage device timing (CUDA events recorded on the launching stream after every
+ * launch).  begin: allocate room for max_launches events and start recording.
+ * end: synchronise, then report per stage (up to max_stages) its name (32 bytes each,
+ * NUL-terminated), total milliseconds and launch count; *n_stages = stages seen. */
+int glassnet_profile_begin(glassnet_t net, int32_t max_launches);
+int glassnet_profile_end(glassnet_t net, int32_t max_stages, char* names, double* total_ms,
+                         int32_t* launches, int32_t* n_stages);
+
+/* ---- row-tile sharding (one process per GPU, NCCL point-to-point halos) ---- */
+
+/* ncclGetUniqueId into id[128] (rank 0 calls it and broadcasts the bytes). */
+int glassnet_get_unique_id(uint8_t id[128]);
+/* ncclCommInitRank on the current device; collective over nranks processes. */
+int glassnet_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank,
+                         glassnet_comm_t* out);
+void glassnet_comm_destroy(glassnet_comm_t comm);
+/* Rows [row0, row0+rows) of the full frame owned by `rank` of `nranks`: rows are split
+ * in units of u = 2^(levels-1); rank r gets units [floor(rU/N), floor((r+1)U/N)). */
+int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int32_t rank, int32_t* row0,
+                       int32_t* rows);
+/* Collective forward of ONE frame split in row tiles: each rank passes its tile's
+ * rows (pointers cover rows [row0,row0+rows) of gbuf/direct/tbuf/tcount/out).  The
+ * result equals glassnet_forward's rows bitwise (reading R22). */
+int glassnet_forward_sharded(glassnet_t net, glassnet_comm_t comm, const void* gbuf,
+                             const void* direct, const void* tbuf, const uint8_t* tcount,
+                             float* out, glassnet_stream_t stream);
+
+void glassnet_destroy(glassnet_t net);
+const char* glassnet_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLASSNET_H_ */

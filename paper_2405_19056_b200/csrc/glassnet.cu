@@ -1,0 +1,442 @@
+// glassnet.cu -- the C ABI (include/glassnet.h): validation, weight repack, workspace,
+// and the per-batch kernel chain.  PAPER.md §3.4 defines the network; the
+// layer-by-layer graph and every reading are in DESIGN.md.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/glassnet.h"
+#include "kernels_simt.cuh"
+#include "kernels_tc.cuh"
+#include "net.h"
+
+namespace {
+thread_local std::string g_err;
+}
+
+int gn_fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return gn_fail(GLASSNET_ERR_CUDA, "%s failed: %s", #x, cudaGetErrorString(e_));      \
+  } while (0)
+
+extern "C" const char* glassnet_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------------ validation
+static int validate_dims(const glassnet_dims* d) {
+  if (!d) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "dims is NULL");
+  if (d->abi_version != GLASSNET_ABI_VERSION)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "abi_version %d != %d", d->abi_version,
+                   GLASSNET_ABI_VERSION);
+  if (d->levels < 2 || d->levels > 4)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "levels must be 2..4 (got %d)", d->levels);
+  if (d->height < 1 || d->width < 1 || d->max_batch < 1)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "height/width/max_batch must be >= 1");
+  if (d->k_slots < 1) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "k_slots must be >= 1");
+  if (d->k_slots > 16) return gn_fail(GLASSNET_ERR_UNSUPPORTED, "k_slots > 16 is not implemented");
+  if (d->precision != GLASSNET_BF16 && d->precision != GLASSNET_FP32)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "precision must be GLASSNET_BF16 or GLASSNET_FP32");
+  if (d->pool != GLASSNET_POOL_SUM && d->pool != GLASSNET_POOL_MEAN)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "pool must be GLASSNET_POOL_SUM or _MEAN");
+  const int u = 1 << (d->levels - 1);
+  if (d->height % u || d->width % u)
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "height and width must be multiples of 2^(levels-1)=%d", u);
+  for (int l = 0; l < d->levels; ++l)
+    if (d->widths[l] < 16 || d->widths[l] > 256 || d->widths[l] % 16)
+      return gn_fail(GLASSNET_ERR_UNSUPPORTED, "widths[%d]=%d must be a multiple of 16 in [16,256]", l,
+                     d->widths[l]);
+  if (d->widths[0] > 32)
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "widths[0] > 32 is not implemented");
+  if (d->t_hidden != 16 && d->t_hidden != 32 && d->t_hidden != 64)
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "t_hidden must be 16, 32 or 64");
+  return GLASSNET_OK;
+}
+
+extern "C" size_t glassnet_weight_count(const glassnet_dims* d) {
+  if (validate_dims(d) != GLASSNET_OK) return 0;
+  const int h = d->t_hidden, L = d->levels;
+  const int* c = d->widths;
+  size_t n = (size_t)h * 11 + h + (size_t)h * h + h;
+  int cin = 15;
+  for (int l = 0; l < L; ++l) { n += (size_t)c[l] * 9 * cin + c[l]; cin = c[l]; }
+  n += (size_t)c[0] * (c[0] + h + 1) + c[0];
+  for (int l = L - 1; l >= 1; --l) n += (size_t)c[l - 1] * 9 * c[l] + c[l - 1];
+  const int nO = c[0] + ((d->flags & GLASSNET_FLAG_R_TAKES_LD) ? 3 : 0);
+  n += (size_t)3 * nO + 3;
+  return n;
+}
+
+// ------------------------------------------------------------------------ create
+static float round_bf16(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+template <typename X>
+static int dev_upload(X** dst, const std::vector<X>& v, size_t* acc) {
+  CUDA_TRY(cudaMalloc((void**)dst, v.size() * sizeof(X)));
+  CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));
+  *acc += v.size() * sizeof(X);
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_create(const float* weights, size_t n_weights, const glassnet_dims* dims,
+                               int device, glassnet_t* out) {
+  if (!out) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  int rc = validate_dims(dims);
+  if (rc) return rc;
+  if (!weights) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "weights is NULL");
+  const size_t need = glassnet_weight_count(dims);
+  if (n_weights != need)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "n_weights=%zu but dims need %zu", n_weights, need);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return gn_fail(GLASSNET_ERR_CUDA, "no CUDA device (this library has no CPU path)");
+  if (device < 0 || device >= ndev)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "device %d out of range [0,%d)", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                   device, prop.major, prop.minor);
+
+  glassnet* net = new glassnet();
+  net->d = *dims;
+  net->dev = device;
+  net->num_sms = prop.multiProcessorCount;
+  net->tc = (dims->precision == GLASSNET_BF16);
+  const glassnet_dims& d = *dims;
+  const int L = d.levels, h = d.t_hidden;
+  const int* c = d.widths;
+  const bool bf = d.precision == GLASSNET_BF16;
+  const bool ld = (d.flags & GLASSNET_FLAG_R_TAKES_LD) != 0;
+  auto W = [&](float v) { return bf ? round_bf16(v) : v; };
+
+  // ---- parse the blob (documented order) ----
+  const float* p = weights;
+  std::vector<const float*> FW(L), Fb(L), RW(L), Rb(L);
+  const float *T1W = p; p += (size_t)h * 11; const float* T1b = p; p += h;
+  const float *T2W = p; p += (size_t)h * h; const float* T2b = p; p += h;
+  int cin = 15;
+  for (int l = 0; l < L; ++l) { FW[l] = p; p += (size_t)c[l] * 9 * cin; Fb[l] = p; p += c[l]; cin = c[l]; }
+  const int NB = c[0] + h + 1;
+  const float* BW = p; p += (size_t)c[0] * NB; const float* Bb = p; p += c[0];
+  for (int l = L - 1; l >= 1; --l) { RW[l] = p; p += (size_t)c[l - 1] * 9 * c[l]; Rb[l] = p; p += c[l - 1]; }
+  const int NO = c[0] + (ld ? 3 : 0);
+  const float* OW = p; p += (size_t)3 * NO; const float* Ob = p;
+
+  // ---- SIMT packs ----
+  std::vector<float> tb;
+  for (int i = 0; i < h * 11; ++i) tb.push_back(W(T1W[i]));
+  for (int i = 0; i < h; ++i) tb.push_back(T1b[i]);
+  for (int i = 0; i < h * h; ++i) tb.push_back(W(T2W[i]));
+  for (int i = 0; i < h; ++i) tb.push_back(T2b[i]);
+  for (int i = 0; i < c[0] * NB; ++i) tb.push_back(W(BW[i]));
+  for (int i = 0; i < c[0]; ++i) tb.push_back(Bb[i]);
+  for (int i = 0; i < 3 * NO; ++i) tb.push_back(W(OW[i]));
+  for (int i = 0; i < 3; ++i) tb.push_back(Ob[i]);
+  rc = dev_upload(&net->w_tb, tb, &net->w_bytes);
+  if (rc) { glassnet_destroy(net); return rc; }
+  // conv: OHWI [co][ky][kx][ci] -> [tap][ci_pad][co]
+  auto pack_conv = [&](const float* src, int co_n, int ci_n, int ci_pad, std::vector<float>& dst) {
+    dst.assign((size_t)9 * ci_pad * co_n, 0.f);
+    for (int co = 0; co < co_n; ++co)
+      for (int t = 0; t < 9; ++t)
+        for (int ci = 0; ci < ci_n; ++ci)
+          dst[((size_t)t * ci_pad + ci) * co_n + co] = W(src[((size_t)co * 9 + t) * ci_n + ci]);
+  };
+  std::vector<float> tmp;
+  for (int l = 0; l < L; ++l) {
+    const int ci = l == 0 ? 15 : c[l - 1], cip = l == 0 ? 16 : c[l - 1];
+    pack_conv(FW[l], c[l], ci, cip, tmp);
+    if ((rc = dev_upload(&net->convW[l], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    std::vector<float> bb(Fb[l], Fb[l] + c[l]);
+    if ((rc = dev_upload(&net->convB[l], bb, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+  }
+  for (int l = L - 1; l >= 1; --l) {
+    pack_conv(RW[l], c[l - 1], c[l], c[l], tmp);
+    if ((rc = dev_upload(&net->convW[4 + l], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    std::vector<float> bb(Rb[l], Rb[l] + c[l - 1]);
+    if ((rc = dev_upload(&net->convB[4 + l], bb, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+  }
+  std::vector<float> wz((size_t)3 * c[0]);
+  for (int o = 0; o < 3; ++o)
+    for (int i = 0; i < c[0]; ++i) wz[(size_t)o * c[0] + i] = W(OW[(size_t)o * NO + i]);
+  if ((rc = dev_upload(&net->wz, wz, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+
+  // ---- tensor-core packs (bf16 mode) ----
+  if (bf) {
+    rc = gn::tc_pack_weights(net, T1W, T1b, T2W, T2b, FW, Fb, BW, Bb, RW, Rb, OW, Ob);
+    if (rc) { glassnet_destroy(net); return rc; }
+  }
+
+  // ---- workspace (independent of K: the T stage streams fragments) ----
+  const size_t es = bf ? 2 : 4;
+  const size_t B = (size_t)d.max_batch;
+  size_t ws = 0;
+  auto alloc = [&](void** ptr, size_t bytes) -> int {
+    if (cudaMalloc(ptr, bytes) != cudaSuccess)
+      return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "cudaMalloc(%zu) failed", bytes);
+    ws += bytes;
+    return GLASSNET_OK;
+  };
+  size_t Hl[4], Wl[4];
+  for (int l = 0; l < L; ++l) { Hl[l] = (size_t)d.height >> l; Wl[l] = (size_t)d.width >> l; }
+  const size_t P0 = Hl[0] * Wl[0];
+  rc = alloc(&net->x16, B * P0 * 16 * es);
+  for (int l = 0; l < L && !rc; ++l) rc = alloc(&net->e[l], B * Hl[l] * Wl[l] * c[l] * es);
+  if (!rc) rc = alloc((void**)&net->psi, B * P0 * 3 * sizeof(float));
+  for (int l = 1; l < L && !rc; ++l) rc = alloc(&net->y[l], B * Hl[l] * Wl[l] * c[l - 1] * es);
+  for (int l = 1; l < L - 1 && !rc; ++l) rc = alloc(&net->dd[l], B * Hl[l] * Wl[l] * c[l] * es);
+  if (!rc) rc = alloc((void**)&net->z, B * Hl[1] * Wl[1] * 3 * sizeof(float));
+  if (rc) { glassnet_destroy(net); return rc; }
+  net->ws_bytes = ws;
+  if (bf && (rc = gn::tc_setup(net))) { glassnet_destroy(net); return rc; }
+  *out = net;
+  return GLASSNET_OK;
+}
+
+extern "C" void glassnet_destroy(glassnet_t net) {
+  if (!net) return;
+  cudaSetDevice(net->dev);
+  void* ptrs[] = {net->w_tb, net->wz, net->x16, net->psi, net->z, net->st_g, net->st_d, net->st_t,
+                  net->st_n, net->st_o};
+  for (void* q : ptrs) if (q) cudaFree(q);
+  for (int i = 0; i < 8; ++i) { if (net->convW[i]) cudaFree(net->convW[i]); if (net->convB[i]) cudaFree(net->convB[i]); }
+  for (int i = 0; i < 4; ++i) { if (net->e[i]) cudaFree(net->e[i]); if (net->y[i]) cudaFree(net->y[i]); if (net->dd[i]) cudaFree(net->dd[i]); }
+  gn::tc_release(net);
+  for (auto e : net->prof.ev) cudaEventDestroy(e);
+  delete net;
+}
+
+extern "C" size_t glassnet_workspace_bytes(glassnet_t net) { return net ? net->ws_bytes : 0; }
+extern "C" size_t glassnet_weight_bytes(glassnet_t net) { return net ? net->w_bytes : 0; }
+
+extern "C" int glassnet_set_kernel_family(glassnet_t net, int tensor_cores) {
+  if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
+  if (tensor_cores && net->d.precision != GLASSNET_BF16)
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core kernels need GLASSNET_BF16 (fp32 check mode is FFMA)");
+  net->tc = tensor_cores != 0;
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_launches_per_forward(glassnet_t net, int32_t batch) {
+  if (!net) return 0;
+  const int L = net->d.levels;
+  if (net->tc) return gn::tc_launches(net, batch);
+  return 1 + L + 1 + 2 * (L - 2) + 1 + 1;
+}
+
+// ------------------------------------------------------------------------ forward (SIMT)
+static inline unsigned nblk(long n, int b) { return (unsigned)((n + b - 1) / b); }
+
+template <typename T>
+static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
+                        float* out, int B, cudaStream_t st, int row_lo = 0) {
+  const glassnet_dims& d = net->d;
+  const int L = d.levels, K = d.k_slots, h = d.t_hidden;
+  const int* c = d.widths;
+  const bool norm = (d.flags & GLASSNET_FLAG_INPUT_NORM) != 0;
+  const bool ld = (d.flags & GLASSNET_FLAG_R_TAKES_LD) != 0;
+  int Hl[4], Wl[4];
+  for (int l = 0; l < L; ++l) { Hl[l] = d.height >> l; Wl[l] = d.width >> l; }
+  const long P0 = (long)B * Hl[0] * Wl[0];
+  T* x16 = (T*)net->x16;
+  net->prof.mark(nullptr, st);
+  gn::k_prep_x<T><<<nblk(P0, 256), 256, 0, st>>>(gbuf, direct, x16, P0, norm);
+  net->prof.mark("prep_x", st);
+  static const char* conv_names[8] = {"conv_F0", "conv_F1", "conv_F2", "conv_F3", "", "conv_R1", "conv_R2", "conv_R3"};
+  auto conv = [&](const T* in, int l_in, int cin, int wi, int cout, int stride, T* o, int epi) {
+    const int Ho = Hl[l_in] / stride, Wo = Wl[l_in] / stride;
+    const long npix = (long)B * Ho * Wo;
+    const int nj = cout >= 32 ? 32 : 16;
+    dim3 grid(nblk(npix, 128), cout / nj);
+    const float* w = net->convW[wi];
+    const float* bb = net->convB[wi];
+    if (epi == 0) {
+      if (nj == 32)
+        gn::k_conv3x3_simt<T, 32, 0><<<grid, 128, 0, st>>>(in, Hl[l_in], Wl[l_in], cin, w, bb, cout, stride, o, Ho, Wo, npix, nullptr, nullptr);
+      else
+        gn::k_conv3x3_simt<T, 16, 0><<<grid, 128, 0, st>>>(in, Hl[l_in], Wl[l_in], cin, w, bb, cout, stride, o, Ho, Wo, npix, nullptr, nullptr);
+    } else {
+      if (nj == 32)
+        gn::k_conv3x3_simt<T, 32, 1><<<grid, 128, 0, st>>>(in, Hl[l_in], Wl[l_in], cin, w, bb, cout, stride, nullptr, Ho, Wo, npix, net->wz, net->z);
+      else
+        gn::k_conv3x3_simt<T, 16, 1><<<grid, 128, 0, st>>>(in, Hl[l_in], Wl[l_in], cin, w, bb, cout, stride, nullptr, Ho, Wo, npix, net->wz, net->z);
+    }
+    net->prof.mark(conv_names[wi], st);
+  };
+  T* e[4];
+  for (int l = 0; l < L; ++l) e[l] = (T*)net->e[l];
+  conv(x16, 0, 16, 0, c[0], 1, e[0], 0);
+  for (int l = 1; l < L; ++l) conv(e[l - 1], l - 1, c[l - 1], l, c[l], 2, e[l], 0);
+  // T + B + psi
+  {
+    const int NB = c[0] + h + 1, NO = c[0] + (ld ? 3 : 0);
+    const size_t smem = sizeof(float) * (h * 11 + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3);
+    const unsigned g = nblk(P0, 128);
+#define TB_LAUNCH(HH, CC)                                                                              \
+  {                                                                                                    \
+    auto kfn = gn::k_tb_simt<T, HH, CC>;                                                               \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                \
+    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e[0], direct, net->w_tb, net->psi, P0, K, d.pool, ld, norm); \
+  }
+    if (h == 64 && c[0] == 32) TB_LAUNCH(64, 32)
+    else if (h == 64 && c[0] == 16) TB_LAUNCH(64, 16)
+    else if (h == 32 && c[0] == 32) TB_LAUNCH(32, 32)
+    else if (h == 32 && c[0] == 16) TB_LAUNCH(32, 16)
+    else if (h == 16 && c[0] == 32) TB_LAUNCH(16, 32)
+    else TB_LAUNCH(16, 16)
+#undef TB_LAUNCH
+    net->prof.mark("T_B_psi", st);
+  }
+  // R: d_{L-1} = e_{L-1}
+  const T* dcur = e[L - 1];
+  for (int l = L - 1; l >= 2; --l) {
+    T* yl = (T*)net->y[l];
+    conv(dcur, l, c[l], 4 + l, c[l - 1], 1, yl, 0);
+    T* dn = (T*)net->dd[l - 1];
+    const long nvec = (long)B * Hl[l - 1] * Wl[l - 1] * (c[l - 1] / 8);
+    gn::k_up2add<T><<<nblk(nvec, 256), 256, 0, st>>>(yl, Hl[l], Wl[l], e[l - 1], dn, Hl[l - 1], Wl[l - 1], c[l - 1], nvec);
+    net->prof.mark("up2add", st);
+    dcur = dn;
+  }
+  conv(dcur, 1, c[1], 4 + 1, c[0], 1, nullptr, 1);  // R_1 -> z (3 fp32 at level 1)
+  gn::k_output<<<nblk(P0, 256), 256, 0, st>>>(net->z, Hl[1], Wl[1], net->psi, out, Hl[0], Wl[0], P0);
+  net->prof.mark("output", st);
+  (void)row_lo;
+  CUDA_TRY(cudaGetLastError());
+  return GLASSNET_OK;
+}
+
+static int check_ptr(const void* p, const char* name) {
+  if (!p) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "%s is NULL", name);
+  if ((uintptr_t)p % 16) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "%s is not 16-byte aligned", name);
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_forward(glassnet_t net, const void* gbuf, const void* direct, const void* tbuf,
+                                const uint8_t* tcount, float* out, int32_t batch, glassnet_stream_t stream) {
+  if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
+  int rc;
+  if ((rc = check_ptr(gbuf, "gbuf")) || (rc = check_ptr(direct, "direct")) || (rc = check_ptr(tbuf, "tbuf")) ||
+      (rc = check_ptr(out, "out")))
+    return rc;
+  if (!tcount) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "tcount is NULL");
+  if (batch < 1 || batch > net->d.max_batch)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "batch=%d outside [1, max_batch=%d]", batch, net->d.max_batch);
+  CUDA_TRY(cudaSetDevice(net->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (net->d.precision == GLASSNET_FP32)
+    return forward_simt<float>(net, (const float*)gbuf, (const float*)direct, (const float*)tbuf, tcount, out, batch, st);
+  if (net->tc)
+    return gn::tc_forward(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
+                          (const __nv_bfloat16*)tbuf, tcount, out, batch, st);
+  return forward_simt<__nv_bfloat16>(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
+                                     (const __nv_bfloat16*)tbuf, tcount, out, batch, st);
+}
+
+extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const void* direct, const void* tbuf,
+                                     const uint8_t* tcount, float* out, int32_t batch, glassnet_stream_t stream) {
+  if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
+  if (!gbuf || !direct || !tbuf || !tcount || !out)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "a host buffer is NULL");
+  if (batch < 1 || batch > net->d.max_batch)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "batch=%d outside [1, max_batch=%d]", batch, net->d.max_batch);
+  CUDA_TRY(cudaSetDevice(net->dev));
+  const glassnet_dims& d = net->d;
+  const size_t es = d.precision == GLASSNET_BF16 ? 2 : 4;
+  const size_t P = (size_t)d.height * d.width;
+  const size_t MB = (size_t)d.max_batch;
+  if (!net->st_g) {  // device staging, allocated once per handle on first use
+    CUDA_TRY(cudaMalloc(&net->st_g, MB * P * 12 * es));
+    CUDA_TRY(cudaMalloc(&net->st_d, MB * P * 3 * es));
+    CUDA_TRY(cudaMalloc(&net->st_t, MB * P * d.k_slots * 11 * es));
+    CUDA_TRY(cudaMalloc(&net->st_n, MB * P));
+    CUDA_TRY(cudaMalloc((void**)&net->st_o, MB * P * 3 * sizeof(float)));
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t Bn = (size_t)batch;
+  CUDA_TRY(cudaMemcpyAsync(net->st_g, gbuf, Bn * P * 12 * es, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(net->st_d, direct, Bn * P * 3 * es, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(net->st_t, tbuf, Bn * P * d.k_slots * 11 * es, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(net->st_n, tcount, Bn * P, cudaMemcpyHostToDevice, st));
+  int rc = glassnet_forward(net, net->st_g, net->st_d, net->st_t, (const uint8_t*)net->st_n, net->st_o, batch, stream);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, net->st_o, Bn * P * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GLASSNET_OK;
+}
+
+// ------------------------------------------------------------------------ profiling
+extern "C" int glassnet_profile_begin(glassnet_t net, int32_t max_launches) {
+  if (!net || max_launches < 2) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "bad profile_begin args");
+  CUDA_TRY(cudaSetDevice(net->dev));
+  StageProfiler& p = net->prof;
+  for (auto e : p.ev) cudaEventDestroy(e);
+  p.ev.assign((size_t)max_launches, nullptr);
+  p.stage.assign((size_t)max_launches, -1);
+  for (auto& e : p.ev) CUDA_TRY(cudaEventCreate(&e));
+  p.used = 0;
+  p.on = true;
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_profile_end(glassnet_t net, int32_t max_stages, char* names, double* total_ms,
+                                    int32_t* launches, int32_t* n_stages) {
+  if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
+  StageProfiler& p = net->prof;
+  p.on = false;
+  std::vector<double> tot(p.names.size(), 0.0);
+  std::vector<int> cnt(p.names.size(), 0);
+  if (p.used) CUDA_TRY(cudaEventSynchronize(p.ev[p.used - 1]));
+  for (size_t i = 1; i < p.used; ++i) {
+    if (p.stage[i] < 0) continue;
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.ev[i - 1], p.ev[i]));
+    tot[p.stage[i]] += ms;
+    cnt[p.stage[i]] += 1;
+  }
+  const int n = (int)p.names.size();
+  if (n_stages) *n_stages = n;
+  for (int i = 0; i < n && i < max_stages; ++i) {
+    if (names) { strncpy(names + 32 * i, p.names[i].c_str(), 31); names[32 * i + 31] = 0; }
+    if (total_ms) total_ms[i] = tot[i];
+    if (launches) launches[i] = cnt[i];
+  }
+  for (auto e : p.ev) cudaEventDestroy(e);
+  p.ev.clear(); p.stage.clear(); p.names.clear(); p.used = 0;
+  return GLASSNET_OK;
+}
+
+// ------------------------------------------------------------------------ tiles
+extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int32_t rank, int32_t* row0,
+                                  int32_t* rows) {
+  int rc = validate_dims(dims);
+  if (rc) return rc;
+  if (nranks < 1 || rank < 0 || rank >= nranks || !row0 || !rows)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "bad nranks/rank/out pointers");
+  const int u = 1 << (dims->levels - 1);
+  const long U = dims->height / u;
+  const long a = U * rank / nranks, b = U * (rank + 1) / nranks;
+  if (b <= a) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "too many ranks (%d) for %ld row units", nranks, U);
+  *row0 = (int32_t)(a * u);
+  *rows = (int32_t)((b - a) * u);
+  return GLASSNET_OK;
+}

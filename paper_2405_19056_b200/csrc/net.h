@@ -1,0 +1,58 @@
+// net.h -- the handle behind glassnet_t (library-internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/glassnet.h"
+
+int gn_fail(int code, const char* fmt, ...);
+
+#include <cuda_runtime.h>
+#include <string>
+
+// Optional per-stage timing with CUDA events on the launching stream (bench.py's
+// roofline): when enabled, an event is recorded after every launch.
+struct StageProfiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> stage;           // stage id of the interval ending at ev[i] (-1 = start)
+  std::vector<std::string> names;
+  size_t used = 0;
+  int id(const char* n) {
+    for (size_t i = 0; i < names.size(); ++i) if (names[i] == n) return (int)i;
+    names.push_back(n);
+    return (int)names.size() - 1;
+  }
+  void mark(const char* n, cudaStream_t st) {
+    if (!on || used >= ev.size()) return;
+    stage[used] = n ? id(n) : -1;
+    cudaEventRecord(ev[used++], st);
+  }
+};
+
+struct glassnet {
+  glassnet_dims d{};
+  int dev = 0;
+  int num_sms = 148;
+  bool tc = false;          // bf16 mode: tensor-core kernel family
+  // SIMT weight packs (fp32; W tensors pre-rounded to bf16 values in bf16 mode)
+  float* w_tb = nullptr;    // W1 b1 W2 b2 WB bB WO bO
+  float* convW[8] = {};     // [l] = F_l, [4+l] = R_l ; layout [tap][ci][co]
+  float* convB[8] = {};
+  float* wz = nullptr;      // [3][c0] = W_O[:, :c0]
+  // workspace (per max_batch)
+  void* x16 = nullptr;      // [B][H][W][16]
+  void* e[4] = {};          // encoder features
+  float* psi = nullptr;     // [B][H][W][3]   (reading R15)
+  void* y[4] = {};          // y_l at level l
+  void* dd[4] = {};         // d_l (1 <= l <= L-2)
+  float* z = nullptr;       // [B][H/2][W/2][3]
+  size_t ws_bytes = 0, w_bytes = 0;
+  // staging for glassnet_forward_host
+  void *st_g = nullptr, *st_d = nullptr, *st_t = nullptr, *st_n = nullptr;
+  float* st_o = nullptr;
+  // tensor-core state (kernels_tc.cuh)
+  void* tc_state = nullptr;
+  StageProfiler prof;
+};

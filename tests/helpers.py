@@ -1,0 +1,62 @@
+"""Test helpers: host<->torch marshalling and the windowed oracle for sampled full-size parity."""
+import numpy as np
+
+import oracle
+import synth
+
+BF16_TOL = (3e-2, 3e-3)    # BASELINE.json north_star: max abs, mean abs on the [0,1] output (bf16 mode)
+FP32_TOL = 1e-4            # fp32 check mode
+
+
+def to_torch(fr, device="cuda"):
+    import torch
+    if fr.precision == "bf16":
+        cv = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16)
+    else:
+        cv = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+    g, d, t = (cv(a).to(device) for a in (fr.gbuf, fr.direct, fr.tbuf))
+    n = torch.from_numpy(np.ascontiguousarray(fr.tcount)).to(device)
+    return g, d, t, n
+
+
+def weights_for(cfg, seed=0):
+    return synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=seed,
+                              bf16_weights=(cfg.precision == "bf16"))
+
+
+def net_for(cfg, max_batch=None, **kw):
+    from paper_2405_19056_b200 import GlassNet, make_dims
+    dims = make_dims(cfg.height, cfg.width, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels,
+                     precision=cfg.precision, max_batch=cfg.batch if max_batch is None else max_batch,
+                     pool=cfg.pool, **kw)
+    return GlassNet(weights_for(cfg), dims)
+
+
+def oracle_full(cfg, weights, fr, frame_idx=0):
+    g, d, t, n = fr.as64()
+    dims = oracle.dims_from_cfg(cfg)
+    return oracle.forward(dims, weights.astype(np.float64), g[frame_idx], d[frame_idx], t[frame_idx],
+                          n[frame_idx])
+
+
+def window_oracle(cfg, weights, frame, rows, cols, margin=64, seed=1, mask=None):
+    """Oracle output for out[frame, rows[0]:rows[1], cols[0]:cols[1]] computed on a crop of
+    the frame extended by `margin` px (aligned to 2^(L-1)); inputs drawn by the host
+    generator for exactly that crop (tile-invariant).  Bitwise equal to the full-frame
+    oracle when margin covers the receptive field (pinned in test_window_oracle)."""
+    u = 1 << (cfg.levels - 1)
+    H, W = cfg.height, cfg.width
+    a = max(0, (rows[0] - margin) // u * u)
+    b = min(H, -(-(rows[1] + margin) // u) * u)
+    c = max(0, (cols[0] - margin) // u * u)
+    e = min(W, -(-(cols[1] + margin) // u) * u)
+    fr = synth.gen_frames(cfg, seed=seed, frame0=frame, nframes=1, rows=(a, b), cols=(c, e), mask=mask)
+    g, d, t, n = fr.as64()
+    dims = oracle.make_dims(b - a, e - c, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool)
+    out = oracle.forward(dims, weights.astype(np.float64), g[0], d[0], t[0], n[0])
+    return out[rows[0] - a:rows[1] - a, cols[0] - c:cols[1] - c]
+
+
+def errs(gpu, ref):
+    e = np.abs(np.asarray(gpu, np.float64) - ref)
+    return float(e.max()), float(e.mean())

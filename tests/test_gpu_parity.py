@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star): bf16 mode max abs <= 3e-2 and mean abs <= 3e-3 on
+the [0,1] output; fp32 check mode max abs <= 1e-4.  Bitwise: slot permutation, masked
+garbage, run-to-run determinism, kernel-family independence of the permutation property.
+"""
+import numpy as np
+import pytest
+
+import synth
+from helpers import BF16_TOL, FP32_TOL, errs, net_for, oracle_full, to_torch, weights_for, window_oracle
+
+pytestmark = pytest.mark.gpu
+
+C1NET = dict(levels=4, widths=(32, 64, 128, 256), t_hidden=64)
+FAMILIES = ["tc", "simt"]
+
+
+def _cfg(name, H, W, B, K, prec, net=None, **kw):
+    n = net or C1NET
+    return synth.Config(name, H, W, B, K, n["levels"], n["widths"], n["t_hidden"], prec, **kw)
+
+
+def _run(cfg, fr, family=None, net=None):
+    import torch
+    net = net or net_for(cfg)
+    if family is not None:
+        net.set_kernel_family(family == "tc")
+    g, d, t, n = to_torch(fr)
+    out = net.forward(g, d, t, n)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), net
+
+
+def test_synth_device_matches_numpy(cuda_ok):
+    from synth import device
+    for prec in ("bf16", "fp32"):
+        cfg = _cfg("s", 40, 56, 2, 5, prec)
+        host = synth.gen_frames(cfg, seed=7)
+        g, d, t, n = device.alloc_and_fill(cfg, seed=7)
+        dev = [a.cpu().view(__import__("torch").int16).numpy().view(np.uint16) if prec == "bf16" else a.cpu().numpy()
+               for a in (g, d, t)]
+        assert np.array_equal(dev[0], host.gbuf) and np.array_equal(dev[1], host.direct)
+        assert np.array_equal(dev[2], host.tbuf) and np.array_equal(n.cpu().numpy(), host.tcount)
+        # row window + frame offset
+        g2, d2, t2, n2 = device.alloc_and_fill(cfg, nframes=1, seed=7, frame0=1, rows=(8, 24))
+        assert np.array_equal(n2.cpu().numpy()[0], host.tcount[1, 8:24])
+    # disc mask mode
+    cfg = _cfg("s2", 48, 80, 1, 8, "bf16", tcount_mode="discs")
+    m = synth.disc_mask(1, 48, 80)
+    _, _, _, n = device.alloc_and_fill(cfg, mask=m)
+    assert np.array_equal(n.cpu().numpy(), synth.gen_frames(cfg, mask=m).tcount)
+
+
+def test_fp32_check_mode_c0(cuda_ok):
+    """configs[0] (64x64, K=4, fp32): max abs <= 1e-4 (P15)."""
+    cfg = synth.CONFIGS["c0"]
+    fr = synth.gen_frames(cfg)
+    out, _ = _run(cfg, fr)
+    mx, mean = errs(out[0], oracle_full(cfg, weights_for(cfg), fr))
+    print(f"c0 fp32: max {mx:.3e} mean {mean:.3e}")
+    assert mx <= FP32_TOL
+
+
+def test_fp32_check_mode_c1_net_ragged(cuda_ok):
+    cfg = _cfg("f32", 40, 136, 2, 8, "fp32")
+    fr = synth.gen_frames(cfg)
+    out, _ = _run(cfg, fr)
+    w = weights_for(cfg)
+    for b in range(2):
+        mx, _ = errs(out[b], oracle_full(cfg, w, fr, b))
+        assert mx <= FP32_TOL, (b, mx)
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("H,W,K,B", [(64, 96, 8, 2), (40, 280, 8, 1), (32, 136, 16, 1), (24, 48, 3, 3)])
+def test_bf16_parity_small(cuda_ok, family, H, W, K, B):
+    """Several tiles plus ragged tails; c1 network; K in {3, 8, 16}."""
+    cfg = _cfg("b", H, W, B, K, "bf16")
+    fr = synth.gen_frames(cfg)
+    out, _ = _run(cfg, fr, family)
+    w = weights_for(cfg)
+    for b in range(B):
+        mx, mean = errs(out[b], oracle_full(cfg, w, fr, b))
+        print(f"{family} {H}x{W} K={K} frame {b}: max {mx:.3e} mean {mean:.3e}")
+        assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1]
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+def test_mean_pool_and_c0_net_bf16(cuda_ok, family):
+    cfg = synth.Config("m", 32, 64, 1, 4, 3, (16, 32, 64), 32, "bf16", pool="mean")
+    fr = synth.gen_frames(cfg)
+    out, _ = _run(cfg, fr, family)
+    mx, mean = errs(out[0], oracle_full(cfg, weights_for(cfg), fr))
+    assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1]
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_permutation_garbage_bitwise(cuda_ok, family, prec):
+    """P3/P4 on the GPU: permuting the valid slots and filling masked slots with NaN/Inf
+    bit patterns gives a bitwise-identical output (table:OrderLoss P:666-679; R4, R5)."""
+    if prec == "fp32" and family == "tc":
+        pytest.skip("fp32 check mode has only the FFMA family")
+    rng = np.random.default_rng(5)
+    cfg = _cfg("p", 32, 48, 1, 8, prec)
+    fr = synth.gen_frames(cfg)
+    out, net = _run(cfg, fr, family)
+    tb = fr.tbuf.copy()
+    n = fr.tcount[0]
+    garbage = (np.array([0x7FC0, 0x7F80, 0xFF80, 0xFFFF], np.uint16) if prec == "bf16"
+               else np.array([np.nan, np.inf, -np.inf, 3e38], np.float32))
+    for y in range(32):
+        for x in range(48):
+            m = int(n[y, x])
+            tb[0, y, x, :m] = fr.tbuf[0, y, x, rng.permutation(m)]
+            tb[0, y, x, m:] = rng.choice(garbage, size=(8 - m, 11))
+    fr2 = synth.Frames(fr.gbuf, fr.direct, tb, fr.tcount, prec)
+    out2, _ = _run(cfg, fr2, family, net)
+    assert np.array_equal(out.view(np.uint32), out2.view(np.uint32))
+    out3, _ = _run(cfg, fr, family, net)                       # run-to-run determinism
+    assert np.array_equal(out.view(np.uint32), out3.view(np.uint32))
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+def test_empty_and_full_counts(cuda_ok, family):
+    """P5: n = 0 everywhere (the empty-set latent) and n = K everywhere, and n > K clamps."""
+    cfg = _cfg("e", 32, 32, 1, 8, "bf16")
+    fr = synth.gen_frames(cfg)
+    w = weights_for(cfg)
+    for fill in (0, 8, 255):
+        fr2 = synth.Frames(fr.gbuf, fr.direct, fr.tbuf, np.full_like(fr.tcount, fill), "bf16")
+        out, _ = _run(cfg, fr2, family)
+        fr_ref = synth.Frames(fr.gbuf, fr.direct, fr.tbuf, np.full_like(fr.tcount, min(fill, 8)), "bf16")
+        mx, mean = errs(out[0], oracle_full(cfg, w, fr_ref))
+        assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1], (fill, mx)
+
+
+def test_workspace_independent_of_K(cuda_ok):
+    """P12 (fig:MemUsage): the library's workspace does not grow with K."""
+    sizes = []
+    for K in (4, 8, 16):
+        cfg = _cfg("k", 64, 64, 2, K, "bf16")
+        net = net_for(cfg)
+        sizes.append(net.workspace_bytes())
+        net.close()
+    assert sizes[0] == sizes[1] == sizes[2], sizes
+
+
+def test_families_agree(cuda_ok):
+    """The tensor-core and SIMT families compute the same function (both vs each other)."""
+    cfg = _cfg("fa", 48, 128, 1, 8, "bf16")
+    fr = synth.gen_frames(cfg)
+    a, net = _run(cfg, fr, "tc")
+    b, _ = _run(cfg, fr, "simt", net)
+    assert np.abs(a - b).max() < 3e-2
+
+
+# ------------------------------------------------------------------ full-size (sampled)
+def _full_size(cfg_name, frames, patches, family="tc", mask=None):
+    import torch
+    from synth import device
+    cfg = synth.CONFIGS[cfg_name]
+    net = net_for(cfg)
+    net.set_kernel_family(family == "tc")
+    g, d, t, n = device.alloc_and_fill(cfg, mask=mask)
+    out = net.forward(g, d, t, n)
+    torch.cuda.synchronize()
+    w = weights_for(cfg)
+    worst = (0.0, 0.0)
+    for f in frames:
+        for (r0, c0) in patches:
+            rows, cols = (r0, r0 + 16), (c0, c0 + 32)
+            ref = window_oracle(cfg, w, f, rows, cols, margin=40, mask=mask)
+            got = out[f, rows[0]:rows[1], cols[0]:cols[1]].cpu().numpy()
+            mx, mean = errs(got, ref)
+            worst = (max(worst[0], mx), max(worst[1], mean))
+            assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1], (cfg_name, f, r0, c0, mx, mean)
+    print(f"{cfg_name} sampled: worst max {worst[0]:.3e} worst mean {worst[1]:.3e}")
+    return out
+
+
+def test_full_size_c1(cuda_ok):
+    _full_size("c1", [0, 3], [(0, 0), (248, 240), (496, 480)])
+
+
+def test_full_size_c2(cuda_ok):
+    m = synth.disc_mask(1, 720, 1280)
+    _full_size("c2", [0], [(0, 0), (360, 640), (704, 1248), (100, 900)], mask=m)
+
+
+def test_full_size_c3_bench_config(cuda_ok):
+    """configs[3] in the launch configuration bench.py times (batch 32, 1920x1080)."""
+    _full_size("c3", [0, 17, 31], [(0, 0), (536, 960), (1064, 1888)])
+
+
+def test_full_size_c4(cuda_ok):
+    _full_size("c4", [0], [(0, 0), (1080, 1920), (2144, 3808)])
