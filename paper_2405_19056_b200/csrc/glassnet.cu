@@ -181,7 +181,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   if ((rc = dev_upload(&net->wz, wz, &net->w_bytes))) { glassnet_destroy(net); return rc; }
 
   // ---- tensor-core packs (bf16 mode) ----
-  if (bf) {
+  if (bf && gn::tc_supported(d)) {
     rc = gn::tc_pack_weights(net, T1W, T1b, T2W, T2b, FW, Fb, BW, Bb, RW, Rb, OW, Ob);
     if (rc) { glassnet_destroy(net); return rc; }
   }
@@ -207,7 +207,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   if (!rc) rc = alloc((void**)&net->z, B * Hl[1] * Wl[1] * 3 * sizeof(float));
   if (rc) { glassnet_destroy(net); return rc; }
   net->ws_bytes = ws;
-  if (bf && (rc = gn::tc_setup(net))) { glassnet_destroy(net); return rc; }
+  net->tc = bf && gn::tc_supported(d);
   *out = net;
   return GLASSNET_OK;
 }
@@ -232,6 +232,9 @@ extern "C" int glassnet_set_kernel_family(glassnet_t net, int tensor_cores) {
   if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
   if (tensor_cores && net->d.precision != GLASSNET_BF16)
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core kernels need GLASSNET_BF16 (fp32 check mode is FFMA)");
+  if (tensor_cores && !gn::tc_supported(net->d))
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "no tensor-core kernels for t_hidden=%d widths[0]=%d", net->d.t_hidden,
+                   net->d.widths[0]);
   net->tc = tensor_cores != 0;
   return GLASSNET_OK;
 }
@@ -239,7 +242,7 @@ extern "C" int glassnet_set_kernel_family(glassnet_t net, int tensor_cores) {
 extern "C" int glassnet_launches_per_forward(glassnet_t net, int32_t batch) {
   if (!net) return 0;
   const int L = net->d.levels;
-  if (net->tc) return gn::tc_launches(net, batch);
+  (void)batch;
   return 1 + L + 1 + 2 * (L - 2) + 1 + 1;
 }
 
@@ -247,8 +250,8 @@ extern "C" int glassnet_launches_per_forward(glassnet_t net, int32_t batch) {
 static inline unsigned nblk(long n, int b) { return (unsigned)((n + b - 1) / b); }
 
 template <typename T>
-static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
-                        float* out, int B, cudaStream_t st, int row_lo = 0) {
+static int forward_chain(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
+                         float* out, int B, cudaStream_t st, bool tc) {
   const glassnet_dims& d = net->d;
   const int L = d.levels, K = d.k_slots, h = d.t_hidden;
   const int* c = d.widths;
@@ -287,7 +290,14 @@ static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* 
   conv(x16, 0, 16, 0, c[0], 1, e[0], 0);
   for (int l = 1; l < L; ++l) conv(e[l - 1], l - 1, c[l - 1], l, c[l], 2, e[l], 0);
   // T + B + psi
-  {
+  if (tc) {
+    if constexpr (sizeof(T) == 2) {
+      int trc = gn::tc_launch_tb(net, (const __nv_bfloat16*)tbuf, tcount, (const __nv_bfloat16*)e[0],
+                                 (const __nv_bfloat16*)direct, P0, st);
+      if (trc) return trc;
+      net->prof.mark("T_B_psi", st);
+    }
+  } else {
     const int NB = c[0] + h + 1, NO = c[0] + (ld ? 3 : 0);
     const size_t smem = sizeof(float) * (h * 11 + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3);
     const unsigned g = nblk(P0, 128);
@@ -320,7 +330,6 @@ static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* 
   conv(dcur, 1, c[1], 4 + 1, c[0], 1, nullptr, 1);  // R_1 -> z (3 fp32 at level 1)
   gn::k_output<<<nblk(P0, 256), 256, 0, st>>>(net->z, Hl[1], Wl[1], net->psi, out, Hl[0], Wl[0], P0);
   net->prof.mark("output", st);
-  (void)row_lo;
   CUDA_TRY(cudaGetLastError());
   return GLASSNET_OK;
 }
@@ -344,12 +353,10 @@ extern "C" int glassnet_forward(glassnet_t net, const void* gbuf, const void* di
   CUDA_TRY(cudaSetDevice(net->dev));
   cudaStream_t st = (cudaStream_t)stream;
   if (net->d.precision == GLASSNET_FP32)
-    return forward_simt<float>(net, (const float*)gbuf, (const float*)direct, (const float*)tbuf, tcount, out, batch, st);
-  if (net->tc)
-    return gn::tc_forward(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
-                          (const __nv_bfloat16*)tbuf, tcount, out, batch, st);
-  return forward_simt<__nv_bfloat16>(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
-                                     (const __nv_bfloat16*)tbuf, tcount, out, batch, st);
+    return forward_chain<float>(net, (const float*)gbuf, (const float*)direct, (const float*)tbuf, tcount, out, batch,
+                                st, false);
+  return forward_chain<__nv_bfloat16>(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
+                                      (const __nv_bfloat16*)tbuf, tcount, out, batch, st, net->tc);
 }
 
 extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const void* direct, const void* tbuf,

@@ -1,25 +1,439 @@
-// kernels_tc.cuh -- tcgen05 tensor-core kernels (bf16 mode).  Placeholder until the
-// tcgen05 family lands: bf16 mode runs the SIMT family.
+// kernels_tc.cuh -- tcgen05 tensor-core kernels for bf16 mode.
+//
+// k_tb_tc: the fused T + B + psi kernel.  Per 128-pixel tile and per
+// fragment slot s (canonical order, reading R5):
+//   A1[128x16]  = records (11 ch, bf16) | 1,1,1 (bias hi/mid/lo columns) | 0        (smem)
+//   acc         = A1 * W1ext^T                   (TMEM, fp32)      T.h layer 1
+//   A2[128xH+16]= ReLU(acc) (bf16) | 1,1,1 | 0                         (smem)
+//   acc         = A2 * W2ext^T                   (TMEM)            T.h layer 2
+//   A3[128xH]   = ReLU(acc) / (mean ? n : 1)  (f16)                  (smem)
+//   accB       += A3 * W_B,tau^T                 (TMEM)            g = sum (Eq. eq:SymmetricNN)
+// with accB initialised by e0 * W_B,e0^T.  The pool over fragments is carried out by the
+// tensor core's accumulation: W_B (sum_k a2_k) = sum_k (W_B a2_k) (linearity; reading R15-
+// style rewrite).  Per-fragment activations never leave the SM.
+// Invalid slots are all-zero rows including the bias columns, so they contribute exactly 0.
+// Epilogue: phi = ReLU(accB + b_B + w_Bn n); psi = W_O,d0 phi + W_O,L L_d + b_O (fp32).
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <vector>
 
 #include "net.h"
+#include "tc_ptx.cuh"
 
 namespace gn {
 
-inline int tc_pack_weights(glassnet*, const float*, const float*, const float*, const float*,
-                           const std::vector<const float*>&, const std::vector<const float*>&,
-                           const float*, const float*, const std::vector<const float*>&,
-                           const std::vector<const float*>&, const float*, const float*) {
+// ------------------------------------------------------------------------ T+B+psi
+template <int K, int H, int C0>
+struct TbLayout {
+  static constexpr int KA2 = H + 16;
+  static constexpr int W1_B = H * 16 * 2;
+  static constexpr int W2_B = H * KA2 * 2;
+  static constexpr int WBT_B = C0 * H * 2;
+  static constexpr int WBE_B = C0 * C0 * 2;
+  static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B;
+  static constexpr int NPAR = C0 + C0 + 3 * (C0 + 3) + 3;
+  static constexpr int OFF_W = 0;
+  static constexpr int OFF_W1 = OFF_W, OFF_W2 = OFF_W1 + W1_B, OFF_WBT = OFF_W2 + W2_B, OFF_WBE = OFF_WBT + WBT_B;
+  static constexpr int OFF_A1 = OFF_W + WIMG_B;
+  static constexpr int OFF_A2 = OFF_A1 + 128 * 16 * 2;
+  static constexpr int OFF_A3 = OFF_A2 + 128 * KA2 * 2;
+  static constexpr int OFF_AE = OFF_A3 + 128 * H * 2;
+  static constexpr int OFF_ST = OFF_AE + 128 * C0 * 2;
+  static constexpr int ST_B = ((128 * K * 22) + 15) / 16 * 16;
+  static constexpr int OFF_PAR = OFF_ST + ST_B;
+  static constexpr int OFF_BAR = (OFF_PAR + NPAR * 4 + 15) / 16 * 16;
+  static constexpr int SMEM = OFF_BAR + 16;
+  static constexpr int TMEM_COLS = (H + C0) <= 64 ? 64 : ((H + C0) <= 128 ? 128 : 256);
+};
+
+template <int K>
+__device__ __forceinline__ bool frag_less(const uint16_t* rec, int ia, int ib, uint64_t ka, uint64_t kb, int m) {
+  const bool va = ia < m, vb = ib < m;
+  if (va != vb) return va;
+  if (!va) return false;
+  if (ka != kb) return ka < kb;
+  const uint16_t* a = rec + ia * 11;
+  const uint16_t* b = rec + ib * 11;
+#pragma unroll 1
+  for (int c = 3; c < 11; ++c)
+    if (a[c] != b[c]) return a[c] < b[c];
+  return false;
+}
+
+template <int K, int H, int C0>
+__global__ void __launch_bounds__(128, 2)
+k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const uint16_t* __restrict__ e0,
+        const uint16_t* __restrict__ direct, const uint8_t* __restrict__ wimg, const float* __restrict__ params,
+        float* __restrict__ psi, long P, int pool, int r_takes_ld) {
+  using S = TbLayout<K, H, C0>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 8);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  for (int i = tid; i < S::WIMG_B / 16; i += 128)
+    reinterpret_cast<int4*>(smem + S::OFF_W)[i] = reinterpret_cast<const int4*>(wimg)[i];
+  float* par = reinterpret_cast<float*>(smem + S::OFF_PAR);
+  for (int i = tid; i < S::NPAR; i += 128) par[i] = params[i];
+  if (tid == 0) { tc::mbar_init(mbar, 1); tc::fence_mbar_init(); }
+  if (warp == 0) tc::tmem_alloc<S::TMEM_COLS>(tptr);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+  const uint32_t t_acc = tmem, t_accB = tmem + H;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const float* bB = par;
+  const float* wBn = par + C0;
+  const int NO = C0 + 3;
+  const float* WO = par + 2 * C0;
+  const float* bO = WO + 3 * NO;
+
+  const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sA2 = tc::smem_u32(smem + S::OFF_A2);
+  const uint32_t sA3 = tc::smem_u32(smem + S::OFF_A3), sAE = tc::smem_u32(smem + S::OFF_AE);
+  const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
+  const uint32_t sWBT = tc::smem_u32(smem + S::OFF_WBT), sWBE = tc::smem_u32(smem + S::OFF_WBE);
+  constexpr uint32_t PL = 128 * 16;   // one K-plane of a 128-row A operand
+  constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
+  constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
+  constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
+  const uint16_t* st = reinterpret_cast<const uint16_t*>(smem + S::OFF_ST);
+  uint32_t phase = 0;
+  const long ntiles = (P + 127) / 128;
+
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long p0 = tile * 128;
+    const int np = (int)min((long)128, P - p0);
+    {  // stage the tile's records (coalesced 8-byte loads)
+      const uint2* src = reinterpret_cast<const uint2*>(tbuf + p0 * K * 11);
+      uint2* dst = reinterpret_cast<uint2*>(smem + S::OFF_ST);
+      const int nu = np * K * 22 / 8;
+      for (int i = tid; i < nu; i += 128) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const int r = tid;
+    const long p = p0 + r;
+    const bool pv = r < np;
+    int m = pv ? (int)tcount[p] : 0;
+    m = m < K ? m : K;
+    const uint16_t* rec = st + r * K * 11;
+    // ---- canonical fragment order (R5): sort (validity, key64, rest) ----
+    uint64_t key[K];
+    int ix[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      ix[k] = k;
+      const uint16_t* q = rec + k * 11;
+      key[k] = k < m ? ((uint64_t)q[7] << 48) | ((uint64_t)q[0] << 32) | ((uint64_t)q[1] << 16) | (uint64_t)q[2]
+                     : ~0ull;
+    }
+#pragma unroll
+    for (int pass = 0; pass < K; ++pass) {
+#pragma unroll
+      for (int i = pass & 1; i + 1 < K; i += 2) {
+        if (frag_less<K>(rec, ix[i + 1], ix[i], key[i + 1], key[i], m)) {
+          uint64_t tk = key[i]; key[i] = key[i + 1]; key[i + 1] = tk;
+          int ti = ix[i]; ix[i] = ix[i + 1]; ix[i + 1] = ti;
+        }
+      }
+    }
+    // ---- operands that do not depend on the slot ----
+    if (pv) {
+      const uint4* e = reinterpret_cast<const uint4*>(e0 + p * C0);
+#pragma unroll
+      for (int j = 0; j < C0 / 8; ++j) {
+        uint4 v = __ldg(e + j);
+        tc::sts128(sAE + j * PL + r * 16, v.x, v.y, v.z, v.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < C0 / 8; ++j) tc::sts128(sAE + j * PL + r * 16, 0, 0, 0, 0);
+    }
+    float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;
+    if (pv) {
+      ld0 = __uint_as_float((uint32_t)direct[p * 3 + 0] << 16);
+      ld1 = __uint_as_float((uint32_t)direct[p * 3 + 1] << 16);
+      ld2 = __uint_as_float((uint32_t)direct[p * 3 + 2] << 16);
+    }
+    const float inv_m = (pool == 1 && m > 0) ? 1.f / (float)m : 1.f;
+    auto write_A1 = [&](int s) {
+      uint32_t w[8];
+      if (s < m) {
+        const uint16_t* q = rec + ix[s] * 11;
+        w[0] = q[0] | ((uint32_t)q[1] << 16);
+        w[1] = q[2] | ((uint32_t)q[3] << 16);
+        w[2] = q[4] | ((uint32_t)q[5] << 16);
+        w[3] = q[6] | ((uint32_t)q[7] << 16);
+        w[4] = q[8] | ((uint32_t)q[9] << 16);
+        w[5] = q[10] | (0x3F80u << 16);
+        w[6] = 0x3F80u | (0x3F80u << 16);
+        w[7] = 0;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = 0;
+      }
+      tc::sts128(sA1 + r * 16, w[0], w[1], w[2], w[3]);
+      tc::sts128(sA1 + PL + r * 16, w[4], w[5], w[6], w[7]);
+    };
+    write_A1(0);
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int q = 0; q < C0 / 16; ++q)
+        tc::mma_f16_ss(t_accB, tc::smem_desc(sAE + 2 * q * PL, PL, 128),
+                       tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
+      tc::mma_f16_ss(t_acc, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
+      tc::mma_commit(mbar);
+    }
+#pragma unroll 1
+    for (int s = 0; s < K; ++s) {
+      tc::mbar_wait(mbar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      // epilogue 1: a1 = ReLU(acc) -> bf16 -> A2 ; bias columns
+#pragma unroll
+      for (int c = 0; c < H / 16; ++c) {
+        uint32_t v[16];
+        tc::tmem_ld16(t_acc + lane_off + c * 16, v);
+        tc::tmem_ld_wait();
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = tc::cvt_relu_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        tc::sts128(sA2 + (2 * c) * PL + r * 16, w[0], w[1], w[2], w[3]);
+        tc::sts128(sA2 + (2 * c + 1) * PL + r * 16, w[4], w[5], w[6], w[7]);
+      }
+      {
+        const uint32_t one = s < m ? 0x3F80u : 0u;
+        tc::sts128(sA2 + (H / 8) * PL + r * 16, one | (one << 16), one, 0, 0);
+        tc::sts128(sA2 + (H / 8 + 1) * PL + r * 16, 0, 0, 0, 0);
+      }
+      tc::fence_before_sync();
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+#pragma unroll
+        for (int q = 0; q < S::KA2 / 16; ++q)
+          tc::mma_f16_ss(t_acc, tc::smem_desc(sA2 + 2 * q * PL, PL, 128),
+                         tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
+        tc::mma_commit(mbar);
+      }
+      tc::mbar_wait(mbar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      // epilogue 2: a2 = ReLU(acc) (/n in mean mode) -> f16 -> A3
+#pragma unroll
+      for (int c = 0; c < H / 16; ++c) {
+        uint32_t v[16];
+        tc::tmem_ld16(t_acc + lane_off + c * 16, v);
+        tc::tmem_ld_wait();
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          w[i] = tc::cvt_relu_f16x2(__uint_as_float(v[2 * i]) * inv_m, __uint_as_float(v[2 * i + 1]) * inv_m);
+        tc::sts128(sA3 + (2 * c) * PL + r * 16, w[0], w[1], w[2], w[3]);
+        tc::sts128(sA3 + (2 * c + 1) * PL + r * 16, w[4], w[5], w[6], w[7]);
+      }
+      if (s + 1 < K) write_A1(s + 1);
+      tc::fence_before_sync();
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+#pragma unroll
+        for (int q = 0; q < H / 16; ++q)
+          tc::mma_f16_ss(t_accB, tc::smem_desc(sA3 + 2 * q * PL, PL, 128),
+                         tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
+        if (s + 1 < K)
+          tc::mma_f16_ss(t_acc, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
+        tc::mma_commit(mbar);
+      }
+    }
+    tc::mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+    // epilogue 3: phi = ReLU(accB + b_B + w_Bn m); psi = W_O phi + W_O,L L_d + b_O
+    float ps0 = bO[0], ps1 = bO[1], ps2 = bO[2];
+    if (r_takes_ld) {
+      ps0 = fmaf(WO[0 * NO + C0 + 0], ld0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], ld1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], ld2, ps0);
+      ps1 = fmaf(WO[1 * NO + C0 + 0], ld0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], ld1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], ld2, ps1);
+      ps2 = fmaf(WO[2 * NO + C0 + 0], ld0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], ld1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], ld2, ps2);
+    }
+    const float fm = (float)m;
+#pragma unroll
+    for (int c = 0; c < C0 / 16; ++c) {
+      uint32_t v[16];
+      tc::tmem_ld16(t_accB + lane_off + c * 16, v);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int o = c * 16 + i;
+        const float phi = relu(__uint_as_float(v[i]) + bB[o] + wBn[o] * fm);
+        ps0 = fmaf(WO[0 * NO + o], phi, ps0);
+        ps1 = fmaf(WO[1 * NO + o], phi, ps1);
+        ps2 = fmaf(WO[2 * NO + o], phi, ps2);
+      }
+    }
+    if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
+    tc::fence_before_sync();
+    __syncthreads();
+  }
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<S::TMEM_COLS>(tmem);
+}
+
+// ------------------------------------------------------------------------ host side
+struct TcState {
+  uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
+  float* tb_par = nullptr;      // bB, wBn, WO (c0+3 wide), bO
+};
+
+static inline uint16_t h_bf16(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+  return (uint16_t)u;
+}
+static inline float h_bf16f(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+static inline uint16_t h_f16(float f) {
+  __half h = __float2half_rn(f);
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
+}
+
+// K-major, SWIZZLE_NONE operand image: plane j (K columns 8j..8j+7) holds all N rows.
+static void pack_kmajor(const std::vector<float>& W, int N, int Kc, bool f16, std::vector<uint8_t>& out) {
+  const size_t base = out.size();
+  out.resize(base + (size_t)N * Kc * 2);
+  uint16_t* o = reinterpret_cast<uint16_t*>(out.data() + base);
+  for (int j = 0; j < Kc / 8; ++j)
+    for (int n = 0; n < N; ++n)
+      for (int kk = 0; kk < 8; ++kk) {
+        const float v = W[(size_t)n * Kc + 8 * j + kk];
+        o[((size_t)j * N + n) * 8 + kk] = f16 ? h_f16(v) : h_bf16(v);
+      }
+}
+
+// b = hi + mid + lo with each piece bf16 (exact for normal fp32 b).
+static void split3(float b, float& hi, float& mid, float& lo) {
+  hi = h_bf16f(h_bf16(b));
+  double r = (double)b - hi;
+  mid = h_bf16f(h_bf16((float)r));
+  r -= mid;
+  lo = h_bf16f(h_bf16((float)r));
+}
+
+inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, const float* T2W, const float* T2b,
+                           const std::vector<const float*>& FW, const std::vector<const float*>& Fb,
+                           const float* BW, const float* Bb, const std::vector<const float*>& RW,
+                           const std::vector<const float*>& Rb, const float* OW, const float* Ob) {
+  (void)FW; (void)Fb; (void)RW; (void)Rb;
+  const glassnet_dims& d = net->d;
+  const int H = d.t_hidden, C0 = d.widths[0];
+  const bool norm = (d.flags & GLASSNET_FLAG_INPUT_NORM) != 0;
+  const bool ld = (d.flags & GLASSNET_FLAG_R_TAKES_LD) != 0;
+  TcState* s = new TcState();
+  net->tc_state = s;
+  auto rb = [](float v) { return h_bf16f(h_bf16(v)); };
+  std::vector<uint8_t> img;
+  // W1ext [H][16]: cols 0..10 = W1 (depth col x 2^-7 when normalising), 11..13 = b1 hi/mid/lo
+  std::vector<float> w1((size_t)H * 16, 0.f);
+  for (int o = 0; o < H; ++o) {
+    for (int i = 0; i < 11; ++i) w1[(size_t)o * 16 + i] = rb(T1W[o * 11 + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
+    split3(T1b[o], w1[(size_t)o * 16 + 11], w1[(size_t)o * 16 + 12], w1[(size_t)o * 16 + 13]);
+  }
+  pack_kmajor(w1, H, 16, false, img);
+  // W2ext [H][H+16]
+  const int KA2 = H + 16;
+  std::vector<float> w2((size_t)H * KA2, 0.f);
+  for (int o = 0; o < H; ++o) {
+    for (int i = 0; i < H; ++i) w2[(size_t)o * KA2 + i] = rb(T2W[o * H + i]);
+    split3(T2b[o], w2[(size_t)o * KA2 + H], w2[(size_t)o * KA2 + H + 1], w2[(size_t)o * KA2 + H + 2]);
+  }
+  pack_kmajor(w2, H, KA2, false, img);
+  const int NB = C0 + H + 1;
+  std::vector<float> wbt((size_t)C0 * H), wbe((size_t)C0 * C0);
+  for (int o = 0; o < C0; ++o) {
+    for (int j = 0; j < H; ++j) wbt[(size_t)o * H + j] = rb(BW[(size_t)o * NB + C0 + j]);
+    for (int i = 0; i < C0; ++i) wbe[(size_t)o * C0 + i] = rb(BW[(size_t)o * NB + i]);
+  }
+  pack_kmajor(wbt, C0, H, true, img);
+  pack_kmajor(wbe, C0, C0, false, img);
+  std::vector<float> par;
+  for (int o = 0; o < C0; ++o) par.push_back(Bb[o]);
+  for (int o = 0; o < C0; ++o) par.push_back(rb(BW[(size_t)o * NB + C0 + H]));
+  const int NO = C0 + (ld ? 3 : 0);
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < C0 + 3; ++i) par.push_back(i < NO ? rb(OW[(size_t)j * NO + i]) : 0.f);
+  for (int j = 0; j < 3; ++j) par.push_back(Ob[j]);
+  if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess || cudaMalloc(&s->tb_par, par.size() * 4) != cudaSuccess)
+    return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "tc weight alloc");
+  cudaMemcpy(s->tb_wimg, img.data(), img.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(s->tb_par, par.data(), par.size() * 4, cudaMemcpyHostToDevice);
+  net->w_bytes += img.size() + par.size() * 4;
   return 0;
 }
-inline int tc_setup(glassnet* net) { net->tc = false; return 0; }
-inline void tc_release(glassnet*) {}
-inline int tc_launches(glassnet*, int) { return 0; }
-inline int tc_forward(glassnet* net, const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
-                      const uint8_t*, float*, int, cudaStream_t) {
-  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core family not built");
+
+inline bool tc_supported(const glassnet_dims& d) {
+  return (d.t_hidden == 32 || d.t_hidden == 64) && (d.widths[0] == 16 || d.widths[0] == 32);
+}
+
+inline void tc_release(glassnet* net) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  if (!s) return;
+  if (s->tb_wimg) cudaFree(s->tb_wimg);
+  if (s->tb_par) cudaFree(s->tb_par);
+  delete s;
+  net->tc_state = nullptr;
+}
+
+template <int K, int H, int C0>
+static int launch_tb_tc_k(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
+                          const __nv_bfloat16* direct, long P, cudaStream_t st) {
+  using S = TbLayout<K, H, C0>;
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  auto kfn = k_tb_tc<K, H, C0>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+  const long ntiles = (P + 127) / 128;
+  long grid = 2L * net->num_sms;
+  if (grid > ntiles) grid = ntiles;
+  kfn<<<(unsigned)grid, 128, S::SMEM, st>>>(
+      reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
+      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, net->psi, P, net->d.pool,
+      (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0);
+  return 0;
+}
+
+template <int H, int C0>
+static int launch_tb_tc_h(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
+                          const __nv_bfloat16* direct, long P, cudaStream_t st) {
+  switch (net->d.k_slots) {
+#define KCASE(k) case k: return launch_tb_tc_k<k, H, C0>(net, tbuf, tcount, e0, direct, P, st);
+    KCASE(1) KCASE(2) KCASE(3) KCASE(4) KCASE(5) KCASE(6) KCASE(7) KCASE(8)
+    KCASE(9) KCASE(10) KCASE(11) KCASE(12) KCASE(13) KCASE(14) KCASE(15) KCASE(16)
+#undef KCASE
+  }
+  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "k_slots");
+}
+
+inline int tc_launch_tb(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
+                        const __nv_bfloat16* direct, long P, cudaStream_t st) {
+  const int H = net->d.t_hidden, C0 = net->d.widths[0];
+  if (H == 64 && C0 == 32) return launch_tb_tc_h<64, 32>(net, tbuf, tcount, e0, direct, P, st);
+  if (H == 32 && C0 == 16) return launch_tb_tc_h<32, 16>(net, tbuf, tcount, e0, direct, P, st);
+  if (H == 32 && C0 == 32) return launch_tb_tc_h<32, 32>(net, tbuf, tcount, e0, direct, P, st);
+  if (H == 64 && C0 == 16) return launch_tb_tc_h<64, 16>(net, tbuf, tcount, e0, direct, P, st);
+  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core T kernel: (t_hidden, widths[0]) = (%d, %d)", H, C0);
 }
 
 }  // namespace gn
