@@ -180,12 +180,6 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
     for (int i = 0; i < c[0]; ++i) wz[(size_t)o * c[0] + i] = W(OW[(size_t)o * NO + i]);
   if ((rc = dev_upload(&net->wz, wz, &net->w_bytes))) { glassnet_destroy(net); return rc; }
 
-  // ---- tensor-core packs (bf16 mode) ----
-  if (bf && gn::tc_supported(d)) {
-    rc = gn::tc_pack_weights(net, T1W, T1b, T2W, T2b, FW, Fb, BW, Bb, RW, Rb, OW, Ob);
-    if (rc) { glassnet_destroy(net); return rc; }
-  }
-
   // ---- workspace (independent of K: the T stage streams fragments) ----
   const size_t es = bf ? 2 : 4;
   const size_t B = (size_t)d.max_batch;
@@ -207,6 +201,12 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   if (!rc) rc = alloc((void**)&net->z, B * Hl[1] * Wl[1] * 3 * sizeof(float));
   if (rc) { glassnet_destroy(net); return rc; }
   net->ws_bytes = ws;
+  // ---- tensor-core packs (bf16 mode) ----
+  if (bf && gn::tc_supported(d)) {
+    rc = gn::tc_pack_weights(net, T1W, T1b, T2W, T2b, FW, Fb, BW, Bb, RW, Rb, OW, Ob);
+    if (!rc) rc = gn::tc_setup_convs(net, FW, RW);
+    if (rc) { glassnet_destroy(net); return rc; }
+  }
   net->tc = bf && gn::tc_supported(d);
   *out = net;
   return GLASSNET_OK;
@@ -266,6 +266,11 @@ static int forward_chain(glassnet* net, const T* gbuf, const T* direct, const T*
   net->prof.mark("prep_x", st);
   static const char* conv_names[8] = {"conv_F0", "conv_F1", "conv_F2", "conv_F3", "", "conv_R1", "conv_R2", "conv_R3"};
   auto conv = [&](const T* in, int l_in, int cin, int wi, int cout, int stride, T* o, int epi) {
+    if (tc) {
+      gn::tc_launch_conv(net, wi, B, st);
+      net->prof.mark(conv_names[wi], st);
+      return;
+    }
     const int Ho = Hl[l_in] / stride, Wo = Wl[l_in] / stride;
     const long npix = (long)B * Ho * Wo;
     const int nj = cout >= 32 ? 32 : 16;

@@ -1,0 +1,226 @@
+// kernels_conv_tc.cuh -- NHWC bf16 implicit-GEMM conv3x3 on tcgen05.
+//
+// out[b][oy][ox][co] = ReLU(bias[co] + sum_{ky,kx,ci} W[co][ky][kx][ci] in[b][s*oy+ky-1][s*ox+kx-1][ci])
+// (PAPER.md P:366-383 scene encoder F / rendering network R; reading R10/R12).
+//
+// GEMM view per CTA tile: M = 128 output pixels of one output row, N = NS output
+// channels (a split of C_out), K = 9 taps x C_in.  The A operand is never materialised:
+// TMA copies, per 16-channel chunk, the 3 input rows of the tile's halo into shared
+// memory (zero fill outside the image = the conv's zero padding) in the K-major
+// "interleaved" core-matrix layout, and each of the 9 taps is a shifted UMMA descriptor
+// into that halo (stride 2 uses even/odd de-interleaved halos so every tap is affine).
+// The weights of the CTA's N-split stay resident in shared memory for the whole
+// persistent kernel.  Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner),
+// 2..5 = epilogue (TMEM -> bias/ReLU -> bf16 NHWC store, or the z projection of R_1).
+// Accumulators are double-buffered in TMEM so the epilogue overlaps the next tile.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "net.h"
+#include "tc_ptx.cuh"
+
+namespace gn {
+namespace conv {
+
+constexpr int TILE_M = 128;
+// bytes of one 8-channel plane of the halo in shared memory (128-byte aligned pieces)
+template <int S> struct Halo;
+template <> struct Halo<1> {
+  static constexpr int SLOTS = TILE_M + 2;                       // x0-1 .. x0+128
+  static constexpr int PLANE = (3 * SLOTS * 16 + 127) / 128 * 128;
+  static constexpr int TX = 3 * SLOTS * 16;                      // bytes TMA writes per plane
+};
+template <> struct Halo<2> {
+  static constexpr int EVEN = 3 * TILE_M * 16;                   // pixels 2(x0+i)
+  static constexpr int ODD_OFF = EVEN;                           // pixels 2(x0+i)-1, i = 0..128
+  static constexpr int PLANE = (EVEN + 3 * (TILE_M + 1) * 16 + 127) / 128 * 128;
+  static constexpr int TX = EVEN + 3 * (TILE_M + 1) * 16;
+};
+
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          dst),
+      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+          dst),
+      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+struct ConvArgs {
+  const uint8_t* wimg;   // [nsplit][9][Cin/8][NS][8] bf16 (K-major planes)
+  const float* bias;     // [Cout]
+  uint16_t* out;         // [B][Ho][Wo][Cout] bf16 (EPI 0)
+  const float* wz;       // [3][Cout] (EPI 1)
+  float* zout;           // [B][Ho][Wo][3] (EPI 1)
+  int Cin, Cout, Ho, Wo, B, nsplit, nstage;
+};
+
+template <int S, int NS, int EPI>
+__global__ void __launch_bounds__(192, 1)
+k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
+  using HL = Halo<S>;
+  constexpr int SB = 2 * HL::PLANE;                 // one stage = 16 channels = 2 planes
+  constexpr int TMEM_COLS = (2 * NS) <= 32 ? 32 : (2 * NS) <= 64 ? 64 : (2 * NS) <= 128 ? 128 : (2 * NS) <= 256 ? 256 : 512;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Cin = a.Cin, NST = a.nstage;
+  const int wbytes = 9 * Cin * NS * 2;
+  uint8_t* sW = smem;
+  uint8_t* sA = smem + ((wbytes + 1023) / 1024) * 1024;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + NST * SB);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NST;
+  uint64_t* tfull = bars + 2 * NST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int split = blockIdx.x % a.nsplit;
+  {  // resident weights of this split
+    const int4* src = reinterpret_cast<const int4*>(a.wimg + (size_t)split * wbytes);
+    int4* dst = reinterpret_cast<int4*>(sW);
+    for (int i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(tfull + i, 1); tc::mbar_init(tempty + i, 128); }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tptr);
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+
+  const int ntx = (a.Wo + TILE_M - 1) / TILE_M;
+  const long ntiles = (long)a.B * a.Ho * ntx;
+  const int cta = blockIdx.x / a.nsplit, ncta = gridDim.x / a.nsplit;
+  const int nchunk = Cin / 16;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t ph = 0;
+      for (long t = cta; t < ntiles; t += ncta) {
+        const int xt = (int)(t % ntx);
+        const long r = t / ntx;
+        const int oy = (int)(r % a.Ho);
+        const int b = (int)(r / a.Ho);
+        const int x0 = xt * TILE_M;
+        for (int c = 0; c < nchunk; ++c) {
+          tc::mbar_wait(empty + stage, ph ^ 1);
+          tc::mbar_arrive_expect_tx(full + stage, 2 * HL::TX);
+          const uint32_t dst = tc::smem_u32(sA + stage * SB);
+          for (int j = 0; j < 2; ++j) {
+            const int ch = (2 * c + j) * 8;
+            if (S == 1) {
+              tma_4d(dst + j * HL::PLANE, &tmA, ch, x0 - 1, oy - 1, b, full + stage);
+            } else {
+              tma_5d(dst + j * HL::PLANE, &tmA, ch, 0, x0, 2 * oy - 1, b, full + stage);
+              tma_5d(dst + j * HL::PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, 2 * oy - 1, b, full + stage);
+            }
+          }
+          if (++stage == NST) { stage = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t IDESC = tc::idesc_f16(128, NS, 1, 1);
+      const uint32_t sWa = tc::smem_u32(sW), sAa = tc::smem_u32(sA);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (long t = cta; t < ntiles; t += ncta) {
+        tc::mbar_wait(tempty + acc, aph ^ 1);
+        tc::fence_after_sync();
+        const uint32_t d = tmem + acc * NS;
+        for (int c = 0; c < nchunk; ++c) {
+          tc::mbar_wait(full + stage, ph);
+          tc::fence_after_sync();
+          const uint32_t base = sAa + stage * SB;
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int ky = tap / 3, kx = tap % 3;
+            uint32_t aoff;
+            if (S == 1) aoff = (ky * Halo<1>::SLOTS + kx) * 16;
+            else aoff = kx == 1 ? ky * TILE_M * 16 : Halo<2>::ODD_OFF + (ky * (TILE_M + 1) + (kx == 2 ? 1 : 0)) * 16;
+            const uint64_t ad = tc::smem_desc(base + aoff, HL::PLANE, 128);
+            const uint64_t bd = tc::smem_desc(sWa + (uint32_t)((tap * (Cin / 8) + 2 * c) * NS * 16), NS * 16, 128);
+            tc::mma_f16_ss(d, ad, bd, IDESC, (c | tap) != 0);
+          }
+          tc::mma_commit(empty + stage);
+          if (++stage == NST) { stage = 0; ph ^= 1; }
+        }
+        tc::mma_commit(tfull + acc);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5
+    const int q = warp & 3;               // TMEM lane quarter of this warp
+    const int m = q * 32 + lane;
+    const int co0 = split * NS;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (long t = cta; t < ntiles; t += ncta) {
+      const int xt = (int)(t % ntx);
+      const long r = t / ntx;
+      const int oy = (int)(r % a.Ho);
+      const int b = (int)(r / a.Ho);
+      const int px = xt * TILE_M + m;
+      const bool valid = px < a.Wo;
+      const long opix = ((long)b * a.Ho + oy) * a.Wo + px;
+      tc::mbar_wait(tfull + acc, aph);
+      tc::fence_after_sync();
+      const uint32_t taddr = tmem + acc * NS + ((uint32_t)(q * 32) << 16);
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < NS / 16; ++c) {
+        uint32_t v[16];
+        tc::tmem_ld16(taddr + c * 16, v);
+        tc::tmem_ld_wait();
+        float y[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[i] = relu(__uint_as_float(v[i]) + __ldg(a.bias + co0 + c * 16 + i));
+        if (EPI == 0) {
+          if (valid) {
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = tc::cvt_bf16x2(y[2 * i], y[2 * i + 1]);
+            uint4* dst = reinterpret_cast<uint4*>(a.out + opix * a.Cout + co0 + c * 16);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int o = c * 16 + i;
+            z0 = fmaf(__ldg(a.wz + o), y[i], z0);
+            z1 = fmaf(__ldg(a.wz + NS + o), y[i], z1);
+            z2 = fmaf(__ldg(a.wz + 2 * NS + o), y[i], z2);
+          }
+        }
+      }
+      if (EPI == 1 && valid) {
+        a.zout[opix * 3 + 0] = z0; a.zout[opix * 3 + 1] = z1; a.zout[opix * 3 + 2] = z2;
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(tempty + acc);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+}  // namespace conv
+}  // namespace gn

@@ -19,6 +19,7 @@
 
 #include <vector>
 
+#include "kernels_conv_tc.cuh"
 #include "net.h"
 #include "tc_ptx.cuh"
 
@@ -287,9 +288,22 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
 }
 
 // ------------------------------------------------------------------------ host side
+struct TcConv {
+  bool used = false;
+  int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0;
+  int Hi = 0, Wi = 0, Ho = 0, Wo = 0;
+  size_t smem = 0;
+  int ctas_per_sm = 1;
+  CUtensorMap mA, mO;
+  uint8_t* wimg = nullptr;
+  const float* bias = nullptr;
+  uint16_t* out = nullptr;
+};
+
 struct TcState {
   uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
   float* tb_par = nullptr;      // bB, wBn, WO (c0+3 wide), bO
+  TcConv conv[8];               // [l] = F_l, [4+l] = R_l
 };
 
 static inline uint16_t h_bf16(float f) {
@@ -384,6 +398,142 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   return 0;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// Halo tensor maps over an NHWC bf16 activation [B][H][W][C] (zero fill out of bounds).
+static int make_halo_maps(TcConv& L, void* in, int B, int C) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return gn_fail(GLASSNET_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r;
+  if (L.S == 1) {
+    const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)L.Wi, (cuuint64_t)L.Hi, (cuuint64_t)B};
+    const cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)L.Wi * C * 2, (cuuint64_t)L.Hi * L.Wi * C * 2};
+    const cuuint32_t box[4] = {8, conv::Halo<1>::SLOTS, 3, 1};
+    r = enc(&L.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    L.mO = L.mA;
+  } else {
+    const cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)L.Wi / 2, (cuuint64_t)L.Hi, (cuuint64_t)B};
+    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, (cuuint64_t)L.Wi * C * 2,
+                               (cuuint64_t)L.Hi * L.Wi * C * 2};
+    const cuuint32_t boxE[5] = {8, 1, conv::TILE_M, 3, 1};
+    const cuuint32_t boxO[5] = {8, 1, conv::TILE_M + 1, 3, 1};
+    r = enc(&L.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+      r = enc(&L.mO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxO, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return gn_fail(GLASSNET_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+static size_t conv_smem(int S, int Cin, int NS, int nstage) {
+  const size_t sb = 2 * (S == 1 ? conv::Halo<1>::PLANE : conv::Halo<2>::PLANE);
+  return (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024 + nstage * sb + (2 * nstage + 4) * 8 + 16;
+}
+
+// One conv layer: choose the N split so the split's weights stay resident, pack them.
+static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const float* bias, int cin_real, int Cin,
+                      int Cout, int Hi, int Wi, void* in, void* out, int epi) {
+  constexpr size_t LIMIT = 232448 - 1024;
+  L.used = true; L.S = S; L.Cin = Cin; L.Cout = Cout; L.epi = epi;
+  L.Hi = Hi; L.Wi = Wi; L.Ho = Hi / S; L.Wo = Wi / S;
+  int NS = Cout;
+  while (NS > 16 && conv_smem(S, Cin, NS, 2) > LIMIT) NS /= 2;
+  if (conv_smem(S, Cin, NS, 2) > LIMIT || (epi == 1 && NS != Cout))
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv %d->%d does not fit shared memory", Cin, Cout);
+  L.NS = NS;
+  L.nsplit = Cout / NS;
+  L.nstage = 4;
+  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage) > LIMIT) --L.nstage;
+  L.smem = conv_smem(S, Cin, NS, L.nstage);
+  const int tcols = 2 * NS <= 32 ? 32 : 2 * NS <= 64 ? 64 : 2 * NS <= 128 ? 128 : 2 * NS <= 256 ? 256 : 512;
+  L.ctas_per_sm = (int)(232448 / (L.smem + 1024));
+  if (L.ctas_per_sm > 2) L.ctas_per_sm = 2;
+  if (L.ctas_per_sm * tcols > 512) L.ctas_per_sm = 512 / tcols;
+  if (L.ctas_per_sm < 1) L.ctas_per_sm = 1;
+  // weights: [split][tap][Cin/8][NS][8] bf16
+  std::vector<uint16_t> img((size_t)L.nsplit * 9 * Cin * NS, 0);
+  for (int sp = 0; sp < L.nsplit; ++sp)
+    for (int t = 0; t < 9; ++t)
+      for (int j = 0; j < Cin / 8; ++j)
+        for (int n = 0; n < NS; ++n)
+          for (int kk = 0; kk < 8; ++kk) {
+            const int co = sp * NS + n, ci = 8 * j + kk;
+            const float v = ci < cin_real ? W[((size_t)co * 9 + t) * cin_real + ci] : 0.f;
+            img[((((size_t)sp * 9 + t) * (Cin / 8) + j) * NS + n) * 8 + kk] = h_bf16(v);
+          }
+  if (cudaMalloc(&L.wimg, img.size() * 2) != cudaSuccess)
+    return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "conv weight image");
+  cudaMemcpy(L.wimg, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
+  net->w_bytes += img.size() * 2;
+  L.bias = bias;
+  L.out = reinterpret_cast<uint16_t*>(out);
+  return make_halo_maps(L, in, net->d.max_batch, Cin);
+}
+
+template <int S, int NS, int EPI>
+static void launch_conv_k(glassnet* net, const TcConv& L, int B, cudaStream_t st) {
+  auto kfn = conv::k_conv_tc<S, NS, EPI>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+  conv::ConvArgs a;
+  a.wimg = L.wimg; a.bias = L.bias; a.out = L.out; a.wz = net->wz; a.zout = net->z;
+  a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = L.Ho; a.Wo = L.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
+  const long ntiles = (long)B * L.Ho * ((L.Wo + conv::TILE_M - 1) / conv::TILE_M);
+  long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
+  if (per_split > ntiles) per_split = ntiles;
+  if (per_split < 1) per_split = 1;
+  kfn<<<(unsigned)(per_split * L.nsplit), 192, L.smem, st>>>(L.mA, L.mO, a);
+}
+
+static int launch_conv(glassnet* net, const TcConv& L, int B, cudaStream_t st) {
+#define CONV_CASE(S_, NS_, E_) \
+  if (L.S == S_ && L.NS == NS_ && L.epi == E_) { launch_conv_k<S_, NS_, E_>(net, L, B, st); return 0; }
+  CONV_CASE(1, 16, 0) CONV_CASE(1, 32, 0) CONV_CASE(1, 64, 0) CONV_CASE(1, 128, 0) CONV_CASE(1, 256, 0)
+  CONV_CASE(2, 16, 0) CONV_CASE(2, 32, 0) CONV_CASE(2, 64, 0) CONV_CASE(2, 128, 0) CONV_CASE(2, 256, 0)
+  CONV_CASE(1, 16, 1) CONV_CASE(1, 32, 1)
+#undef CONV_CASE
+  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv variant S=%d NS=%d epi=%d", L.S, L.NS, L.epi);
+}
+
+inline int tc_setup_convs(glassnet* net, const std::vector<const float*>& FW, const std::vector<const float*>& RW) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  const glassnet_dims& d = net->d;
+  const int L = d.levels;
+  const int* c = d.widths;
+  int rc = setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], d.height, d.width, net->x16, net->e[0], 0);
+  for (int l = 1; l < L && !rc; ++l)
+    rc = setup_conv(net, s->conv[l], 2, FW[l], net->convB[l], c[l - 1], c[l - 1], c[l], d.height >> (l - 1),
+                    d.width >> (l - 1), net->e[l - 1], net->e[l], 0);
+  for (int l = L - 1; l >= 1 && !rc; --l) {
+    void* in = (l == L - 1) ? net->e[L - 1] : net->dd[l];
+    rc = setup_conv(net, s->conv[4 + l], 1, RW[l], net->convB[4 + l], c[l], c[l], c[l - 1], d.height >> l,
+                    d.width >> l, in, l == 1 ? nullptr : net->y[l], l == 1 ? 1 : 0);
+  }
+  return rc;
+}
+
+inline int tc_launch_conv(glassnet* net, int idx, int B, cudaStream_t st) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  return launch_conv(net, s->conv[idx], B, st);
+}
+
 inline bool tc_supported(const glassnet_dims& d) {
   return (d.t_hidden == 32 || d.t_hidden == 64) && (d.widths[0] == 16 || d.widths[0] == 32);
 }
@@ -393,6 +543,7 @@ inline void tc_release(glassnet* net) {
   if (!s) return;
   if (s->tb_wimg) cudaFree(s->tb_wimg);
   if (s->tb_par) cudaFree(s->tb_par);
+  for (auto& c : s->conv) if (c.wimg) cudaFree(c.wimg);
   delete s;
   net->tc_state = nullptr;
 }
