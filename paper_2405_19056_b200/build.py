@@ -47,7 +47,7 @@ def build_lib(force=False, verbose=True):
     if not force and not _stale(LIB, deps):
         return LIB
     nccl = _nccl_dir()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if os.environ.get("GN_PTXAS_V") else "-O3",
            "-I", os.path.join(nccl, "include"), "-o", LIB, *srcs,
            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]

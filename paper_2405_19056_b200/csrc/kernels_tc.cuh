@@ -20,272 +20,11 @@
 #include <vector>
 
 #include "kernels_conv_tc.cuh"
+#include "kernels_tb_tc.cuh"
 #include "net.h"
 #include "tc_ptx.cuh"
 
 namespace gn {
-
-// ------------------------------------------------------------------------ T+B+psi
-template <int K, int H, int C0>
-struct TbLayout {
-  static constexpr int KA2 = H + 16;
-  static constexpr int W1_B = H * 16 * 2;
-  static constexpr int W2_B = H * KA2 * 2;
-  static constexpr int WBT_B = C0 * H * 2;
-  static constexpr int WBE_B = C0 * C0 * 2;
-  static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B;
-  static constexpr int NPAR = C0 + C0 + 3 * (C0 + 3) + 3;
-  static constexpr int OFF_W = 0;
-  static constexpr int OFF_W1 = OFF_W, OFF_W2 = OFF_W1 + W1_B, OFF_WBT = OFF_W2 + W2_B, OFF_WBE = OFF_WBT + WBT_B;
-  static constexpr int OFF_A1 = OFF_W + WIMG_B;
-  static constexpr int OFF_A2 = OFF_A1 + 128 * 16 * 2;
-  static constexpr int OFF_A3 = OFF_A2 + 128 * KA2 * 2;
-  static constexpr int OFF_AE = OFF_A3 + 128 * H * 2;
-  static constexpr int OFF_ST = OFF_AE + 128 * C0 * 2;
-  static constexpr int ST_B = ((128 * K * 22) + 15) / 16 * 16;
-  static constexpr int OFF_PAR = OFF_ST + ST_B;
-  static constexpr int OFF_BAR = (OFF_PAR + NPAR * 4 + 15) / 16 * 16;
-  static constexpr int SMEM = OFF_BAR + 16;
-  static constexpr int TMEM_COLS = (H + C0) <= 64 ? 64 : ((H + C0) <= 128 ? 128 : 256);
-};
-
-template <int K>
-__device__ __forceinline__ bool frag_less(const uint16_t* rec, int ia, int ib, uint64_t ka, uint64_t kb, int m) {
-  const bool va = ia < m, vb = ib < m;
-  if (va != vb) return va;
-  if (!va) return false;
-  if (ka != kb) return ka < kb;
-  const uint16_t* a = rec + ia * 11;
-  const uint16_t* b = rec + ib * 11;
-#pragma unroll 1
-  for (int c = 3; c < 11; ++c)
-    if (a[c] != b[c]) return a[c] < b[c];
-  return false;
-}
-
-template <int K, int H, int C0>
-__global__ void __launch_bounds__(128, 2)
-k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const uint16_t* __restrict__ e0,
-        const uint16_t* __restrict__ direct, const uint8_t* __restrict__ wimg, const float* __restrict__ params,
-        float* __restrict__ psi, long P, int pool, int r_takes_ld) {
-  using S = TbLayout<K, H, C0>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 8);
-  const int tid = threadIdx.x, warp = tid >> 5;
-
-  for (int i = tid; i < S::WIMG_B / 16; i += 128)
-    reinterpret_cast<int4*>(smem + S::OFF_W)[i] = reinterpret_cast<const int4*>(wimg)[i];
-  float* par = reinterpret_cast<float*>(smem + S::OFF_PAR);
-  for (int i = tid; i < S::NPAR; i += 128) par[i] = params[i];
-  if (tid == 0) { tc::mbar_init(mbar, 1); tc::fence_mbar_init(); }
-  if (warp == 0) tc::tmem_alloc<S::TMEM_COLS>(tptr);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tptr;
-  const uint32_t t_acc = tmem, t_accB = tmem + H;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  const float* bB = par;
-  const float* wBn = par + C0;
-  const int NO = C0 + 3;
-  const float* WO = par + 2 * C0;
-  const float* bO = WO + 3 * NO;
-
-  const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sA2 = tc::smem_u32(smem + S::OFF_A2);
-  const uint32_t sA3 = tc::smem_u32(smem + S::OFF_A3), sAE = tc::smem_u32(smem + S::OFF_AE);
-  const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
-  const uint32_t sWBT = tc::smem_u32(smem + S::OFF_WBT), sWBE = tc::smem_u32(smem + S::OFF_WBE);
-  constexpr uint32_t PL = 128 * 16;   // one K-plane of a 128-row A operand
-  constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
-  constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
-  constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
-  const uint16_t* st = reinterpret_cast<const uint16_t*>(smem + S::OFF_ST);
-  uint32_t phase = 0;
-  const long ntiles = (P + 127) / 128;
-
-  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long p0 = tile * 128;
-    const int np = (int)min((long)128, P - p0);
-    {  // stage the tile's records (coalesced 8-byte loads)
-      const uint2* src = reinterpret_cast<const uint2*>(tbuf + p0 * K * 11);
-      uint2* dst = reinterpret_cast<uint2*>(smem + S::OFF_ST);
-      const int nu = np * K * 22 / 8;
-      for (int i = tid; i < nu; i += 128) dst[i] = __ldg(src + i);
-    }
-    __syncthreads();
-    const int r = tid;
-    const long p = p0 + r;
-    const bool pv = r < np;
-    int m = pv ? (int)tcount[p] : 0;
-    m = m < K ? m : K;
-    const uint16_t* rec = st + r * K * 11;
-    // ---- canonical fragment order (R5): sort (validity, key64, rest) ----
-    uint64_t key[K];
-    int ix[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      ix[k] = k;
-      const uint16_t* q = rec + k * 11;
-      key[k] = k < m ? ((uint64_t)q[7] << 48) | ((uint64_t)q[0] << 32) | ((uint64_t)q[1] << 16) | (uint64_t)q[2]
-                     : ~0ull;
-    }
-#pragma unroll
-    for (int pass = 0; pass < K; ++pass) {
-#pragma unroll
-      for (int i = pass & 1; i + 1 < K; i += 2) {
-        if (frag_less<K>(rec, ix[i + 1], ix[i], key[i + 1], key[i], m)) {
-          uint64_t tk = key[i]; key[i] = key[i + 1]; key[i + 1] = tk;
-          int ti = ix[i]; ix[i] = ix[i + 1]; ix[i + 1] = ti;
-        }
-      }
-    }
-    // ---- operands that do not depend on the slot ----
-    if (pv) {
-      const uint4* e = reinterpret_cast<const uint4*>(e0 + p * C0);
-#pragma unroll
-      for (int j = 0; j < C0 / 8; ++j) {
-        uint4 v = __ldg(e + j);
-        tc::sts128(sAE + j * PL + r * 16, v.x, v.y, v.z, v.w);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < C0 / 8; ++j) tc::sts128(sAE + j * PL + r * 16, 0, 0, 0, 0);
-    }
-    float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;
-    if (pv) {
-      ld0 = __uint_as_float((uint32_t)direct[p * 3 + 0] << 16);
-      ld1 = __uint_as_float((uint32_t)direct[p * 3 + 1] << 16);
-      ld2 = __uint_as_float((uint32_t)direct[p * 3 + 2] << 16);
-    }
-    const float inv_m = (pool == 1 && m > 0) ? 1.f / (float)m : 1.f;
-    auto write_A1 = [&](int s) {
-      uint32_t w[8];
-      if (s < m) {
-        const uint16_t* q = rec + ix[s] * 11;
-        w[0] = q[0] | ((uint32_t)q[1] << 16);
-        w[1] = q[2] | ((uint32_t)q[3] << 16);
-        w[2] = q[4] | ((uint32_t)q[5] << 16);
-        w[3] = q[6] | ((uint32_t)q[7] << 16);
-        w[4] = q[8] | ((uint32_t)q[9] << 16);
-        w[5] = q[10] | (0x3F80u << 16);
-        w[6] = 0x3F80u | (0x3F80u << 16);
-        w[7] = 0;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = 0;
-      }
-      tc::sts128(sA1 + r * 16, w[0], w[1], w[2], w[3]);
-      tc::sts128(sA1 + PL + r * 16, w[4], w[5], w[6], w[7]);
-    };
-    write_A1(0);
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after_sync();
-#pragma unroll
-      for (int q = 0; q < C0 / 16; ++q)
-        tc::mma_f16_ss(t_accB, tc::smem_desc(sAE + 2 * q * PL, PL, 128),
-                       tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-      tc::mma_f16_ss(t_acc, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
-      tc::mma_commit(mbar);
-    }
-#pragma unroll 1
-    for (int s = 0; s < K; ++s) {
-      tc::mbar_wait(mbar, phase);
-      phase ^= 1;
-      tc::fence_after_sync();
-      // epilogue 1: a1 = ReLU(acc) -> bf16 -> A2 ; bias columns
-#pragma unroll
-      for (int c = 0; c < H / 16; ++c) {
-        uint32_t v[16];
-        tc::tmem_ld16(t_acc + lane_off + c * 16, v);
-        tc::tmem_ld_wait();
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = tc::cvt_relu_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-        tc::sts128(sA2 + (2 * c) * PL + r * 16, w[0], w[1], w[2], w[3]);
-        tc::sts128(sA2 + (2 * c + 1) * PL + r * 16, w[4], w[5], w[6], w[7]);
-      }
-      {
-        const uint32_t one = s < m ? 0x3F80u : 0u;
-        tc::sts128(sA2 + (H / 8) * PL + r * 16, one | (one << 16), one, 0, 0);
-        tc::sts128(sA2 + (H / 8 + 1) * PL + r * 16, 0, 0, 0, 0);
-      }
-      tc::fence_before_sync();
-      tc::fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after_sync();
-#pragma unroll
-        for (int q = 0; q < S::KA2 / 16; ++q)
-          tc::mma_f16_ss(t_acc, tc::smem_desc(sA2 + 2 * q * PL, PL, 128),
-                         tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
-        tc::mma_commit(mbar);
-      }
-      tc::mbar_wait(mbar, phase);
-      phase ^= 1;
-      tc::fence_after_sync();
-      // epilogue 2: a2 = ReLU(acc) (/n in mean mode) -> f16 -> A3
-#pragma unroll
-      for (int c = 0; c < H / 16; ++c) {
-        uint32_t v[16];
-        tc::tmem_ld16(t_acc + lane_off + c * 16, v);
-        tc::tmem_ld_wait();
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          w[i] = tc::cvt_relu_f16x2(__uint_as_float(v[2 * i]) * inv_m, __uint_as_float(v[2 * i + 1]) * inv_m);
-        tc::sts128(sA3 + (2 * c) * PL + r * 16, w[0], w[1], w[2], w[3]);
-        tc::sts128(sA3 + (2 * c + 1) * PL + r * 16, w[4], w[5], w[6], w[7]);
-      }
-      if (s + 1 < K) write_A1(s + 1);
-      tc::fence_before_sync();
-      tc::fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after_sync();
-#pragma unroll
-        for (int q = 0; q < H / 16; ++q)
-          tc::mma_f16_ss(t_accB, tc::smem_desc(sA3 + 2 * q * PL, PL, 128),
-                         tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
-        if (s + 1 < K)
-          tc::mma_f16_ss(t_acc, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
-        tc::mma_commit(mbar);
-      }
-    }
-    tc::mbar_wait(mbar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
-    // epilogue 3: phi = ReLU(accB + b_B + w_Bn m); psi = W_O phi + W_O,L L_d + b_O
-    float ps0 = bO[0], ps1 = bO[1], ps2 = bO[2];
-    if (r_takes_ld) {
-      ps0 = fmaf(WO[0 * NO + C0 + 0], ld0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], ld1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], ld2, ps0);
-      ps1 = fmaf(WO[1 * NO + C0 + 0], ld0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], ld1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], ld2, ps1);
-      ps2 = fmaf(WO[2 * NO + C0 + 0], ld0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], ld1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], ld2, ps2);
-    }
-    const float fm = (float)m;
-#pragma unroll
-    for (int c = 0; c < C0 / 16; ++c) {
-      uint32_t v[16];
-      tc::tmem_ld16(t_accB + lane_off + c * 16, v);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int o = c * 16 + i;
-        const float phi = relu(__uint_as_float(v[i]) + bB[o] + wBn[o] * fm);
-        ps0 = fmaf(WO[0 * NO + o], phi, ps0);
-        ps1 = fmaf(WO[1 * NO + o], phi, ps1);
-        ps2 = fmaf(WO[2 * NO + o], phi, ps2);
-      }
-    }
-    if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
-    tc::fence_before_sync();
-    __syncthreads();
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<S::TMEM_COLS>(tmem);
-}
 
 // ------------------------------------------------------------------------ host side
 struct TcConv {
@@ -556,7 +295,7 @@ static int launch_tb_tc_k(glassnet* net, const __nv_bfloat16* tbuf, const uint8_
   auto kfn = k_tb_tc<K, H, C0>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   const long ntiles = (P + 127) / 128;
-  long grid = 2L * net->num_sms;
+  long grid = (long)S::MINB * net->num_sms;
   if (grid > ntiles) grid = ntiles;
   kfn<<<(unsigned)grid, 128, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
