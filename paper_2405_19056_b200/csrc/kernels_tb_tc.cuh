@@ -3,46 +3,32 @@
 // PAPER.md Eq. eq:SymmetricNN: tau = sum_i h(b_i), h shared; B;
 // the psi projection is reading R15.  One CTA = one 128-pixel tile at a time,
 // thread r owns pixel r (= TMEM lane r = MMA row r).  Per tile:
-//   1. each thread loads its pixel's K records into registers and sorts the valid ones
-//      into the canonical order (reading R5: lexicographic on the storage bits) with a
-//      Batcher odd-even merge network; invalid slots become all-ones and sort last.
-//   2. per slot s (canonical order):
-//        A1 = [record_s | 1 1 1 | 0 0]                      (bf16, 128 x 16)
-//        acc = A1 W1ext^T          (bias b1 via the three 1-columns, split hi/mid/lo)
-//        A2 = [ReLU(acc) bf16 | 1 1 1 0..]                   (128 x (h+16))
-//        acc = A2 W2ext^T          (bias b2 likewise)
-//        A3 = ReLU(acc) (/n in mean mode)  f16               (128 x h)
-//        accB += A3 W_B,tau^T      -- g = sum is done by the tensor core's accumulation:
-//                                      W_B sum_s a2_s = sum_s W_B a2_s (linearity)
-//      accB starts as e0 W_B,e0^T.  Invalid slots are all-zero rows (bias columns too),
-//      so they add exactly 0; per-fragment activations never leave the SM.
+//   1. each thread loads its pixel's K records into registers and gives every valid
+//      record its rank in the canonical order (reading R5: lexicographic on the storage
+//      bits, slot index as the last tie-break, which only orders identical records); the
+//      record's A1 row [record | 1 1 1 | 0 0] is stored at that rank, masked slots get
+//      zero rows.  No data moves between registers: ranks are computed, rows scattered.
+//   2. software-pipelined slot rounds t = 0 .. Kt (Kt = the tile's largest valid count):
+//        epilogue 2 of slot t-1:  A3 = ReLU(acc2) (/n in mean mode) -> f16
+//        epilogue 1 of slot t:    A2 = [ReLU(acc1) -> bf16 | 1 1 1 0..] (1s only if valid)
+//        then one MMA batch:      accB += A3 W_B,tau^T   (slot t-1)
+//                                 acc2  = A2 W2ext^T      (slot t)
+//                                 acc1  = A1[t+1] W1ext^T (slot t+1)
+//      so each slot costs one MMA round trip.  accB starts as e0 W_B,e0^T; the pool
+//      g = sum is the tensor core's accumulation (W_B sum_s a2_s = sum_s W_B a2_s).
+//      Masked slots are all-zero rows (bias columns included) and contribute exactly 0;
+//      per-fragment activations never leave the SM.
 //   3. phi = ReLU(accB + b_B + w_Bn n);  psi = W_O,d0 phi + W_O,L L_d + b_O  -> HBM (fp32).
-// A1, A2, A3 and the e0 operand share one 20 KB shared-memory region (their lifetimes do
-// not overlap, see the comments at each write), so 4 CTAs (4 independent MMA chains)
-// fit on an SM.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
 namespace gn {
-
-// Batcher odd-even merge sort network for N = 2^p inputs (compile time).
-template <int N>
-struct SortNet {
-  int a[N * N], b[N * N];
-  int n;
-  constexpr SortNet() : a(), b(), n(0) {
-    for (int p = 1; p < N; p += p)
-      for (int k = p; k >= 1; k /= 2)
-        for (int j = k % p; j + k <= N - 1; j += 2 * k)
-          for (int i = 0; i <= (k - 1 < N - j - k - 1 ? k - 1 : N - j - k - 1); ++i)
-            if ((i + j) / (p * 2) == (i + j + k) / (p * 2)) { a[n] = i + j; b[n] = i + j + k; ++n; }
-  }
-};
-constexpr int pow2_ceil(int k) { return k <= 1 ? 1 : 2 * pow2_ceil((k + 1) / 2); }
 
 template <int K, int H, int C0>
 struct TbLayout {
@@ -54,58 +40,59 @@ struct TbLayout {
   static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B;
   static constexpr int NPAR = C0 + C0 + 3 * (C0 + 3) + 3;
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBT = OFF_W2 + W2_B, OFF_WBE = OFF_WBT + WBT_B;
-  static constexpr int PL = 128 * 16;          // one 8-column K-plane of a 128-row operand
-  static constexpr int OFF_OP = WIMG_B;        // operand region: KA2/8 planes
-  // planes of the operand region:  A2 = 0 .. KA2/8-1 ; A3 = 0 .. H/8-1 ; AE = 0 .. C0/8-1 ;
-  //                                A1 = the last two planes (H/8, H/8+1)  [>= C0/8 and >= H/8]
-  static constexpr int A1_PLANE = H / 8;
-  static constexpr int OFF_PAR = OFF_OP + (KA2 / 8) * PL;
-  static constexpr int OFF_BAR = (OFF_PAR + NPAR * 4 + 15) / 16 * 16;
-  static constexpr int SMEM = OFF_BAR + 16;
-  static constexpr int TMEM_COLS = (H + C0) <= 64 ? 64 : ((H + C0) <= 128 ? 128 : 256);
-  static constexpr int REC_B = K * 22;          // bytes of one pixel's records
+  static constexpr int PL = 128 * 16;                 // one 8-column K-plane of a 128-row operand
+  // one chain (= one warpgroup working on its own tile stream):
+  static constexpr int CH_A1 = 0;                     // K slots x 2 planes
+  static constexpr int CH_A2 = CH_A1 + K * 2 * PL;    // KA2/8 planes
+  static constexpr int CH_A3 = CH_A2 + (KA2 / 8) * PL;  // H/8 planes; the e0 operand aliases it
+  static constexpr int CH_B = CH_A3 + (H / 8) * PL;
+  static constexpr int OFF_PAR = WIMG_B;
+  static constexpr int OFF_BAR = (OFF_PAR + NPAR * 4 + 15) / 16 * 16;   // 4 mbarriers + tmem ptr
+  static constexpr int OFF_RED = OFF_BAR + 48;        // 4 chains x 4 ints: per-warp max count
+  static constexpr int OFF_CH = (OFF_RED + 64 + 1023) / 1024 * 1024;
+  static constexpr int TCOLS = (2 * H + C0 + 31) / 32 * 32;   // TMEM columns per chain
+  static constexpr int NCH_T = 512 / TCOLS;
+  static constexpr int NCH_S = (232448 - 1024 - OFF_CH) / CH_B;
+  static constexpr int NCH = NCH_T < NCH_S ? (NCH_T < 4 ? NCH_T : 4) : (NCH_S < 4 ? NCH_S : 4);
+  static constexpr int SMEM = OFF_CH + NCH * CH_B;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int REC_B = K * 22;                // bytes of one pixel's records
   static constexpr int VW = REC_B % 16 == 0 ? 16 : REC_B % 8 == 0 ? 8 : REC_B % 4 == 0 ? 4 : 2;
   static constexpr int NV = REC_B / VW;
-  static constexpr int MINB = K <= 8 ? 4 : 2;
 };
 
-struct Frag {                    // one record as the 6 words of an A1 row + its sort key
-  uint32_t w[6];                 // ch0|ch1, ch2|ch3, ch4|ch5, ch6|ch7, ch8|ch9, ch10|1.0
-  uint64_t key;                  // depth, ch0, ch1, ch2  (16 bits each)
-};
-
-__device__ __forceinline__ bool frag_lt(const Frag& x, const Frag& y) {
-  if (x.key != y.key) return x.key < y.key;
-#pragma unroll
-  for (int j = 1; j < 6; ++j)
-    if (x.w[j] != y.w[j]) return x.w[j] < y.w[j];
-  return false;
-}
-
-template <int K, int H, int C0>
-__global__ void __launch_bounds__(128, TbLayout<K, H, C0>::MINB)
+template <int K, int H, int C0, int POOL>
+__global__ void __launch_bounds__(128 * TbLayout<K, H, C0>::NCH, 1)
 k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const uint16_t* __restrict__ e0,
         const uint16_t* __restrict__ direct, const uint8_t* __restrict__ wimg, const float* __restrict__ params,
-        float* __restrict__ psi, long P, int pool, int r_takes_ld) {
+        float* __restrict__ psi, long P, int r_takes_ld) {
   using S = TbLayout<K, H, C0>;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 8);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  constexpr int NCH = S::NCH;
+  const int g = threadIdx.x >> 7;                    // chain (warpgroup) index
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + g;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 32);
+  int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 4 * g;
+  const int tid = threadIdx.x & 127, warp = tid >> 5, lane = tid & 31;
+  const int bar_id = 1 + g;                          // named barrier of this warpgroup
 
-  for (int i = tid; i < S::WIMG_B / 16; i += 128)
+  for (int i = threadIdx.x; i < S::WIMG_B / 16; i += blockDim.x)
     reinterpret_cast<int4*>(smem)[i] = reinterpret_cast<const int4*>(wimg)[i];
   float* par = reinterpret_cast<float*>(smem + S::OFF_PAR);
-  for (int i = tid; i < S::NPAR; i += 128) par[i] = params[i];
-  if (tid == 0) { tc::mbar_init(mbar, 1); tc::fence_mbar_init(); }
-  if (warp == 0) tc::tmem_alloc<S::TMEM_COLS>(tptr);
+  for (int i = threadIdx.x; i < S::NPAR; i += blockDim.x) par[i] = params[i];
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < NCH; ++c) tc::mbar_init(reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + c, 1);
+    tc::fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc<S::TMEM_COLS>(tptr);
   tc::fence_proxy_async();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tmem = *tptr;
-  const uint32_t t_acc = tmem, t_accB = tmem + H;
+  const uint32_t tmem = *tptr + g * S::TCOLS;
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const uint32_t t_acc1 = tmem, t_acc2 = tmem + H, t_accB = tmem + 2 * H;
+  uint8_t* chs = smem + S::OFF_CH + g * S::CH_B;
   const float* bB = par;
   const float* wBn = par + C0;
   constexpr int NO = C0 + 3;
@@ -113,27 +100,25 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
   const float* bO = WO + 3 * NO;
 
   constexpr uint32_t PL = S::PL;
-  const uint32_t sOP = tc::smem_u32(smem + S::OFF_OP);
-  const uint32_t sA1 = sOP + S::A1_PLANE * PL;
+  const uint32_t sA1 = tc::smem_u32(chs + S::CH_A1), sA2 = tc::smem_u32(chs + S::CH_A2);
+  const uint32_t sA3 = tc::smem_u32(chs + S::CH_A3);
   const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
   const uint32_t sWBT = tc::smem_u32(smem + S::OFF_WBT), sWBE = tc::smem_u32(smem + S::OFF_WBE);
   constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
   constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
   constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
-  constexpr int NP2 = pow2_ceil(K);
-  constexpr SortNet<NP2> NET{};
   uint32_t phase = 0;
   const long ntiles = (P + 127) / 128;
   const int r = tid;
 
-  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (long tile = (long)blockIdx.x * NCH + g; tile < ntiles; tile += (long)gridDim.x * NCH) {
     const long p = tile * 128 + r;
     const bool pv = p < P;
     int m = pv ? (int)__ldg(tcount + p) : 0;
     m = m < K ? m : K;
-    // ---- 1. records -> registers (this pixel's K*22 contiguous bytes) ----
-    uint16_t h[K * 11];
+    // ---- 1. records -> registers -> canonical rank -> A1 rows ----
     {
+      uint16_t h[K * 11];
       using V = typename std::conditional<S::VW == 16, uint4,
                 typename std::conditional<S::VW == 8, uint2,
                 typename std::conditional<S::VW == 4, uint32_t, uint16_t>::type>::type>::type;
@@ -147,32 +132,58 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
         for (int i = 0; i < S::NV; ++i) memset(&raw[i], 0, sizeof(V));
       }
       memcpy(h, raw, sizeof(h));
-    }
-    Frag f[K];
+      uint32_t w[K][6];
+      uint64_t key[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint16_t* q = h + k * 11;
-      if (k < m) {
-        f[k].w[0] = q[0] | ((uint32_t)q[1] << 16);
-        f[k].w[1] = q[2] | ((uint32_t)q[3] << 16);
-        f[k].w[2] = q[4] | ((uint32_t)q[5] << 16);
-        f[k].w[3] = q[6] | ((uint32_t)q[7] << 16);
-        f[k].w[4] = q[8] | ((uint32_t)q[9] << 16);
-        f[k].w[5] = q[10] | (0x3F80u << 16);
-        f[k].key = ((uint64_t)q[7] << 48) | ((uint64_t)q[0] << 32) | ((uint64_t)q[1] << 16) | (uint64_t)q[2];
-      } else {  // masked slot: any bits may be here (R4) -- replaced, never read
+      for (int k = 0; k < K; ++k) {
+        const uint16_t* q = h + k * 11;
+        w[k][0] = q[0] | ((uint32_t)q[1] << 16);
+        w[k][1] = q[2] | ((uint32_t)q[3] << 16);
+        w[k][2] = q[4] | ((uint32_t)q[5] << 16);
+        w[k][3] = q[6] | ((uint32_t)q[7] << 16);
+        w[k][4] = q[8] | ((uint32_t)q[9] << 16);
+        w[k][5] = q[10] | (0x3F80u << 16);
+        key[k] = ((uint64_t)q[7] << 48) | ((uint64_t)q[0] << 32) | ((uint64_t)q[1] << 16) | (uint64_t)q[2];
+      }
+      int rank[K];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) f[k].w[j] = 0xFFFFFFFFu;
-        f[k].key = ~0ull;
+      for (int k = 0; k < K; ++k) rank[k] = 0;
+#pragma unroll
+      for (int i = 1; i < K; ++i) {
+#pragma unroll
+        for (int j = 0; j < i; ++j) {
+          // is record j before record i?  (key, then remaining words, then slot index)
+          bool jf;
+          if (key[j] != key[i]) jf = key[j] < key[i];
+          else {
+            jf = true;
+#pragma unroll
+            for (int c = 1; c < 6; ++c)
+              if (w[j][c] != w[i][c]) { jf = w[j][c] < w[i][c]; break; }
+          }
+          if (i < m) {            // both valid (j < i < m); masked slots are never read
+            rank[i] += jf ? 1 : 0;
+            rank[j] += jf ? 0 : 1;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (k < m) {
+          const uint32_t dst = sA1 + rank[k] * 2 * PL + r * 16;
+          tc::sts128(dst, w[k][0], w[k][1], w[k][2], w[k][3]);
+          tc::sts128(dst + PL, w[k][4], w[k][5], 0x3F803F80u, 0);
+        } else {
+          const uint32_t dst = sA1 + k * 2 * PL + r * 16;
+          tc::sts128(dst, 0, 0, 0, 0);
+          tc::sts128(dst + PL, 0, 0, 0, 0);
+        }
       }
     }
-    // ---- canonical order: Batcher network, comparators touching padding skipped ----
-#pragma unroll
-    for (int c = 0; c < NET.n; ++c) {
-      const int ia = NET.a[c], ib = NET.b[c];
-      if (ib < K) {
-        if (frag_lt(f[ib], f[ia])) { Frag t = f[ia]; f[ia] = f[ib]; f[ib] = t; }
-      }
+    // the tile's largest count: slots no pixel uses are skipped (they would add 0)
+    {
+      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
+      if (lane == 0) red[warp] = wm;
     }
     float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;
     if (pv) {
@@ -180,103 +191,95 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
       ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
       ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
     }
-    const float inv_m = (pool == 1 && m > 0) ? 1.f / (float)m : 1.f;
-    // e0 operand -> planes 0..C0/8-1 (free: the previous tile's last MMA finished, we
-    // waited on its commit before its epilogue 3).
+    const float inv_m = (POOL == 1 && m > 0) ? 1.f / (float)m : 1.f;
+    // e0 operand in the A3 region (A3 is first written after the round-0 commit).
     if (pv) {
       const uint4* e = reinterpret_cast<const uint4*>(e0 + p * C0);
 #pragma unroll
       for (int j = 0; j < C0 / 8; ++j) {
         uint4 v = __ldg(e + j);
-        tc::sts128(sOP + j * PL + r * 16, v.x, v.y, v.z, v.w);
+        tc::sts128(sA3 + j * PL + r * 16, v.x, v.y, v.z, v.w);
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < C0 / 8; ++j) tc::sts128(sOP + j * PL + r * 16, 0, 0, 0, 0);
+      for (int j = 0; j < C0 / 8; ++j) tc::sts128(sA3 + j * PL + r * 16, 0, 0, 0, 0);
     }
-    auto write_A1 = [&](const Frag& g, bool valid) {
-      if (valid) {
-        tc::sts128(sA1 + r * 16, g.w[0], g.w[1], g.w[2], g.w[3]);
-        tc::sts128(sA1 + PL + r * 16, g.w[4], g.w[5], 0x3F803F80u, 0);
-      } else {
-        tc::sts128(sA1 + r * 16, 0, 0, 0, 0);
-        tc::sts128(sA1 + PL + r * 16, 0, 0, 0, 0);
-      }
-    };
-    write_A1(f[0], 0 < m);
     tc::fence_proxy_async();
-    __syncthreads();
+    tc::bar_sync(bar_id, 128);
+    const int Kt = max(max(red[0], red[1]), max(red[2], red[3]));
     if (tid == 0) {
       tc::fence_after_sync();
 #pragma unroll
       for (int q = 0; q < C0 / 16; ++q)
-        tc::mma_f16_ss(t_accB, tc::smem_desc(sOP + 2 * q * PL, PL, 128),
+        tc::mma_f16_ss(t_accB, tc::smem_desc(sA3 + 2 * q * PL, PL, 128),
                        tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-      tc::mma_f16_ss(t_acc, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
+      if (Kt > 0)
+        tc::mma_f16_ss(t_acc1, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
       tc::mma_commit(mbar);
     }
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
+#pragma unroll 1
+    for (int t = 0; t <= Kt; ++t) {
       tc::mbar_wait(mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
-      // epilogue 1 -> A2 (planes 0..KA2/8-1).  MMA1(s) and the e0 MMA are complete, and
-      // MMA3(s-1) was committed with MMA1(s): nothing reads the region any more.
+      if (t >= 1) {  // epilogue 2 of slot t-1 -> A3 (MMA3(t-2) and the e0 MMA are done)
 #pragma unroll
-      for (int c = 0; c < H / 16; ++c) {
-        uint32_t v[16];
-        tc::tmem_ld16(t_acc + lane_off + c * 16, v);
-        tc::tmem_ld_wait();
-        uint32_t w[8];
+        for (int c = 0; c < H / 32; ++c) {
+          uint32_t v[32];
+          tc::tmem_ld32(t_acc2 + lane_off + c * 32, v);
+          tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = tc::cvt_relu_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-        tc::sts128(sOP + (2 * c) * PL + r * 16, w[0], w[1], w[2], w[3]);
-        tc::sts128(sOP + (2 * c + 1) * PL + r * 16, w[4], w[5], w[6], w[7]);
+          for (int g = 0; g < 4; ++g) {
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float lo = __uint_as_float(v[8 * g + 2 * i]), hi = __uint_as_float(v[8 * g + 2 * i + 1]);
+              if (POOL == 1) { lo *= inv_m; hi *= inv_m; }
+              o[i] = tc::cvt_relu_f16x2(lo, hi);
+            }
+            tc::sts128(sA3 + (4 * c + g) * PL + r * 16, o[0], o[1], o[2], o[3]);
+          }
+        }
       }
-      {
-        const uint32_t one = s < m ? 0x3F80u : 0u;
-        tc::sts128(sOP + (H / 8) * PL + r * 16, one | (one << 16), one, 0, 0);
-        tc::sts128(sOP + (H / 8 + 1) * PL + r * 16, 0, 0, 0, 0);
+      if (t < Kt) {  // epilogue 1 of slot t -> A2 (MMA2(t-1) is done)
+#pragma unroll
+        for (int c = 0; c < H / 32; ++c) {
+          uint32_t v[32];
+          tc::tmem_ld32(t_acc1 + lane_off + c * 32, v);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = tc::cvt_relu_bf16x2(__uint_as_float(v[8 * g + 2 * i]), __uint_as_float(v[8 * g + 2 * i + 1]));
+            tc::sts128(sA2 + (4 * c + g) * PL + r * 16, o[0], o[1], o[2], o[3]);
+          }
+        }
+        const uint32_t one = t < m ? 0x3F80u : 0u;
+        tc::sts128(sA2 + (H / 8) * PL + r * 16, one | (one << 16), one, 0, 0);
+        tc::sts128(sA2 + (H / 8 + 1) * PL + r * 16, 0, 0, 0, 0);
       }
       tc::fence_before_sync();
       tc::fence_proxy_async();
-      __syncthreads();
+      tc::bar_sync(bar_id, 128);
       if (tid == 0) {
         tc::fence_after_sync();
+        if (t >= 1) {
 #pragma unroll
-        for (int q = 0; q < S::KA2 / 16; ++q)
-          tc::mma_f16_ss(t_acc, tc::smem_desc(sOP + 2 * q * PL, PL, 128),
-                         tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
-        tc::mma_commit(mbar);
-      }
-      tc::mbar_wait(mbar, phase);
-      phase ^= 1;
-      tc::fence_after_sync();
-      // epilogue 2 -> A3 (planes 0..H/8-1) and A1(s+1) (planes H/8, H/8+1): MMA2(s) done.
+          for (int q = 0; q < H / 16; ++q)
+            tc::mma_f16_ss(t_accB, tc::smem_desc(sA3 + 2 * q * PL, PL, 128),
+                           tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
+        }
+        if (t < Kt) {
 #pragma unroll
-      for (int c = 0; c < H / 16; ++c) {
-        uint32_t v[16];
-        tc::tmem_ld16(t_acc + lane_off + c * 16, v);
-        tc::tmem_ld_wait();
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          w[i] = tc::cvt_relu_f16x2(__uint_as_float(v[2 * i]) * inv_m, __uint_as_float(v[2 * i + 1]) * inv_m);
-        tc::sts128(sOP + (2 * c) * PL + r * 16, w[0], w[1], w[2], w[3]);
-        tc::sts128(sOP + (2 * c + 1) * PL + r * 16, w[4], w[5], w[6], w[7]);
-      }
-      if (s + 1 < K) write_A1(f[s + 1 < K ? s + 1 : 0], s + 1 < m);
-      tc::fence_before_sync();
-      tc::fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after_sync();
-#pragma unroll
-        for (int q = 0; q < H / 16; ++q)
-          tc::mma_f16_ss(t_accB, tc::smem_desc(sOP + 2 * q * PL, PL, 128),
-                         tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
-        if (s + 1 < K)
-          tc::mma_f16_ss(t_acc, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
+          for (int q = 0; q < S::KA2 / 16; ++q)
+            tc::mma_f16_ss(t_acc2, tc::smem_desc(sA2 + 2 * q * PL, PL, 128),
+                           tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
+        }
+        if (t + 1 < Kt)
+          tc::mma_f16_ss(t_acc1, tc::smem_desc(sA1 + (t + 1) * 2 * PL, PL, 128), tc::smem_desc(sW1, H * 16, 128),
+                         ID_T, 0);
         tc::mma_commit(mbar);
       }
     }
@@ -307,10 +310,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
     }
     if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
     tc::fence_before_sync();
-    __syncthreads();   // all epilogue-3 TMEM reads done before the next tile's MMAs
+    tc::bar_sync(bar_id, 128);   // TMEM reads and red[] of this tile done before the next tile
   }
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<S::TMEM_COLS>(tmem);
+  if (threadIdx.x < 32) tc::tmem_dealloc<S::TMEM_COLS>(*tptr);
 }
 
 }  // namespace gn

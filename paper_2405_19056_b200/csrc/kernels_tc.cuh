@@ -287,21 +287,28 @@ inline void tc_release(glassnet* net) {
   net->tc_state = nullptr;
 }
 
+template <int K, int H, int C0, int POOL>
+static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
+                           const __nv_bfloat16* direct, long P, cudaStream_t st) {
+  using S = TbLayout<K, H, C0>;
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  auto kfn = k_tb_tc<K, H, C0, POOL>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+  const long ntiles = (P + 127) / 128;
+  long grid = net->num_sms;
+  if (grid * S::NCH > ntiles) grid = (ntiles + S::NCH - 1) / S::NCH;
+  kfn<<<(unsigned)grid, 128 * S::NCH, S::SMEM, st>>>(
+      reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
+      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, net->psi, P,
+      (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0);
+  return 0;
+}
+
 template <int K, int H, int C0>
 static int launch_tb_tc_k(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
                           const __nv_bfloat16* direct, long P, cudaStream_t st) {
-  using S = TbLayout<K, H, C0>;
-  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
-  auto kfn = k_tb_tc<K, H, C0>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-  const long ntiles = (P + 127) / 128;
-  long grid = (long)S::MINB * net->num_sms;
-  if (grid > ntiles) grid = ntiles;
-  kfn<<<(unsigned)grid, 128, S::SMEM, st>>>(
-      reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
-      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, net->psi, P, net->d.pool,
-      (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0);
-  return 0;
+  if (net->d.pool == GLASSNET_POOL_MEAN) return launch_tb_tc_kp<K, H, C0, 1>(net, tbuf, tcount, e0, direct, P, st);
+  return launch_tb_tc_kp<K, H, C0, 0>(net, tbuf, tcount, e0, direct, P, st);
 }
 
 template <int H, int C0>
