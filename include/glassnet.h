@@ -141,6 +141,15 @@ int glassnet_forward_sharded(glassnet_t net, glassnet_comm_t comm, const void* g
                              const void* direct, const void* tbuf, const uint8_t* tcount,
                              float* out, glassnet_stream_t stream);
 
+/* Single-device emulation of the row-tile decomposition (tests and diagnostics): nets[r]
+ * is rank r's handle (all on one device, same dims), pointer arrays give each rank's tile.
+ * Runs exactly the per-rank steps of glassnet_forward_sharded, rank by rank, with the
+ * halo rows moved by device-to-device copies instead of NCCL. */
+int glassnet_forward_sharded_local(glassnet_t* nets, int32_t nranks, const void* const* gbuf,
+                                   const void* const* direct, const void* const* tbuf,
+                                   const uint8_t* const* tcount, float* const* out,
+                                   glassnet_stream_t stream);
+
 void glassnet_destroy(glassnet_t net);
 const char* glassnet_last_error(void);
 

@@ -205,6 +205,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   if (bf && gn::tc_supported(d)) {
     rc = gn::tc_pack_weights(net, T1W, T1b, T2W, T2b, FW, Fb, BW, Bb, RW, Rb, OW, Ob);
     if (!rc) rc = gn::tc_setup_convs(net, FW, RW);
+    if (!rc) rc = gn::tc_setup_full_geom(net);
     if (rc) { glassnet_destroy(net); return rc; }
   }
   net->tc = bf && gn::tc_supported(d);
@@ -246,12 +247,20 @@ extern "C" int glassnet_launches_per_forward(glassnet_t net, int32_t batch) {
   return 1 + L + 1 + 2 * (L - 2) + 1 + 1;
 }
 
-// ------------------------------------------------------------------------ forward (SIMT)
+// ------------------------------------------------------------------------ forward (SIMT family)
 static inline unsigned nblk(long n, int b) { return (unsigned)((n + b - 1) / b); }
+static const char* kConvNames[8] = {"conv_F0", "conv_F1", "conv_F2", "conv_F3", "", "conv_R1", "conv_R2", "conv_R3"};
+
+static gn::Up2Rows full_rows(int rows_f, int rows_c) {
+  gn::Up2Rows g;
+  g.rows_f = rows_f; g.rows_f_buf = rows_f; g.grow0_f = 0;
+  g.rows_c_buf = rows_c; g.grow0_c = 0; g.Hc_full = rows_c; g.halo = 0;
+  return g;
+}
 
 template <typename T>
-static int forward_chain(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
-                         float* out, int B, cudaStream_t st, bool tc) {
+static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
+                        float* out, int B, cudaStream_t st) {
   const glassnet_dims& d = net->d;
   const int L = d.levels, K = d.k_slots, h = d.t_hidden;
   const int* c = d.widths;
@@ -264,13 +273,7 @@ static int forward_chain(glassnet* net, const T* gbuf, const T* direct, const T*
   net->prof.mark(nullptr, st);
   gn::k_prep_x<T><<<nblk(P0, 256), 256, 0, st>>>(gbuf, direct, x16, P0, norm);
   net->prof.mark("prep_x", st);
-  static const char* conv_names[8] = {"conv_F0", "conv_F1", "conv_F2", "conv_F3", "", "conv_R1", "conv_R2", "conv_R3"};
   auto conv = [&](const T* in, int l_in, int cin, int wi, int cout, int stride, T* o, int epi) {
-    if (tc) {
-      gn::tc_launch_conv(net, wi, B, st);
-      net->prof.mark(conv_names[wi], st);
-      return;
-    }
     const int Ho = Hl[l_in] / stride, Wo = Wl[l_in] / stride;
     const long npix = (long)B * Ho * Wo;
     const int nj = cout >= 32 ? 32 : 16;
@@ -288,21 +291,13 @@ static int forward_chain(glassnet* net, const T* gbuf, const T* direct, const T*
       else
         gn::k_conv3x3_simt<T, 16, 1><<<grid, 128, 0, st>>>(in, Hl[l_in], Wl[l_in], cin, w, bb, cout, stride, nullptr, Ho, Wo, npix, net->wz, net->z);
     }
-    net->prof.mark(conv_names[wi], st);
+    net->prof.mark(kConvNames[wi], st);
   };
   T* e[4];
   for (int l = 0; l < L; ++l) e[l] = (T*)net->e[l];
   conv(x16, 0, 16, 0, c[0], 1, e[0], 0);
   for (int l = 1; l < L; ++l) conv(e[l - 1], l - 1, c[l - 1], l, c[l], 2, e[l], 0);
-  // T + B + psi
-  if (tc) {
-    if constexpr (sizeof(T) == 2) {
-      int trc = gn::tc_launch_tb(net, (const __nv_bfloat16*)tbuf, tcount, (const __nv_bfloat16*)e[0],
-                                 (const __nv_bfloat16*)direct, P0, st);
-      if (trc) return trc;
-      net->prof.mark("T_B_psi", st);
-    }
-  } else {
+  {  // T + B + psi
     const int NB = c[0] + h + 1, NO = c[0] + (ld ? 3 : 0);
     const size_t smem = sizeof(float) * (h * 11 + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3);
     const unsigned g = nblk(P0, 128);
@@ -328,13 +323,133 @@ static int forward_chain(glassnet* net, const T* gbuf, const T* direct, const T*
     conv(dcur, l, c[l], 4 + l, c[l - 1], 1, yl, 0);
     T* dn = (T*)net->dd[l - 1];
     const long nvec = (long)B * Hl[l - 1] * Wl[l - 1] * (c[l - 1] / 8);
-    gn::k_up2add<T><<<nblk(nvec, 256), 256, 0, st>>>(yl, Hl[l], Wl[l], e[l - 1], dn, Hl[l - 1], Wl[l - 1], c[l - 1], nvec);
+    gn::k_up2add<T><<<nblk(nvec, 256), 256, 0, st>>>(yl, Wl[l], e[l - 1], dn, Wl[l - 1], c[l - 1],
+                                                    full_rows(Hl[l - 1], Hl[l]), nvec);
     net->prof.mark("up2add", st);
     dcur = dn;
   }
   conv(dcur, 1, c[1], 4 + 1, c[0], 1, nullptr, 1);  // R_1 -> z (3 fp32 at level 1)
-  gn::k_output<<<nblk(P0, 256), 256, 0, st>>>(net->z, Hl[1], Wl[1], net->psi, out, Hl[0], Wl[0], P0);
+  gn::k_output<<<nblk(P0, 256), 256, 0, st>>>(net->z, Wl[1], net->psi, out, Wl[0], full_rows(Hl[0], Hl[1]), P0);
   net->prof.mark("output", st);
+  CUDA_TRY(cudaGetLastError());
+  return GLASSNET_OK;
+}
+
+// ------------------------------------------------------------------------ forward (tensor-core family)
+namespace gn {
+
+int tc_steps(const glassnet* net, Step* out, int max) {
+  const int L = net->d.levels;
+  int n = 0;
+  auto push = [&](int kind, int idx) { if (n < max) out[n] = Step{kind, idx}; ++n; };
+  push(ST_PREP, 0);
+  push(ST_EXCH, TEN_X);
+  push(ST_CONV, 0);
+  for (int l = 1; l < L; ++l) { push(ST_EXCH, TEN_E + l - 1); push(ST_CONV, l); }
+  push(ST_TB, 0);
+  push(ST_EXCH, TEN_E + L - 1);
+  push(ST_CONV, 4 + L - 1);
+  for (int l = L - 1; l >= 2; --l) {
+    push(ST_EXCH, TEN_Y + l);
+    push(ST_UP, l);
+    push(ST_EXCH, TEN_D + l - 1);
+    push(ST_CONV, 4 + l - 1);
+  }
+  push(ST_EXCH, TEN_Z);
+  push(ST_OUT, 0);
+  return n;
+}
+
+int tc_prepare_tile(glassnet* net, int nranks, int rank, int row0, int rows) {
+  return tc_setup_tile_geom(net, nranks, rank, row0, rows);
+}
+
+static Geom& geom_of(glassnet* net, bool tile) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  return tile ? *s->tile : s->full;
+}
+
+int tc_tensor_rows(glassnet* net, bool tile, int tensor, char** base, size_t* row_bytes, int* rows) {
+  Geom& G = geom_of(net, tile);
+  const int* c = net->d.widths;
+  int l = 0;
+  size_t ch = 0, es = 2;
+  void* p = nullptr;
+  if (tensor == TEN_X) { l = 0; ch = 16; p = G.x16; }
+  else if (tensor >= TEN_E && tensor < TEN_E + 4) { l = tensor - TEN_E; ch = c[l]; p = G.e[l]; }
+  else if (tensor >= TEN_Y && tensor < TEN_Y + 4) { l = tensor - TEN_Y; ch = c[l - 1]; p = G.y[l]; }
+  else if (tensor >= TEN_D && tensor < TEN_D + 4) { l = tensor - TEN_D; ch = c[l]; p = G.dd[l]; }
+  else if (tensor == TEN_Z) { l = 1; ch = 3; es = 4; p = G.z; }
+  if (!p) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "tensor %d has no buffer", tensor);
+  *base = reinterpret_cast<char*>(p);
+  *row_bytes = (size_t)G.W[l] * ch * es;
+  *rows = G.rows[l];
+  return 0;
+}
+
+int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, const void* direct, const void* tbuf,
+                const uint8_t* tcount, float* out, int B, cudaStream_t st) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  Geom& G = geom_of(net, tile);
+  const glassnet_dims& d = net->d;
+  const int* c = d.widths;
+  const int h = G.halo;
+  const long P0 = (long)B * G.rows[0] * G.W[0];
+  typedef __nv_bfloat16 bf;
+  switch (sp.kind) {
+    case ST_PREP: {
+      bf* x = (bf*)G.x16 + (size_t)h * G.W[0] * 16;
+      k_prep_x<bf><<<nblk(P0, 256), 256, 0, st>>>((const bf*)gbuf, (const bf*)direct, x, P0,
+                                                   (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
+      net->prof.mark("prep_x", st);
+      return 0;
+    }
+    case ST_CONV: {
+      int rc = launch_conv(net, s->conv[sp.idx], G.cg[sp.idx], B, st);
+      net->prof.mark(kConvNames[sp.idx], st);
+      return rc;
+    }
+    case ST_TB: {
+      const bf* e0 = (const bf*)G.e[0] + (size_t)h * G.W[0] * c[0];
+      int rc = tc_launch_tb(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, st);
+      net->prof.mark("T_B_psi", st);
+      return rc;
+    }
+    case ST_UP: {
+      const int l = sp.idx;
+      Up2Rows g;
+      g.rows_f = G.rows[l - 1]; g.rows_f_buf = G.rows[l - 1] + 2 * h; g.grow0_f = G.grow0[l - 1];
+      g.rows_c_buf = G.rows[l] + 2 * h; g.grow0_c = G.grow0[l]; g.Hc_full = G.Hfull[l]; g.halo = h;
+      const long nvec = (long)B * G.rows[l - 1] * G.W[l - 1] * (c[l - 1] / 8);
+      k_up2add<bf><<<nblk(nvec, 256), 256, 0, st>>>((const bf*)G.y[l], G.W[l], (const bf*)G.e[l - 1], (bf*)G.dd[l - 1],
+                                                     G.W[l - 1], c[l - 1], g, nvec);
+      net->prof.mark("up2add", st);
+      return 0;
+    }
+    case ST_OUT: {
+      Up2Rows g;
+      g.rows_f = G.rows[0]; g.rows_f_buf = G.rows[0] + 2 * h; g.grow0_f = G.grow0[0];
+      g.rows_c_buf = G.rows[1] + 2 * h; g.grow0_c = G.grow0[1]; g.Hc_full = G.Hfull[1]; g.halo = h;
+      k_output<<<nblk(P0, 256), 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g, P0);
+      net->prof.mark("output", st);
+      return 0;
+    }
+    default:
+      return 0;   // ST_EXCH: the caller's transport
+  }
+}
+
+}  // namespace gn
+
+static int forward_tc(glassnet* net, const void* gbuf, const void* direct, const void* tbuf, const uint8_t* tcount,
+                      float* out, int B, cudaStream_t st) {
+  gn::Step steps[64];
+  const int n = gn::tc_steps(net, steps, 64);
+  net->prof.mark(nullptr, st);
+  for (int i = 0; i < n; ++i) {
+    int rc = gn::tc_run_step(net, false, steps[i], gbuf, direct, tbuf, tcount, out, B, st);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaGetLastError());
   return GLASSNET_OK;
 }
@@ -358,10 +473,10 @@ extern "C" int glassnet_forward(glassnet_t net, const void* gbuf, const void* di
   CUDA_TRY(cudaSetDevice(net->dev));
   cudaStream_t st = (cudaStream_t)stream;
   if (net->d.precision == GLASSNET_FP32)
-    return forward_chain<float>(net, (const float*)gbuf, (const float*)direct, (const float*)tbuf, tcount, out, batch,
-                                st, false);
-  return forward_chain<__nv_bfloat16>(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
-                                      (const __nv_bfloat16*)tbuf, tcount, out, batch, st, net->tc);
+    return forward_simt<float>(net, (const float*)gbuf, (const float*)direct, (const float*)tbuf, tcount, out, batch, st);
+  if (net->tc) return forward_tc(net, gbuf, direct, tbuf, tcount, out, batch, st);
+  return forward_simt<__nv_bfloat16>(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct,
+                                     (const __nv_bfloat16*)tbuf, tcount, out, batch, st);
 }
 
 extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const void* direct, const void* tbuf,

@@ -62,6 +62,10 @@ struct ConvArgs {
   const float* wz;       // [3][Cout] (EPI 1)
   float* zout;           // [B][Ho][Wo][3] (EPI 1)
   int Cin, Cout, Ho, Wo, B, nsplit, nstage;
+  // row geometry (row tiles carry one halo row above/below; full frame: 0, 0, Ho)
+  int in_row_off;        // input buffer row of global-relative row 0
+  int out_row_off;       // output buffer row of output row 0
+  int out_rows_buf;      // output buffer rows per frame
 };
 
 template <int S, int NS, int EPI>
@@ -122,11 +126,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t dst = tc::smem_u32(sA + stage * SB);
           for (int j = 0; j < 2; ++j) {
             const int ch = (2 * c + j) * 8;
+            const int iy = S * oy - 1 + a.in_row_off;
             if (S == 1) {
-              tma_4d(dst + j * HL::PLANE, &tmA, ch, x0 - 1, oy - 1, b, full + stage);
+              tma_4d(dst + j * HL::PLANE, &tmA, ch, x0 - 1, iy, b, full + stage);
             } else {
-              tma_5d(dst + j * HL::PLANE, &tmA, ch, 0, x0, 2 * oy - 1, b, full + stage);
-              tma_5d(dst + j * HL::PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, 2 * oy - 1, b, full + stage);
+              tma_5d(dst + j * HL::PLANE, &tmA, ch, 0, x0, iy, b, full + stage);
+              tma_5d(dst + j * HL::PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, iy, b, full + stage);
             }
           }
           if (++stage == NST) { stage = 0; ph ^= 1; }
@@ -177,7 +182,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const int b = (int)(r / a.Ho);
       const int px = xt * TILE_M + m;
       const bool valid = px < a.Wo;
-      const long opix = ((long)b * a.Ho + oy) * a.Wo + px;
+      const long opix = ((long)b * a.out_rows_buf + oy + a.out_row_off) * a.Wo + px;
       tc::mbar_wait(tfull + acc, aph);
       tc::fence_after_sync();
       const uint32_t taddr = tmem + acc * NS + ((uint32_t)(q * 32) << 16);

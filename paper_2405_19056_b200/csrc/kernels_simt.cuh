@@ -229,27 +229,40 @@ __global__ void __launch_bounds__(128) k_tb_simt(
   psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2;
 }
 
+// Row geometry of an up2 step: the coarse input may be a row tile with halo rows.
+//   fine interior row Y (0..rows_f) is global row grow0_f + Y; its bilinear taps are
+//   clamped in GLOBAL coarse rows [0, Hc_full) and read from local buffer row
+//   (tap - grow0_c + halo).  Full frame: grow0 = 0, halo = 0, buffers = interior.
+struct Up2Rows {
+  int rows_f, rows_f_buf, grow0_f;   // fine level (skip, d, psi, out)
+  int rows_c_buf, grow0_c, Hc_full;  // coarse level (y or z)
+  int halo;
+};
+
 // d = up2(y) + skip (bilinear x2, half-pixel, edge clamp, cropped), 8 channels/thread.
 template <typename T>
-__global__ void k_up2add(const T* __restrict__ y, int h, int w, const T* __restrict__ skip,
-                         T* __restrict__ d, int H2, int W2, int C, long nvec) {
+__global__ void k_up2add(const T* __restrict__ y, int w, const T* __restrict__ skip, T* __restrict__ d, int W2,
+                         int C, Up2Rows g, long nvec) {
   long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nvec) return;
   const int cv = C / 8;
   const int c8 = (int)(t % cv) * 8;
   long r = t / cv;
   const int X = (int)(r % W2); r /= W2;
-  const int Y = (int)(r % H2);
-  const long b = r / H2;
+  const int Y = (int)(r % g.rows_f);
+  const long b = r / g.rows_f;
   int ya, yb, xa, xb; float wya, wyb, wxa, wxb;
-  up2_taps(Y, h, ya, yb, wya, wyb);
+  up2_taps(g.grow0_f + Y, g.Hc_full, ya, yb, wya, wyb);
+  ya += g.halo - g.grow0_c;
+  yb += g.halo - g.grow0_c;
   up2_taps(X, w, xa, xb, wxa, wxb);
+  const long yb0 = b * g.rows_c_buf;
   float v00[8], v01[8], v10[8], v11[8], sk[8], o[8];
-  load8(y + ((b * h + ya) * w + xa) * C + c8, v00);
-  load8(y + ((b * h + ya) * w + xb) * C + c8, v01);
-  load8(y + ((b * h + yb) * w + xa) * C + c8, v10);
-  load8(y + ((b * h + yb) * w + xb) * C + c8, v11);
-  const long q = ((b * H2 + Y) * W2 + X) * C + c8;
+  load8(y + ((yb0 + ya) * w + xa) * C + c8, v00);
+  load8(y + ((yb0 + ya) * w + xb) * C + c8, v01);
+  load8(y + ((yb0 + yb) * w + xa) * C + c8, v10);
+  load8(y + ((yb0 + yb) * w + xb) * C + c8, v11);
+  const long q = ((b * g.rows_f_buf + Y + g.halo) * W2 + X) * C + c8;
   load8(skip + q, sk);
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -259,21 +272,24 @@ __global__ void k_up2add(const T* __restrict__ y, int h, int w, const T* __restr
 
 // out = sigmoid(up2(z) + psi): the level-0 skip-add and output 1x1 rewritten with the
 // 3-channel projections (reading R15; exact in real arithmetic by linearity).
-__global__ void k_output(const float* __restrict__ z, int h, int w, const float* __restrict__ psi,
-                         float* __restrict__ out, int H, int W, long P) {
+__global__ void k_output(const float* __restrict__ z, int w, const float* __restrict__ psi,
+                         float* __restrict__ out, int W, Up2Rows g, long P) {
   long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const int X = (int)(p % W);
   long r = p / W;
-  const int Y = (int)(r % H);
-  const long b = r / H;
+  const int Y = (int)(r % g.rows_f);
+  const long b = r / g.rows_f;
   int ya, yb, xa, xb; float wya, wyb, wxa, wxb;
-  up2_taps(Y, h, ya, yb, wya, wyb);
+  up2_taps(g.grow0_f + Y, g.Hc_full, ya, yb, wya, wyb);
+  ya += g.halo - g.grow0_c;
+  yb += g.halo - g.grow0_c;
   up2_taps(X, w, xa, xb, wxa, wxb);
-  const float* z00 = z + ((b * h + ya) * w + xa) * 3;
-  const float* z01 = z + ((b * h + ya) * w + xb) * 3;
-  const float* z10 = z + ((b * h + yb) * w + xa) * 3;
-  const float* z11 = z + ((b * h + yb) * w + xb) * 3;
+  const long zb0 = b * g.rows_c_buf;
+  const float* z00 = z + ((zb0 + ya) * w + xa) * 3;
+  const float* z01 = z + ((zb0 + ya) * w + xb) * 3;
+  const float* z10 = z + ((zb0 + yb) * w + xa) * 3;
+  const float* z11 = z + ((zb0 + yb) * w + xb) * 3;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     float l = (wya * wxa) * z00[c] + (wya * wxb) * z01[c] + (wyb * wxa) * z10[c] + (wyb * wxb) * z11[c];

@@ -27,22 +27,44 @@
 namespace gn {
 
 // ------------------------------------------------------------------------ host side
+// Weights-level description of one conv layer (packed once per handle).
 struct TcConv {
   bool used = false;
   int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0;
-  int Hi = 0, Wi = 0, Ho = 0, Wo = 0;
   size_t smem = 0;
   int ctas_per_sm = 1;
-  CUtensorMap mA, mO;
   uint8_t* wimg = nullptr;
   const float* bias = nullptr;
+};
+
+// One conv layer in one execution geometry (buffers, row offsets, tensor maps).
+struct ConvGeom {
+  int Hi_buf = 0, Wi = 0, Ho = 0, Wo = 0, in_row_off = 0, out_row_off = 0, out_rows_buf = 0;
+  CUtensorMap mA, mO;
   uint16_t* out = nullptr;
+  float* zout = nullptr;
+};
+
+// An execution geometry: the full frame (halo = 0, batch up to max_batch) or one rank's
+// row tile of a single frame (halo = 1: every activation buffer carries one extra row
+// above and below its interior rows; at the frame's top/bottom these stay zero).
+struct Geom {
+  int halo = 0, L = 0, Bmax = 1;
+  int rows[4] = {}, W[4] = {}, grow0[4] = {}, Hfull[4] = {};
+  void *x16 = nullptr, *e[4] = {}, *y[4] = {}, *dd[4] = {};
+  float *psi = nullptr, *z = nullptr;
+  ConvGeom cg[8];                 // [l] = F_l, [4+l] = R_l
+  std::vector<void*> owned;       // buffers allocated for this geometry (tiles)
+  size_t bytes = 0;
 };
 
 struct TcState {
   uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
   float* tb_par = nullptr;      // bB, wBn, WO (c0+3 wide), bO
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
+  Geom full;                    // the handle's own workspace
+  Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
+  int tile_nranks = 0, tile_rank = -1;
 };
 
 static inline uint16_t h_bf16(float f) {
@@ -153,29 +175,29 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// Halo tensor maps over an NHWC bf16 activation [B][H][W][C] (zero fill out of bounds).
-static int make_halo_maps(TcConv& L, void* in, int B, int C) {
+// Halo tensor maps over an NHWC bf16 activation [B][Hbuf][W][C] (zero fill out of bounds).
+static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return gn_fail(GLASSNET_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r;
-  if (L.S == 1) {
-    const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)L.Wi, (cuuint64_t)L.Hi, (cuuint64_t)B};
-    const cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)L.Wi * C * 2, (cuuint64_t)L.Hi * L.Wi * C * 2};
+  if (S == 1) {
+    const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)G.Wi, (cuuint64_t)G.Hi_buf, (cuuint64_t)B};
+    const cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)G.Wi * C * 2, (cuuint64_t)G.Hi_buf * G.Wi * C * 2};
     const cuuint32_t box[4] = {8, conv::Halo<1>::SLOTS, 3, 1};
-    r = enc(&L.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    L.mO = L.mA;
+    G.mO = G.mA;
   } else {
-    const cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)L.Wi / 2, (cuuint64_t)L.Hi, (cuuint64_t)B};
-    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, (cuuint64_t)L.Wi * C * 2,
-                               (cuuint64_t)L.Hi * L.Wi * C * 2};
+    const cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)G.Wi / 2, (cuuint64_t)G.Hi_buf, (cuuint64_t)B};
+    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, (cuuint64_t)G.Wi * C * 2,
+                               (cuuint64_t)G.Hi_buf * G.Wi * C * 2};
     const cuuint32_t boxE[5] = {8, 1, conv::TILE_M, 3, 1};
     const cuuint32_t boxO[5] = {8, 1, conv::TILE_M + 1, 3, 1};
-    r = enc(&L.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS)
-      r = enc(&L.mO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxO, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      r = enc(&G.mO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxO, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (r != CUDA_SUCCESS) return gn_fail(GLASSNET_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -189,10 +211,9 @@ static size_t conv_smem(int S, int Cin, int NS, int nstage) {
 
 // One conv layer: choose the N split so the split's weights stay resident, pack them.
 static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const float* bias, int cin_real, int Cin,
-                      int Cout, int Hi, int Wi, void* in, void* out, int epi) {
+                      int Cout, int epi) {
   constexpr size_t LIMIT = 232448 - 1024;
   L.used = true; L.S = S; L.Cin = Cin; L.Cout = Cout; L.epi = epi;
-  L.Hi = Hi; L.Wi = Wi; L.Ho = Hi / S; L.Wo = Wi / S;
   int NS = Cout;
   while (NS > 16 && conv_smem(S, Cin, NS, 2) > LIMIT) NS /= 2;
   if (conv_smem(S, Cin, NS, 2) > LIMIT || (epi == 1 && NS != Cout))
@@ -223,32 +244,7 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
   cudaMemcpy(L.wimg, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
   net->w_bytes += img.size() * 2;
   L.bias = bias;
-  L.out = reinterpret_cast<uint16_t*>(out);
-  return make_halo_maps(L, in, net->d.max_batch, Cin);
-}
-
-template <int S, int NS, int EPI>
-static void launch_conv_k(glassnet* net, const TcConv& L, int B, cudaStream_t st) {
-  auto kfn = conv::k_conv_tc<S, NS, EPI>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-  conv::ConvArgs a;
-  a.wimg = L.wimg; a.bias = L.bias; a.out = L.out; a.wz = net->wz; a.zout = net->z;
-  a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = L.Ho; a.Wo = L.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
-  const long ntiles = (long)B * L.Ho * ((L.Wo + conv::TILE_M - 1) / conv::TILE_M);
-  long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
-  if (per_split > ntiles) per_split = ntiles;
-  if (per_split < 1) per_split = 1;
-  kfn<<<(unsigned)(per_split * L.nsplit), 192, L.smem, st>>>(L.mA, L.mO, a);
-}
-
-static int launch_conv(glassnet* net, const TcConv& L, int B, cudaStream_t st) {
-#define CONV_CASE(S_, NS_, E_) \
-  if (L.S == S_ && L.NS == NS_ && L.epi == E_) { launch_conv_k<S_, NS_, E_>(net, L, B, st); return 0; }
-  CONV_CASE(1, 16, 0) CONV_CASE(1, 32, 0) CONV_CASE(1, 64, 0) CONV_CASE(1, 128, 0) CONV_CASE(1, 256, 0)
-  CONV_CASE(2, 16, 0) CONV_CASE(2, 32, 0) CONV_CASE(2, 64, 0) CONV_CASE(2, 128, 0) CONV_CASE(2, 256, 0)
-  CONV_CASE(1, 16, 1) CONV_CASE(1, 32, 1)
-#undef CONV_CASE
-  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv variant S=%d NS=%d epi=%d", L.S, L.NS, L.epi);
+  return 0;
 }
 
 inline int tc_setup_convs(glassnet* net, const std::vector<const float*>& FW, const std::vector<const float*>& RW) {
@@ -256,21 +252,114 @@ inline int tc_setup_convs(glassnet* net, const std::vector<const float*>& FW, co
   const glassnet_dims& d = net->d;
   const int L = d.levels;
   const int* c = d.widths;
-  int rc = setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], d.height, d.width, net->x16, net->e[0], 0);
-  for (int l = 1; l < L && !rc; ++l)
-    rc = setup_conv(net, s->conv[l], 2, FW[l], net->convB[l], c[l - 1], c[l - 1], c[l], d.height >> (l - 1),
-                    d.width >> (l - 1), net->e[l - 1], net->e[l], 0);
-  for (int l = L - 1; l >= 1 && !rc; --l) {
-    void* in = (l == L - 1) ? net->e[L - 1] : net->dd[l];
-    rc = setup_conv(net, s->conv[4 + l], 1, RW[l], net->convB[4 + l], c[l], c[l], c[l - 1], d.height >> l,
-                    d.width >> l, in, l == 1 ? nullptr : net->y[l], l == 1 ? 1 : 0);
-  }
+  int rc = setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], 0);
+  for (int l = 1; l < L && !rc; ++l) rc = setup_conv(net, s->conv[l], 2, FW[l], net->convB[l], c[l - 1], c[l - 1], c[l], 0);
+  for (int l = L - 1; l >= 1 && !rc; --l)
+    rc = setup_conv(net, s->conv[4 + l], 1, RW[l], net->convB[4 + l], c[l], c[l], c[l - 1], l == 1 ? 1 : 0);
   return rc;
 }
 
-inline int tc_launch_conv(glassnet* net, int idx, int B, cudaStream_t st) {
+// Fill the per-layer conv geometry of G (buffers already set).
+static int geom_convs(glassnet* net, Geom& G) {
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
-  return launch_conv(net, s->conv[idx], B, st);
+  const int L = G.L, h = G.halo;
+  const int* c = net->d.widths;
+  auto set = [&](int idx, int lin, int S, void* in, int cin, int lout, void* out, float* zout) {
+    ConvGeom& g = G.cg[idx];
+    g.Hi_buf = G.rows[lin] + 2 * h; g.Wi = G.W[lin];
+    g.Ho = G.rows[lout]; g.Wo = G.W[lout];
+    g.in_row_off = h; g.out_row_off = h; g.out_rows_buf = G.rows[lout] + 2 * h;
+    g.out = reinterpret_cast<uint16_t*>(out);
+    g.zout = zout;
+    return make_halo_maps(S, g, in, G.Bmax, cin);
+  };
+  int rc = set(0, 0, 1, G.x16, 16, 0, G.e[0], nullptr);
+  for (int l = 1; l < L && !rc; ++l) rc = set(l, l - 1, 2, G.e[l - 1], c[l - 1], l, G.e[l], nullptr);
+  for (int l = L - 1; l >= 1 && !rc; --l) {
+    void* in = (l == L - 1) ? G.e[L - 1] : G.dd[l];
+    rc = set(4 + l, l, 1, in, c[l], l, l == 1 ? nullptr : G.y[l], l == 1 ? G.z : nullptr);
+  }
+  (void)s;
+  return rc;
+}
+
+// The handle's full-frame geometry over its own workspace.
+inline int tc_setup_full_geom(glassnet* net) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  Geom& G = s->full;
+  const glassnet_dims& d = net->d;
+  G.halo = 0; G.L = d.levels; G.Bmax = d.max_batch;
+  for (int l = 0; l < d.levels; ++l) {
+    G.rows[l] = d.height >> l; G.W[l] = d.width >> l; G.grow0[l] = 0; G.Hfull[l] = d.height >> l;
+    G.e[l] = net->e[l]; G.y[l] = net->y[l]; G.dd[l] = net->dd[l];
+  }
+  G.x16 = net->x16; G.psi = net->psi; G.z = net->z;
+  return geom_convs(net, G);
+}
+
+// Row-tile geometry for rank `rank` of `nranks` (one frame, halo rows, own buffers).
+inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int rows0) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  if (s->tile && s->tile_nranks == nranks && s->tile_rank == rank) return 0;
+  if (s->tile) { for (void* q : s->tile->owned) cudaFree(q); delete s->tile; s->tile = nullptr; }
+  const glassnet_dims& d = net->d;
+  const int L = d.levels;
+  const int* c = d.widths;
+  Geom* G = new Geom();
+  G->halo = 1; G->L = L; G->Bmax = 1;
+  for (int l = 0; l < L; ++l) {
+    G->rows[l] = rows0 >> l; G->W[l] = d.width >> l; G->grow0[l] = row0 >> l; G->Hfull[l] = d.height >> l;
+  }
+  auto alloc = [&](size_t bytes) -> void* {
+    void* q = nullptr;
+    if (cudaMalloc(&q, bytes) != cudaSuccess) return nullptr;
+    cudaMemset(q, 0, bytes);
+    G->owned.push_back(q);
+    G->bytes += bytes;
+    return q;
+  };
+  bool ok = (G->x16 = alloc((size_t)(G->rows[0] + 2) * G->W[0] * 16 * 2)) != nullptr;
+  for (int l = 0; l < L && ok; ++l) ok = (G->e[l] = alloc((size_t)(G->rows[l] + 2) * G->W[l] * c[l] * 2)) != nullptr;
+  for (int l = 2; l < L && ok; ++l) ok = (G->y[l] = alloc((size_t)(G->rows[l] + 2) * G->W[l] * c[l - 1] * 2)) != nullptr;
+  for (int l = 1; l < L - 1 && ok; ++l) ok = (G->dd[l] = alloc((size_t)(G->rows[l] + 2) * G->W[l] * c[l] * 2)) != nullptr;
+  if (ok) ok = (G->z = (float*)alloc((size_t)(G->rows[1] + 2) * G->W[1] * 3 * 4)) != nullptr;
+  if (ok) ok = (G->psi = (float*)alloc((size_t)G->rows[0] * G->W[0] * 3 * 4)) != nullptr;
+  if (!ok) {
+    for (void* q : G->owned) cudaFree(q);
+    delete G;
+    return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "row-tile workspace");
+  }
+  int rc = geom_convs(net, *G);
+  if (rc) { for (void* q : G->owned) cudaFree(q); delete G; return rc; }
+  s->tile = G;
+  s->tile_nranks = nranks;
+  s->tile_rank = rank;
+  return 0;
+}
+
+template <int S, int NS, int EPI>
+static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
+  auto kfn = conv::k_conv_tc<S, NS, EPI>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+  conv::ConvArgs a;
+  a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
+  a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
+  a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
+  const long ntiles = (long)B * G.Ho * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
+  long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
+  if (per_split > ntiles) per_split = ntiles;
+  if (per_split < 1) per_split = 1;
+  kfn<<<(unsigned)(per_split * L.nsplit), 192, L.smem, st>>>(G.mA, G.mO, a);
+}
+
+static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
+#define CONV_CASE(S_, NS_, E_) \
+  if (L.S == S_ && L.NS == NS_ && L.epi == E_) { launch_conv_k<S_, NS_, E_>(net, L, G, B, st); return 0; }
+  CONV_CASE(1, 16, 0) CONV_CASE(1, 32, 0) CONV_CASE(1, 64, 0) CONV_CASE(1, 128, 0) CONV_CASE(1, 256, 0)
+  CONV_CASE(2, 16, 0) CONV_CASE(2, 32, 0) CONV_CASE(2, 64, 0) CONV_CASE(2, 128, 0) CONV_CASE(2, 256, 0)
+  CONV_CASE(1, 16, 1) CONV_CASE(1, 32, 1)
+#undef CONV_CASE
+  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv variant S=%d NS=%d epi=%d", L.S, L.NS, L.epi);
 }
 
 inline bool tc_supported(const glassnet_dims& d) {
@@ -283,13 +372,14 @@ inline void tc_release(glassnet* net) {
   if (s->tb_wimg) cudaFree(s->tb_wimg);
   if (s->tb_par) cudaFree(s->tb_par);
   for (auto& c : s->conv) if (c.wimg) cudaFree(c.wimg);
+  if (s->tile) { for (void* q : s->tile->owned) cudaFree(q); delete s->tile; }
   delete s;
   net->tc_state = nullptr;
 }
 
 template <int K, int H, int C0, int POOL>
 static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
-                           const __nv_bfloat16* direct, long P, cudaStream_t st) {
+                           const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   using S = TbLayout<K, H, C0>;
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
   auto kfn = k_tb_tc<K, H, C0, POOL>;
@@ -299,23 +389,23 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   if (grid * S::NCH > ntiles) grid = (ntiles + S::NCH - 1) / S::NCH;
   kfn<<<(unsigned)grid, 128 * S::NCH, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
-      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, net->psi, P,
+      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, psi, P,
       (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0);
   return 0;
 }
 
 template <int K, int H, int C0>
 static int launch_tb_tc_k(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
-                          const __nv_bfloat16* direct, long P, cudaStream_t st) {
-  if (net->d.pool == GLASSNET_POOL_MEAN) return launch_tb_tc_kp<K, H, C0, 1>(net, tbuf, tcount, e0, direct, P, st);
-  return launch_tb_tc_kp<K, H, C0, 0>(net, tbuf, tcount, e0, direct, P, st);
+                          const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
+  if (net->d.pool == GLASSNET_POOL_MEAN) return launch_tb_tc_kp<K, H, C0, 1>(net, tbuf, tcount, e0, direct, psi, P, st);
+  return launch_tb_tc_kp<K, H, C0, 0>(net, tbuf, tcount, e0, direct, psi, P, st);
 }
 
 template <int H, int C0>
 static int launch_tb_tc_h(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
-                          const __nv_bfloat16* direct, long P, cudaStream_t st) {
+                          const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   switch (net->d.k_slots) {
-#define KCASE(k) case k: return launch_tb_tc_k<k, H, C0>(net, tbuf, tcount, e0, direct, P, st);
+#define KCASE(k) case k: return launch_tb_tc_k<k, H, C0>(net, tbuf, tcount, e0, direct, psi, P, st);
     KCASE(1) KCASE(2) KCASE(3) KCASE(4) KCASE(5) KCASE(6) KCASE(7) KCASE(8)
     KCASE(9) KCASE(10) KCASE(11) KCASE(12) KCASE(13) KCASE(14) KCASE(15) KCASE(16)
 #undef KCASE
@@ -324,12 +414,12 @@ static int launch_tb_tc_h(glassnet* net, const __nv_bfloat16* tbuf, const uint8_
 }
 
 inline int tc_launch_tb(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
-                        const __nv_bfloat16* direct, long P, cudaStream_t st) {
+                        const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   const int H = net->d.t_hidden, C0 = net->d.widths[0];
-  if (H == 64 && C0 == 32) return launch_tb_tc_h<64, 32>(net, tbuf, tcount, e0, direct, P, st);
-  if (H == 32 && C0 == 16) return launch_tb_tc_h<32, 16>(net, tbuf, tcount, e0, direct, P, st);
-  if (H == 32 && C0 == 32) return launch_tb_tc_h<32, 32>(net, tbuf, tcount, e0, direct, P, st);
-  if (H == 64 && C0 == 16) return launch_tb_tc_h<64, 16>(net, tbuf, tcount, e0, direct, P, st);
+  if (H == 64 && C0 == 32) return launch_tb_tc_h<64, 32>(net, tbuf, tcount, e0, direct, psi, P, st);
+  if (H == 32 && C0 == 16) return launch_tb_tc_h<32, 16>(net, tbuf, tcount, e0, direct, psi, P, st);
+  if (H == 32 && C0 == 32) return launch_tb_tc_h<32, 32>(net, tbuf, tcount, e0, direct, psi, P, st);
+  if (H == 64 && C0 == 16) return launch_tb_tc_h<64, 16>(net, tbuf, tcount, e0, direct, psi, P, st);
   return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core T kernel: (t_hidden, widths[0]) = (%d, %d)", H, C0);
 }
 

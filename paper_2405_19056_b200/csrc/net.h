@@ -31,6 +31,22 @@ struct StageProfiler {
   }
 };
 
+struct glassnet;
+namespace gn {
+// The tensor-core forward as a list of steps (glassnet.cu).  The full frame runs them
+// back to back; a row tile (forward_sharded, comm.cu) exchanges halo rows at EXCH steps.
+enum StepKind { ST_PREP = 0, ST_CONV = 1, ST_TB = 2, ST_UP = 3, ST_OUT = 4, ST_EXCH = 5 };
+enum TensorId { TEN_X = 0, TEN_E = 1, TEN_Y = 5, TEN_D = 9, TEN_Z = 13 };   // TEN_E + l, ...
+struct Step { int kind; int idx; };   // CONV: conv slot (l = F_l, 4+l = R_l); UP: level; EXCH: tensor
+int tc_steps(const struct ::glassnet* net, Step* out, int max);
+int tc_prepare_tile(struct ::glassnet* net, int nranks, int rank, int row0, int rows);
+int tc_run_step(struct ::glassnet* net, bool tile, const Step& s, const void* gbuf, const void* direct, const void* tbuf,
+                const uint8_t* tcount, float* out, int B, cudaStream_t st);
+// rows of a tensor in the geometry: buffer base, bytes per row, interior rows (halo rows
+// are at buffer rows 0 and rows+1)
+int tc_tensor_rows(struct ::glassnet* net, bool tile, int tensor, char** base, size_t* row_bytes, int* rows);
+}  // namespace gn
+
 struct glassnet {
   glassnet_dims d{};
   int dev = 0;

@@ -24,7 +24,8 @@ EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glas
            "glassnet_workspace_bytes", "glassnet_weight_bytes", "glassnet_launches_per_forward",
            "glassnet_set_kernel_family", "glassnet_get_unique_id", "glassnet_comm_create",
            "glassnet_comm_destroy", "glassnet_tile_rows", "glassnet_forward_sharded",
-           "glassnet_destroy", "glassnet_last_error", "glassnet_profile_begin", "glassnet_profile_end"]
+           "glassnet_destroy", "glassnet_last_error", "glassnet_profile_begin", "glassnet_profile_end",
+           "glassnet_forward_sharded_local"]
 
 
 class GlassNetError(RuntimeError):
@@ -80,6 +81,8 @@ def lib():
         L.glassnet_profile_begin.argtypes = [vp, i32]
         L.glassnet_profile_end.restype = ctypes.c_int
         L.glassnet_profile_end.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.glassnet_forward_sharded_local.restype = ctypes.c_int
+        L.glassnet_forward_sharded_local.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
         L.glassnet_destroy.restype = None
         L.glassnet_destroy.argtypes = [vp]
         L.glassnet_last_error.restype = ctypes.c_char_p
@@ -209,6 +212,15 @@ class GlassNet:
             self.close()
         except Exception:
             pass
+
+
+def forward_sharded_local(nets, tiles, stream=None):
+    """Row-tile decomposition of one frame emulated on one device: nets[r] = rank r's
+    handle, tiles[r] = (gbuf, direct, tbuf, tcount, out) device tensors of rank r's rows."""
+    n = len(nets)
+    arr = lambda i: (ctypes.c_void_p * n)(*[tiles[r][i].data_ptr() for r in range(n)])
+    hs = (ctypes.c_void_p * n)(*[net._h.value for net in nets])
+    _check(lib().glassnet_forward_sharded_local(hs, n, arr(0), arr(1), arr(2), arr(3), arr(4), _stream(stream)))
 
 
 def get_unique_id() -> bytes:
