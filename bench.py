@@ -165,17 +165,31 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[args.config]
-    B = cfg.batch
+    tiles_mode = args.config == "c4"        # configs[4]: ONE frame split in row tiles (strong scaling)
+    B = 1 if tiles_mode else cfg.batch
     H, W, K = cfg.height, cfg.width, cfg.k_slots
     w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True)
-    net = GlassNet(w, make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, precision=cfg.precision,
-                                max_batch=B, pool=cfg.pool))
+    dims = make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, precision=cfg.precision, max_batch=B,
+                     pool=cfg.pool)
+    net = GlassNet(w, dims)
     net.set_kernel_family(args.family == "tc")
-    # inputs resident in HBM: this rank's own 32 frames (weak scaling)
-    g, d, t, n = sdev.alloc_and_fill(cfg, nframes=B, seed=1, frame0=rank * B)
-    out = torch.empty((B, H, W, 3), dtype=torch.float32, device="cuda")
-    mean_n = float(n.float().mean().item())
     stream = torch.cuda.current_stream()
+    if tiles_mode:
+        from paper_2405_19056_b200 import glassnet as gb
+        r0, rows = gb.tile_rows(dims, world, rank)
+        g, d, t, n = sdev.alloc_and_fill(cfg, nframes=1, seed=1, rows=(r0, r0 + rows))
+        out = torch.empty((1, rows, W, 3), dtype=torch.float32, device="cuda")
+        uid = [gb.get_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        comm = gb.Comm(uid[0], world, rank)
+        run = lambda: net.forward_sharded(comm, g, d, t, n, out)
+    else:
+        # inputs resident in HBM: this rank's own 32 frames (weak scaling)
+        g, d, t, n = sdev.alloc_and_fill(cfg, nframes=B, seed=1, frame0=rank * B)
+        out = torch.empty((B, H, W, 3), dtype=torch.float32, device="cuda")
+        run = lambda: net.forward(g, d, t, n, out)
+    mean_n = float(n.float().mean().item())
 
     def barrier():
         if world > 1:
@@ -183,14 +197,14 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        net.forward(g, d, t, n, out)
+        run()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            net.forward(g, d, t, n, out)
+            run()
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -198,16 +212,19 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = float(tmax.item())
-    value = world * B * args.steps / (ms / 1000.0)
+    frames_per_step = 1 if tiles_mode else world * B
+    value = frames_per_step * args.steps / (ms / 1000.0)
 
     # per-stage times (events after every launch, same stream; a second pass of K steps)
     launches = net.launches_per_forward(B)
     net.profile_begin(launches * args.steps + 2)
     for _ in range(args.steps):
-        net.forward(g, d, t, n, out)
+        run()
     stages = net.profile_end()
     torch.cuda.synchronize()
     flops = alg_flops_per_frame(cfg, mean_n)
+    if tiles_mode:   # this rank's share of the frame
+        flops = {k: v * rows / H for k, v in flops.items()}
     step_ms = sum(v[0] for v in stages.values()) / args.steps
     # dominant kernel
     top = max(stages.items(), key=lambda kv: kv[1][0])
@@ -217,11 +234,18 @@ def run_ours(args):
     peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
     stage_flops = {"T_B_psi": flops["T"] + flops["B"], "conv_F0": flops["F0"], "conv_F1": flops["F1"],
                    "conv_F2": flops["F2"], "conv_F3": flops["F3"], "conv_R3": flops["R3"], "conv_R2": flops["R2"],
-                   "conv_R1": flops["R1"] + 2 * (cfg.height * cfg.width // 4) * cfg.widths[0] * 3}
+                   "conv_R1": flops["R1"]}
+    traffic = None   # dram bytes read+write per launch of that kernel from the committed ncu capture
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        if tj.get("config") == cfg.name and top_name in tj.get("kernels", {}):
+            traffic = tj["kernels"][top_name]
     if top_name in stage_flops:
         achieved = stage_flops[top_name] * B / (top_ms / top_cnt / 1000.0) / 1e12
         roof = {"kernel": top_name, "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved / peak_tf, "traffic": None,
+                "frac": achieved / peak_tf, "traffic": traffic,
+                "alg_flops_per_launch": stage_flops[top_name] * B, "launch_ms": top_ms / top_cnt,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
     else:
         roof = {"kernel": top_name, "bound": "hbm", "achieved": None, "peak": peaks.get("hbm_gbs"),
@@ -235,7 +259,7 @@ def run_ours(args):
 
     # end to end: public C-ABI call with pinned HOST buffers (H2D + forward + D2H inside)
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not tiles_mode:
         hg, hd, ht, hn = (x.cpu().pin_memory() for x in (g, d, t, n))
         hout = torch.empty(out.shape, dtype=torch.float32).pin_memory()
         net.forward_host(hg, hd, ht, hn, hout)
@@ -256,18 +280,29 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s, frac = cpu_oracle_band(cfg, (0, 272))
+        band = (0, 272) if not tiles_mode else (0, 64)
+        s, frac = cpu_oracle_band(cfg, band)
         cpu = {"value": frac / s, "unit": "frames/s", "cores": 1, "kind": "oracle",
-               "sample": f"frame 0 rows [0,272) of 1080 ({frac * 100:.1f}% of one 1920x1080 K=8 frame), "
+               "sample": f"frame 0 rows [{band[0]},{band[1]}) of {H} ({frac * 100:.1f}% of one {W}x{H} K={K} frame), "
                          f"fp64 C oracle single-threaded, {s:.1f} s; value = fraction/time"}
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        if tiles_mode:
+            cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, one frame in {world} row tiles, n~U{{0..{K}}}",
+                    "global_batch": 1, "parallelism": f"row tiles x{world} (NCCL send/recv halos)",
+                    "kernel_family": args.family, "l2": "inputs (2.9 GB) larger than L2; no flush",
+                    "mean_valid_fragments": mean_n}
+            metric = f"GlassNet frames/sec at 3840x2160 K=16 (configs[4], one frame row-tiled over {world} GPU)"
+        else:
+            cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, {B} frames per GPU, n~U{{0..{K}}}",
+                    "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world} (frames)",
+                    "kernel_family": args.family, "l2": "inputs (13.7 GB/rank) larger than L2; no flush",
+                    "mean_valid_fragments": mean_n}
+            metric = METRIC
+        line = {"metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": f"{cfg.name}: {W}x{H}, K={K}, {B} frames per GPU, n~U{{0..{K}}}",
-                           "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world} (frames)",
-                           "kernel_family": args.family, "l2": "inputs (13.7 GB/rank) larger than L2; no flush",
-                           "mean_valid_fragments": mean_n},
+                "scaling": "strong" if tiles_mode else "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded generator, synth/)",
+                "config": cfgj,
                 "roofline": roof, "whole_step": whole, "stages": stage_report,
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": launches * args.steps}
