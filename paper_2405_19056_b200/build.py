@@ -49,12 +49,26 @@ def build_lib(force=False, verbose=True):
     nccl = _nccl_dir()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if os.environ.get("GN_PTXAS_V") else "-O3",
+           *os.environ.get("GN_EXTRA_NVCC", "").split(),
            "-I", os.path.join(nccl, "include"), "-o", LIB, *srcs,
            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     return LIB
+
+
+def build_profile_lib(verbose=True):
+    """Diagnostic variant with the T kernel's clock64 phase counters (-DGN_PROFILE_TB)."""
+    global LIB
+    keep = LIB
+    LIB = os.path.join(PKG, "libglassnet_prof.so")
+    try:
+        os.environ["GN_EXTRA_NVCC"] = "-DGN_PROFILE_TB"
+        return build_lib(force=True, verbose=verbose)
+    finally:
+        os.environ.pop("GN_EXTRA_NVCC", None)
+        LIB = keep
 
 
 def build_synth(force=False, verbose=True):

@@ -567,3 +567,15 @@ extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int
   *rows = (int32_t)((b - a) * u);
   return GLASSNET_OK;
 }
+
+#ifdef GN_PROFILE_TB
+extern "C" int glassnet_debug_tb_prof(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, gn::gn_tb_prof, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(gn::gn_tb_prof, z, sizeof z);
+  }
+  return 0;
+}
+#endif

@@ -30,6 +30,17 @@
 
 namespace gn {
 
+#ifdef GN_PROFILE_TB
+// clock64 breakdown of chain 0 of CTA 0 (diagnostic build only)
+__device__ unsigned long long gn_tb_prof[16];
+#define TBP_NOW(v) const long long v = clock64()
+#define TBP_ADD(i, a, b) \
+  if (threadIdx.x == 0 && blockIdx.x == 0) gn_tb_prof[i] += (unsigned long long)((b) - (a))
+#else
+#define TBP_NOW(v)
+#define TBP_ADD(i, a, b)
+#endif
+
 template <int K, int H, int C0>
 struct TbLayout {
   static constexpr int KA2 = H + 16;
@@ -45,11 +56,17 @@ struct TbLayout {
   static constexpr int CH_A1 = 0;                     // K slots x 2 planes
   static constexpr int CH_A2 = CH_A1 + K * 2 * PL;    // KA2/8 planes
   static constexpr int CH_A3 = CH_A2 + (KA2 / 8) * PL;  // H/8 planes; the e0 operand aliases it
+  static constexpr int SBT = 4;                       // tiles per superblock (pixels sorted by count)
+  // superblock sort scratch (perm: SBT*128 u16, wsum: 4 warps x (K+2) ints) lives in the
+  // A2 region, which is free while a superblock is sorted
+  static constexpr int CH_PERM = CH_A2;
+  static constexpr int CH_SCAN = CH_PERM + SBT * 128 * 2;
+  static_assert(SBT * 128 * 2 + 4 * (K + 2) * 4 <= (KA2 / 8) * PL, "sort scratch must fit A2");
   static constexpr int CH_B = CH_A3 + (H / 8) * PL;
   static constexpr int OFF_PAR = WIMG_B;
   static constexpr int OFF_BAR = (OFF_PAR + NPAR * 4 + 15) / 16 * 16;   // 4 mbarriers + tmem ptr
-  static constexpr int OFF_RED = OFF_BAR + 48;        // 4 chains x 4 ints: per-warp max count
-  static constexpr int OFF_CH = (OFF_RED + 64 + 1023) / 1024 * 1024;
+  static constexpr int OFF_RED = OFF_BAR + 48;        // 4 chains x 8 ints: per-warp max count, superblock ids
+  static constexpr int OFF_CH = (OFF_RED + 128 + 127) / 128 * 128;
   static constexpr int TCOLS = (2 * H + C0 + 31) / 32 * 32;   // TMEM columns per chain
   static constexpr int NCH_T = 512 / TCOLS;
   static constexpr int NCH_S = (232448 - 1024 - OFF_CH) / CH_B;
@@ -59,20 +76,21 @@ struct TbLayout {
   static constexpr int REC_B = K * 22;                // bytes of one pixel's records
   static constexpr int VW = REC_B % 16 == 0 ? 16 : REC_B % 8 == 0 ? 8 : REC_B % 4 == 0 ? 4 : 2;
   static constexpr int NV = REC_B / VW;
+  static constexpr bool PREFETCH = K <= 8;            // register budget of the next tile's records
 };
 
 template <int K, int H, int C0, int POOL>
 __global__ void __launch_bounds__(128 * TbLayout<K, H, C0>::NCH, 1)
 k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const uint16_t* __restrict__ e0,
         const uint16_t* __restrict__ direct, const uint8_t* __restrict__ wimg, const float* __restrict__ params,
-        float* __restrict__ psi, long P, int r_takes_ld) {
+        float* __restrict__ psi, long P, int r_takes_ld, int* __restrict__ sched) {
   using S = TbLayout<K, H, C0>;
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int NCH = S::NCH;
   const int g = threadIdx.x >> 7;                    // chain (warpgroup) index
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + g;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 32);
-  int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 4 * g;
+  int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 8 * g;
   const int tid = threadIdx.x & 127, warp = tid >> 5, lane = tid & 31;
   const int bar_id = 1 + g;                          // named barrier of this warpgroup
 
@@ -108,43 +126,154 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
   constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
   constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
   uint32_t phase = 0;
-  const long ntiles = (P + 127) / 128;
   const int r = tid;
+  constexpr int SBT = S::SBT, SBP = SBT * 128;
+  uint16_t* perm = reinterpret_cast<uint16_t*>(chs + S::CH_PERM);
+  int* wsum = reinterpret_cast<int*>(chs + S::CH_SCAN);     // [warp][bin]
+  const long nsb = (P + SBP - 1) / SBP;
+  using V = typename std::conditional<S::VW == 16, uint4,
+            typename std::conditional<S::VW == 8, uint2,
+            typename std::conditional<S::VW == 4, uint32_t, uint16_t>::type>::type>::type;
+  auto load_records = [&](V* dst, long pp, bool ok) {   // the pixel's K*22 contiguous bytes
+    if (ok) {
+      const V* src = reinterpret_cast<const V*>(tbuf + pp * (K * 11));
+#pragma unroll
+      for (int i = 0; i < S::NV; ++i) dst[i] = __ldg(src + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < S::NV; ++i) memset(&dst[i], 0, sizeof(V));
+    }
+  };
 
-  for (long tile = (long)blockIdx.x * NCH + g; tile < ntiles; tile += (long)gridDim.x * NCH) {
-    const long p = tile * 128 + r;
+  // Superblocks of SBT tiles: the superblock's pixels are stably sorted by their valid
+  // count (bins 0..K, absent pixels last) so that each 128-row tile runs only as many slot
+  // rounds as its own largest count.  Per-pixel results do not depend on the row a pixel
+  // lands in (each MMA row is an independent dot product), so this is a pure schedule.
+  // Superblocks are handed out dynamically (global counter, zeroed before the launch); the
+  // next one is claimed one ahead so its inputs can be staged into L2 meanwhile.
+  volatile int* sbn = red + 4;
+  if (tid == 0) sbn[0] = atomicAdd(sched, 1);
+  tc::bar_sync(bar_id, 128);
+  long sb = sbn[0];
+  for (int it = 0; sb < nsb; ++it) {
+    const long q0 = sb * SBP;
+    TBP_NOW(tp_sb0);
+    if (tid == 0) {   // claim the next superblock and stage its inputs into L2
+      const int nx = atomicAdd(sched, 1);
+      sbn[(it + 1) & 1] = nx;
+      const long q1 = (long)nx * SBP;
+      if (q1 < P) {
+        const long np = min((long)SBP, P - q1);
+        const uint32_t rb = (uint32_t)(np * K * 22) & ~15u, eb = (uint32_t)(np * C0 * 2) & ~15u;
+        if (rb) tc::bulk_prefetch_l2(tbuf + q1 * K * 11, rb);
+        if (eb) tc::bulk_prefetch_l2(e0 + q1 * C0, eb);
+        const uint32_t db = (uint32_t)(np * 6) & ~15u, cb = (uint32_t)np & ~15u;
+        if (db && ((q1 * 6) & 15) == 0) tc::bulk_prefetch_l2(direct + q1 * 3, db);
+        if (cb) tc::bulk_prefetch_l2(tcount + q1, cb);
+      }
+    }
+    int mj[SBT];
+#pragma unroll
+    for (int j = 0; j < SBT; ++j) {
+      const long q = q0 + j * 128 + r;
+      mj[j] = q < P ? min((int)__ldg(tcount + q), K) : K + 1;
+    }
+    int cnt[K + 2], incl[K + 2];
+#pragma unroll
+    for (int b = 0; b < K + 2; ++b) {
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < SBT; ++j) c += mj[j] == b ? 1 : 0;
+      cnt[b] = c;
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+      }
+      incl[b] = x;
+      if (lane == 31) wsum[warp * (K + 2) + b] = x;
+    }
+    tc::bar_sync(bar_id, 128);
+    {
+      int base = 0;
+#pragma unroll
+      for (int b = 0; b < K + 2; ++b) {
+        int woff = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int v = wsum[w * (K + 2) + b];
+          woff += w < warp ? v : 0;
+          tot += v;
+        }
+        int pos = base + woff + incl[b] - cnt[b];
+#pragma unroll
+        for (int j = 0; j < SBT; ++j)
+          if (mj[j] == b) perm[pos++] = (uint16_t)((j * 128 + r) | (b << 11));   // row | count
+        base += tot;
+      }
+    }
+    tc::bar_sync(bar_id, 128);
+    int pe_all[SBT];   // this thread's row of every tile of the superblock (row | count << 11)
+#pragma unroll
+    for (int v = 0; v < SBT; ++v) pe_all[v] = perm[v * 128 + r];
+    TBP_NOW(tp_sb1);
+    TBP_ADD(0, tp_sb0, tp_sb1);
+  V nraw[S::NV];   // the next tile's records, loaded while this tile's MMAs run
+  for (int v = 0; v < SBT; ++v) {
+    TBP_NOW(tp_t0);
+    int pe = pe_all[0];
+#pragma unroll
+    for (int u = 1; u < SBT; ++u) pe = v == u ? pe_all[u] : pe;
+    const long p = q0 + (pe & 2047);
     const bool pv = p < P;
-    int m = pv ? (int)__ldg(tcount + p) : 0;
-    m = m < K ? m : K;
+    const int m = pv ? (pe >> 11) : 0;   // min(tcount, K), read once by the superblock sort
     // ---- 1. records -> registers -> canonical rank -> A1 rows ----
     {
-      uint16_t h[K * 11];
-      using V = typename std::conditional<S::VW == 16, uint4,
-                typename std::conditional<S::VW == 8, uint2,
-                typename std::conditional<S::VW == 4, uint32_t, uint16_t>::type>::type>::type;
       V raw[S::NV];
-      if (pv) {
-        const V* src = reinterpret_cast<const V*>(tbuf + p * (K * 11));
+      if (v == 0 || !S::PREFETCH) load_records(raw, p, pv);   // else prefetched during the rounds
+      else {
 #pragma unroll
-        for (int i = 0; i < S::NV; ++i) raw[i] = __ldg(src + i);
-      } else {
-#pragma unroll
-        for (int i = 0; i < S::NV; ++i) memset(&raw[i], 0, sizeof(V));
+        for (int i = 0; i < S::NV; ++i) raw[i] = nraw[i];
       }
-      memcpy(h, raw, sizeof(h));
+      // the pixel's K*11 halfwords as 32-bit words; record k starts at halfword 11k
+      constexpr int NW = (K * 11 + 1) / 2 + 1;
+      uint32_t rw[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) rw[i] = 0;
+      memcpy(rw, raw, K * 22);
+#ifdef GN_PROFILE_TB
+      {  // force the loads to complete for the phase timer
+        uint32_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) acc ^= rw[i];
+        if (acc == 0x12345u) gn_tb_prof[15] += 1;
+      }
+#endif
+      TBP_NOW(tp_l1);
+      TBP_ADD(12, tp_t0, tp_l1);
+      // A1 words of each record (ch0|ch1, .., ch8|ch9, ch10|1.0) and its 64-bit sort key
+      // (depth, ch0, ch1, ch2): one PRMT per word for records at odd halfword offsets.
       uint32_t w[K][6];
       uint64_t key[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const uint16_t* q = h + k * 11;
-        w[k][0] = q[0] | ((uint32_t)q[1] << 16);
-        w[k][1] = q[2] | ((uint32_t)q[3] << 16);
-        w[k][2] = q[4] | ((uint32_t)q[5] << 16);
-        w[k][3] = q[6] | ((uint32_t)q[7] << 16);
-        w[k][4] = q[8] | ((uint32_t)q[9] << 16);
-        w[k][5] = q[10] | (0x3F80u << 16);
-        key[k] = ((uint64_t)q[7] << 48) | ((uint64_t)q[0] << 32) | ((uint64_t)q[1] << 16) | (uint64_t)q[2];
+        const int s0 = 11 * k, wi = s0 >> 1;
+        if ((s0 & 1) == 0) {
+#pragma unroll
+          for (int j = 0; j < 5; ++j) w[k][j] = rw[wi + j];
+          w[k][5] = (rw[wi + 5] & 0xFFFFu) | 0x3F800000u;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 5; ++j) w[k][j] = __byte_perm(rw[wi + j], rw[wi + j + 1], 0x5432);
+          w[k][5] = (rw[wi + 5] >> 16) | 0x3F800000u;
+        }
+        const uint32_t khi = __byte_perm(w[k][0], w[k][3], 0x7610);   // depth<<16 | ch0
+        const uint32_t klo = __byte_perm(w[k][1], w[k][0], 0x7610);   // ch1<<16 | ch2
+        key[k] = ((uint64_t)khi << 32) | klo;
       }
+      TBP_NOW(tp_l2);
+      TBP_ADD(13, tp_l1, tp_l2);
       int rank[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) rank[k] = 0;
@@ -153,18 +282,16 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
 #pragma unroll
         for (int j = 0; j < i; ++j) {
           // is record j before record i?  (key, then remaining words, then slot index)
-          bool jf;
-          if (key[j] != key[i]) jf = key[j] < key[i];
-          else {
+          bool jf = key[j] < key[i];
+          if (key[j] == key[i]) {   // rare: full-record tie-break
             jf = true;
 #pragma unroll
             for (int c = 1; c < 6; ++c)
               if (w[j][c] != w[i][c]) { jf = w[j][c] < w[i][c]; break; }
           }
-          if (i < m) {            // both valid (j < i < m); masked slots are never read
-            rank[i] += jf ? 1 : 0;
-            rank[j] += jf ? 0 : 1;
-          }
+          const bool both = i < m;  // both valid (j < i < m); masked slots are never read
+          rank[i] += (both && jf) ? 1 : 0;
+          rank[j] += (both && !jf) ? 1 : 0;
         }
       }
 #pragma unroll
@@ -179,6 +306,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
           tc::sts128(dst + PL, 0, 0, 0, 0);
         }
       }
+      TBP_NOW(tp_l3);
+      TBP_ADD(14, tp_l2, tp_l3);
     }
     // the tile's largest count: slots no pixel uses are skipped (they would add 0)
     {
@@ -205,8 +334,14 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
       for (int j = 0; j < C0 / 8; ++j) tc::sts128(sA3 + j * PL + r * 16, 0, 0, 0, 0);
     }
     tc::fence_proxy_async();
+    TBP_NOW(tp_t1);
+    TBP_ADD(1, tp_t0, tp_t1);
     tc::bar_sync(bar_id, 128);
+    TBP_NOW(tp_t2);
+    TBP_ADD(2, tp_t1, tp_t2);
     const int Kt = max(max(red[0], red[1]), max(red[2], red[3]));
+    TBP_ADD(10, 0, Kt + 1);
+    TBP_ADD(11, 0, 1);
     if (tid == 0) {
       tc::fence_after_sync();
 #pragma unroll
@@ -217,9 +352,19 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
         tc::mma_f16_ss(t_acc1, tc::smem_desc(sA1, PL, 128), tc::smem_desc(sW1, H * 16, 128), ID_T, 0);
       tc::mma_commit(mbar);
     }
+    if (S::PREFETCH && v + 1 < SBT) {   // prefetch the next tile's records (latency hidden by the rounds)
+      int pe2 = pe_all[0];
+#pragma unroll
+      for (int u = 1; u < SBT; ++u) pe2 = v + 1 == u ? pe_all[u] : pe2;
+      const long p2 = q0 + (pe2 & 2047);
+      load_records(nraw, p2, p2 < P);
+    }
 #pragma unroll 1
     for (int t = 0; t <= Kt; ++t) {
+      TBP_NOW(tp_r0);
       tc::mbar_wait(mbar, phase);
+      TBP_NOW(tp_r1);
+      TBP_ADD(3, tp_r0, tp_r1);
       phase ^= 1;
       tc::fence_after_sync();
       if (t >= 1) {  // epilogue 2 of slot t-1 -> A3 (MMA3(t-2) and the e0 MMA are done)
@@ -260,9 +405,13 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
         tc::sts128(sA2 + (H / 8) * PL + r * 16, one | (one << 16), one, 0, 0);
         tc::sts128(sA2 + (H / 8 + 1) * PL + r * 16, 0, 0, 0, 0);
       }
+      TBP_NOW(tp_r2);
+      TBP_ADD(4, tp_r1, tp_r2);
       tc::fence_before_sync();
       tc::fence_proxy_async();
       tc::bar_sync(bar_id, 128);
+      TBP_NOW(tp_r3);
+      TBP_ADD(5, tp_r2, tp_r3);
       if (tid == 0) {
         tc::fence_after_sync();
         if (t >= 1) {
@@ -283,9 +432,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
         tc::mma_commit(mbar);
       }
     }
+    TBP_NOW(tp_e0);
     tc::mbar_wait(mbar, phase);
     phase ^= 1;
     tc::fence_after_sync();
+    TBP_NOW(tp_e1);
+    TBP_ADD(6, tp_e0, tp_e1);
     // ---- 3. phi and psi ----
     float ps0 = bO[0], ps1 = bO[1], ps2 = bO[2];
     if (r_takes_ld) {
@@ -310,7 +462,13 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint8_t* __restrict__ tcount, c
     }
     if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
     tc::fence_before_sync();
-    tc::bar_sync(bar_id, 128);   // TMEM reads and red[] of this tile done before the next tile
+    TBP_NOW(tp_e2);
+    TBP_ADD(7, tp_e1, tp_e2);
+    tc::bar_sync(bar_id, 128);   // TMEM reads, red[] and perm[] of this tile done before the next
+    TBP_NOW(tp_end);
+    TBP_ADD(9, tp_t0, tp_end);
+  }
+    sb = sbn[(it + 1) & 1];   // written before this superblock's barriers, read after them
   }
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<S::TMEM_COLS>(*tptr);

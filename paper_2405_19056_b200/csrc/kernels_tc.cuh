@@ -64,6 +64,7 @@ struct TcState {
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
+  int* sched = nullptr;         // T kernel's dynamic superblock counter
   int tile_nranks = 0, tile_rank = -1;
 };
 
@@ -373,6 +374,7 @@ inline void tc_release(glassnet* net) {
   if (s->tb_par) cudaFree(s->tb_par);
   for (auto& c : s->conv) if (c.wimg) cudaFree(c.wimg);
   if (s->tile) { for (void* q : s->tile->owned) cudaFree(q); delete s->tile; }
+  if (s->sched) cudaFree(s->sched);
   delete s;
   net->tc_state = nullptr;
 }
@@ -384,13 +386,16 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
   auto kfn = k_tb_tc<K, H, C0, POOL>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-  const long ntiles = (P + 127) / 128;
+  const long nsb = (P + 128 * S::SBT - 1) / (128 * S::SBT);   // superblocks (work units)
   long grid = net->num_sms;
-  if (grid * S::NCH > ntiles) grid = (ntiles + S::NCH - 1) / S::NCH;
+  if (grid * S::NCH > nsb) grid = (nsb + S::NCH - 1) / S::NCH;
+  if (!s->sched && cudaMalloc(&s->sched, sizeof(int)) != cudaSuccess)
+    return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "scheduler counter");
+  cudaMemsetAsync(s->sched, 0, sizeof(int), st);
   kfn<<<(unsigned)grid, 128 * S::NCH, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
       reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, psi, P,
-      (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0);
+      (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0, s->sched);
   return 0;
 }
 

@@ -131,6 +131,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
                : "memory");
 }
 
+// Bulk prefetch of [src, src+bytes) into L2 by the TMA engine (bytes multiple of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ---- conversions ----
 __device__ __forceinline__ uint32_t cvt_relu_bf16x2(float lo, float hi) {
   uint32_t r;

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libglassnet.so")
+LIB_PATH = os.environ.get("GN_LIB", os.path.join(_HERE, "libglassnet.so"))   # GN_LIB: diagnostic builds
 
 GLASSNET_ABI_VERSION = 1
 BF16, FP32 = 0, 1
