@@ -1,18 +1,7 @@
 // kernels_tc.cuh -- tcgen05 tensor-core kernels for bf16 mode.
 //
-// k_tb_tc: the fused T + B + psi kernel.  Per 128-pixel tile and per
-// fragment slot s (canonical order, reading R5):
-//   A1[128x16]  = records (11 ch, bf16) | 1,1,1 (bias hi/mid/lo columns) | 0        (smem)
-//   acc         = A1 * W1ext^T                   (TMEM, fp32)      T.h layer 1
-//   A2[128xH+16]= ReLU(acc) (bf16) | 1,1,1 | 0                         (smem)
-//   acc         = A2 * W2ext^T                   (TMEM)            T.h layer 2
-//   A3[128xH]   = ReLU(acc) / (mean ? n : 1)  (f16)                  (smem)
-//   accB       += A3 * W_B,tau^T                 (TMEM)            g = sum (Eq. eq:SymmetricNN)
-// with accB initialised by e0 * W_B,e0^T.  The pool over fragments is carried out by the
-// tensor core's accumulation: W_B (sum_k a2_k) = sum_k (W_B a2_k) (linearity; reading R15-
-// style rewrite).  Per-fragment activations never leave the SM.
-// Invalid slots are all-zero rows including the bias columns, so they contribute exactly 0.
-// Epilogue: phi = ReLU(accB + b_B + w_Bn n); psi = W_O,d0 phi + W_O,L L_d + b_O (fp32).
+// k_tb_tc: the fused T + B + psi kernel; its design is documented at
+// the top of kernels_tb_tc.cuh.  This file holds the host-side packing and launchers.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -60,7 +49,7 @@ struct Geom {
 
 struct TcState {
   uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
-  float* tb_par = nullptr;      // bB, wBn, WO (c0+3 wide), bO
+  TbParams tb_prm;              // bB, wBn, WO (c0+3 wide), bO, q2 (kernel parameters)
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
@@ -129,14 +118,11 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
     split3(T1b[o], w1[(size_t)o * 16 + 11], w1[(size_t)o * 16 + 12], w1[(size_t)o * 16 + 13]);
   }
   pack_kmajor(w1, H, 16, false, img);
-  // W2ext [H][H+16]
-  const int KA2 = H + 16;
-  std::vector<float> w2((size_t)H * KA2, 0.f);
-  for (int o = 0; o < H; ++o) {
-    for (int i = 0; i < H; ++i) w2[(size_t)o * KA2 + i] = rb(T2W[o * H + i]);
-    split3(T2b[o], w2[(size_t)o * KA2 + H], w2[(size_t)o * KA2 + H + 1], w2[(size_t)o * KA2 + H + 2]);
-  }
-  pack_kmajor(w2, H, KA2, false, img);
+  // W2 [H][H] (the layer-2 bias enters the pool's fixed-point conversion, q2 below)
+  std::vector<float> w2((size_t)H * H, 0.f);
+  for (int o = 0; o < H; ++o)
+    for (int i = 0; i < H; ++i) w2[(size_t)o * H + i] = rb(T2W[o * H + i]);
+  pack_kmajor(w2, H, H, false, img);
   const int NB = C0 + H + 1;
   std::vector<float> wbt((size_t)C0 * H), wbe((size_t)C0 * C0);
   for (int o = 0; o < C0; ++o) {
@@ -145,18 +131,21 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   }
   pack_kmajor(wbt, C0, H, true, img);
   pack_kmajor(wbe, C0, C0, false, img);
-  std::vector<float> par;
-  for (int o = 0; o < C0; ++o) par.push_back(Bb[o]);
-  for (int o = 0; o < C0; ++o) par.push_back(rb(BW[(size_t)o * NB + C0 + H]));
+  TbParams& prm = s->tb_prm;
+  memset(&prm, 0, sizeof prm);
+  for (int o = 0; o < C0; ++o) prm.bB[o] = Bb[o];
+  for (int o = 0; o < C0; ++o) prm.wBn[o] = rb(BW[(size_t)o * NB + C0 + H]);
   const int NO = C0 + (ld ? 3 : 0);
   for (int j = 0; j < 3; ++j)
-    for (int i = 0; i < C0 + 3; ++i) par.push_back(i < NO ? rb(OW[(size_t)j * NO + i]) : 0.f);
-  for (int j = 0; j < 3; ++j) par.push_back(Ob[j]);
-  if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess || cudaMalloc(&s->tb_par, par.size() * 4) != cudaSuccess)
+    for (int i = 0; i < C0 + 3; ++i) prm.WO[j * (C0 + 3) + i] = i < NO ? rb(OW[(size_t)j * NO + i]) : 0.f;
+  for (int j = 0; j < 3; ++j) prm.bO[j] = Ob[j];
+  // q2 = 2^23 + b2 2^12 rounded to fp32 (an integer): the FFMA addend of the pool's
+  // fixed-point conversion (kernels_tb_tc.cuh)
+  for (int o = 0; o < H; ++o) prm.q2[o] = TB_QMAGIC + T2b[o] * TB_QSCALE;
+  if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess)
     return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "tc weight alloc");
   cudaMemcpy(s->tb_wimg, img.data(), img.size(), cudaMemcpyHostToDevice);
-  cudaMemcpy(s->tb_par, par.data(), par.size() * 4, cudaMemcpyHostToDevice);
-  net->w_bytes += img.size() + par.size() * 4;
+  net->w_bytes += img.size() + sizeof(TbParams);
   return 0;
 }
 
@@ -371,7 +360,6 @@ inline void tc_release(glassnet* net) {
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
   if (!s) return;
   if (s->tb_wimg) cudaFree(s->tb_wimg);
-  if (s->tb_par) cudaFree(s->tb_par);
   for (auto& c : s->conv) if (c.wimg) cudaFree(c.wimg);
   if (s->tile) { for (void* q : s->tile->owned) cudaFree(q); delete s->tile; }
   if (s->sched) cudaFree(s->sched);
@@ -394,8 +382,7 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   cudaMemsetAsync(s->sched, 0, sizeof(int), st);
   kfn<<<(unsigned)grid, 128 * S::NCH, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
-      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_par, psi, P,
-      (net->d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0, s->sched);
+      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_prm, psi, P, s->sched);
   return 0;
 }
 

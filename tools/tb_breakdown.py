@@ -21,8 +21,8 @@ L.glassnet_debug_tb_prof(buf, 0)
 v = list(buf)
 tiles, rounds = v[11], v[10]
 names = {0: "superblock sort", 1: "tile prologue (loads, rank, A1/e0 writes)", 2: "prologue barrier", 3: "round: MMA wait",
-         4: "round: epilogues", 5: "round: barrier", 6: "final MMA wait", 7: "epilogue 3 (phi, psi)", 9: "tile total",
-         12: "  prologue: loads (tcount+records)", 13: "  prologue: word assembly", 14: "  prologue: rank + A1 writes"}
+         4: "round: epilogues", 5: "round: barrier", 6: "final MMA wait", 7: "epilogue 3 (phi, psi)", 8: "round: MMA issue (thread 0)", 15: "round: epilogue 2 (pool, overlapped)", 9: "tile total",
+         12: "  prologue: loads (tcount+records)", 13: "tile-start MMA issue (thread 0)", 14: "  prologue: rank + A1 writes"}
 print(f"tiles={tiles} rounds={rounds} rounds/tile={rounds / max(tiles, 1):.2f}")
 for i, nm in names.items():
-    print(f"{nm:45s} {v[i] / max(tiles, 1):10.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):8.0f} cyc/round" if i in (3, 4, 5) else ""))
+    print(f"{nm:45s} {v[i] / max(tiles, 1):10.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):8.0f} cyc/round" if i in (3, 4, 5, 8, 15) else ""))
