@@ -1,4 +1,5 @@
-"""Per-phase clock64 breakdown of one T-kernel chain (diagnostic build, -DGN_PROFILE_TB)."""
+"""Per-phase clock64 breakdown of one T-kernel chain (diagnostic build, -DGN_PROFILE_TB):
+thread 0 of chain 0 of CTA 0 (an epilogue thread)."""
 import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -19,10 +20,10 @@ L.glassnet_debug_tb_prof(buf, 1)
 net.forward(g, d, t, n); torch.cuda.synchronize()
 L.glassnet_debug_tb_prof(buf, 0)
 v = list(buf)
-tiles, rounds = v[11], v[10]
-names = {0: "superblock sort", 1: "tile prologue (loads, rank, A1/e0 writes)", 2: "prologue barrier", 3: "round: MMA wait",
-         4: "round: epilogues", 5: "round: barrier", 6: "final MMA wait", 7: "epilogue 3 (phi, psi)", 8: "round: MMA issue (thread 0)", 15: "round: epilogue 2 (pool, overlapped)", 9: "tile total",
-         12: "  prologue: loads (tcount+records)", 13: "tile-start MMA issue (thread 0)", 14: "  prologue: rank + A1 writes"}
+tiles, rounds = v[11], v[10] - v[11]
+names = {1: "E1 prologue (A1 from staging, cp.async, Kt)", 3: "E1 round: wait for MMA batch",
+         4: "E1 round: epilogue 1 (acc1 -> A2) + arrive", 6: "E1 final: wait last batch, rdyF, wait accB",
+         8: "E1 epilogue 3 (phi, psi)", 9: "tile total"}
 print(f"tiles={tiles} rounds={rounds} rounds/tile={rounds / max(tiles, 1):.2f}")
 for i, nm in names.items():
-    print(f"{nm:45s} {v[i] / max(tiles, 1):10.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):8.0f} cyc/round" if i in (3, 4, 5, 8, 15) else ""))
+    print(f"{nm:50s} {v[i] / max(tiles, 1):8.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):6.0f} cyc/round" if i in (3, 4) else ""))
