@@ -53,7 +53,9 @@ struct TcState {
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
-  int* sched = nullptr;         // T kernel's dynamic superblock counter
+  int* sched = nullptr;         // T kernel's dynamic tile counter
+  uint16_t* perm = nullptr;     // T kernel's count-sorted pixel order (k_tb_sort), one entry per pixel
+  long perm_cap = 0;
   int tile_nranks = 0, tile_rank = -1;
 };
 
@@ -111,17 +113,22 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   net->tc_state = s;
   auto rb = [](float v) { return h_bf16f(h_bf16(v)); };
   std::vector<uint8_t> img;
-  // W1ext [H][16]: cols 0..10 = W1 (depth col x 2^-7 when normalising), 11..13 = b1 hi/mid/lo
-  std::vector<float> w1((size_t)H * 16, 0.f);
-  for (int o = 0; o < H; ++o) {
-    for (int i = 0; i < 11; ++i) w1[(size_t)o * 16 + i] = rb(T1W[o * 11 + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
-    split3(T1b[o], w1[(size_t)o * 16 + 11], w1[(size_t)o * 16 + 12], w1[(size_t)o * 16 + 13]);
+  // W1 in 8 column-offset copies [o][H][32]: the record's 11 weights at columns o..o+10
+  // (depth column x 2^-7 when normalising; bf16-exact), zeros elsewhere.  Record k's K-window
+  // starts at halfword 11k = 8j + o of the row (kernels_tb_tc.cuh); the bias b1 is added in
+  // epilogue 1.
+  for (int o = 0; o < 8; ++o) {
+    std::vector<float> w1((size_t)H * 32, 0.f);
+    for (int n = 0; n < H; ++n)
+      for (int i = 0; i < 11; ++i)
+        w1[(size_t)n * 32 + o + i] = rb(T1W[n * 11 + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
+    pack_kmajor(w1, H, 32, false, img);
   }
-  pack_kmajor(w1, H, 16, false, img);
-  // W2 [H][H] (the layer-2 bias enters the pool's fixed-point conversion, q2 below)
+  // W2 [H][H], scaled by the pool's fixed-point scale 2^12 (exact: a power of two), so the
+  // accumulator is (W2 a1) 2^12; the layer-2 bias enters the conversion (q2 below)
   std::vector<float> w2((size_t)H * H, 0.f);
   for (int o = 0; o < H; ++o)
-    for (int i = 0; i < H; ++i) w2[(size_t)o * H + i] = rb(T2W[o * H + i]);
+    for (int i = 0; i < H; ++i) w2[(size_t)o * H + i] = rb(T2W[o * H + i]) * TB_QSCALE;
   pack_kmajor(w2, H, H, false, img);
   const int NB = C0 + H + 1;
   std::vector<float> wbt((size_t)C0 * H), wbe((size_t)C0 * C0);
@@ -142,7 +149,10 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   // q2 = 2^23 + b2 2^12 rounded to fp32 (an integer): the FFMA addend of the pool's
   // fixed-point conversion (kernels_tb_tc.cuh)
   for (int o = 0; o < H; ++o) prm.q2[o] = TB_QMAGIC + T2b[o] * TB_QSCALE;
-  if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess)
+  for (int o = 0; o < H; ++o) prm.b1[o] = T1b[o];
+  s->perm_cap = ((long)d.max_batch * d.height * d.width + TB_SBP - 1) / TB_SBP * TB_SBP;
+  if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess || cudaMalloc(&s->sched, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&s->perm, s->perm_cap * sizeof(uint16_t)) != cudaSuccess)
     return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "tc weight alloc");
   cudaMemcpy(s->tb_wimg, img.data(), img.size(), cudaMemcpyHostToDevice);
   net->w_bytes += img.size() + sizeof(TbParams);
@@ -363,6 +373,7 @@ inline void tc_release(glassnet* net) {
   for (auto& c : s->conv) if (c.wimg) cudaFree(c.wimg);
   if (s->tile) { for (void* q : s->tile->owned) cudaFree(q); delete s->tile; }
   if (s->sched) cudaFree(s->sched);
+  if (s->perm) cudaFree(s->perm);
   delete s;
   net->tc_state = nullptr;
 }
@@ -372,17 +383,18 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
                            const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   using S = TbLayout<K, H, C0>;
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  const long nsb = (P + TB_SBP - 1) / TB_SBP;
+  if (nsb * TB_SBP > s->perm_cap) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "T kernel: %ld pixels exceed the workspace", P);
+  k_tb_sort<K><<<(unsigned)nsb, 128, 0, st>>>(tcount, s->perm, P);
   auto kfn = k_tb_tc<K, H, C0, POOL>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-  const long nsb = (P + 128 * S::SBT - 1) / (128 * S::SBT);   // superblocks (work units)
+  const long ntiles = nsb * TB_SBT;
   long grid = net->num_sms;
-  if (grid * S::NCH > nsb) grid = (nsb + S::NCH - 1) / S::NCH;
-  if (!s->sched && cudaMalloc(&s->sched, sizeof(int)) != cudaSuccess)
-    return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "scheduler counter");
+  if (grid * S::NCH > ntiles) grid = (ntiles + S::NCH - 1) / S::NCH;
   cudaMemsetAsync(s->sched, 0, sizeof(int), st);
-  kfn<<<(unsigned)grid, 128 * S::NCH, S::SMEM, st>>>(
-      reinterpret_cast<const uint16_t*>(tbuf), tcount, reinterpret_cast<const uint16_t*>(e0),
-      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_prm, psi, P, s->sched);
+  kfn<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(
+      reinterpret_cast<const uint16_t*>(tbuf), reinterpret_cast<const uint16_t*>(e0),
+      reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_prm, s->perm, psi, P, s->sched);
   return 0;
 }
 
