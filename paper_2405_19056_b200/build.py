@@ -58,13 +58,14 @@ def build_lib(force=False, verbose=True):
     return LIB
 
 
-def build_profile_lib(verbose=True):
-    """Diagnostic variant with the T kernel's clock64 phase counters (-DGN_PROFILE_TB)."""
+def build_profile_lib(verbose=True, name="libglassnet_prof.so", defines=("GN_PROFILE_TB",)):
+    """Diagnostic variant (bench configuration's T kernel only): by default with the T
+    kernel's clock64 phase counters (-DGN_PROFILE_TB); `defines` selects ablation switches."""
     global LIB
     keep = LIB
-    LIB = os.path.join(PKG, "libglassnet_prof.so")
+    LIB = os.path.join(PKG, name)
     try:
-        os.environ["GN_EXTRA_NVCC"] = "-DGN_PROFILE_TB"
+        os.environ["GN_EXTRA_NVCC"] = " ".join("-D" + d for d in ("GN_DIAG_K8_ONLY",) + tuple(defines))
         return build_lib(force=True, verbose=verbose)
     finally:
         os.environ.pop("GN_EXTRA_NVCC", None)

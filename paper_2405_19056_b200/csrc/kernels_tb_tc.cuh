@@ -21,23 +21,27 @@
 //
 // Warp specialisation.  A CTA runs NCH independent "chains"; a chain has three roles, all
 // indexed by tile row r = TMEM lane r:
-//   E1 (4 warps)  per tile: publish the rows' counts; issue the cp.asyncs of the NEXT
-//                 tile's records and e0 (double-buffered operands; completion tracked by
-//                 the `loaded` mbarrier, so E1 never waits for global memory);
+//   E1 (4 warps)  producer.  Per tile v: publish the rows' pixels and counts; copy tile
+//                 v+1's records into the other operand buffer (cp.async, zero fill,
+//                 coalesced: consecutive threads take consecutive 16-byte chunks of a row);
 //                 round t: A2 = ReLU(acc1 + b1) -> bf16 -> TMEM
-//                                                    -> MMA: acc2[t&1] = A2 W2^T, acc1 = layer 1 of slot t+1
-//                 final: phi = ReLU(accB + b_B + w_Bn n), psi = W_O,d0 phi + W_O,L L_d + b_O -> HBM
-//   E2 (4 warps)  pool += Q(acc2[s&1] + b2) for every slot s as its batch completes (acc2
-//                 is double-buffered, so this runs beside E1's next slot); then
-//                 tau = pool (f16)                   -> MMA: accB = e0 W_B,e0^T + tau W_B,tau^T
-//   MMA (1 warp)  one thread issues every tcgen05.mma of the chain, and executes the
-//                 generic -> async proxy fence for the operands the others wrote.
-// Hand-offs are mbarriers: loaded[b] (cp.async completion of operand buffer b), rdyA
-// (E1 -> MMA: counts published / A2 written), tstart (E1 -> E2), free2[b] (E2 -> MMA: acc2
-// buffer b read), rdyF (E2 -> MMA: tau written), done1 (commit -> E1, batches holding a
-// layer-1 MMA), done2[b] (commit -> E2, layer-2 batches into buffer b) and doneF (commit ->
-// E1, the accB batch).  Each waiter can be at most one
-// phase behind its barrier by construction.
+//                                      -> MMA: acc2[n&1] = A2 W2^T, acc1 = layer 1 of slot t+1
+//                 E1 does not wait for the tile's drain: it runs on into tile v+1.
+//   E2 (4 warps)  consumer.  Per tile: copy e0 into its operand; pool += Q(acc2 + b2) for
+//                 every slot as its batch completes (acc2 double-buffered, n = running
+//                 layer-2 batch count); tau = pool (f16)
+//                                      -> MMA: accB = e0 W_B,e0^T + tau W_B,tau^T
+//                 then phi = ReLU(accB + b_B + w_Bn n), psi = W_O,d0 phi + W_O,L L_d + b_O -> HBM.
+//   MMA (1 warp)  one thread issues every tcgen05.mma of the chain, executes the generic ->
+//                 async proxy fence for the operands the others wrote, and issues a tile's
+//                 accB batch whenever its tau is ready while it feeds the next tile's rounds.
+// Hand-offs are mbarriers: loadedA[b] / loadedE[b] (cp.async completion of record / e0
+// buffer b), rdyP (E1 -> MMA: a tile's counts), rdyA (E1 -> MMA: A2 written), tstart (E1 ->
+// E2: a tile's rows), tack (E2 -> E1: rows read), free2[b] (E2 -> MMA: acc2 buffer b read),
+// rdyF (E2 -> MMA: tau written), done1 (commit -> E1: prologue batch and batches holding a
+// layer-1 MMA), done2[b] (commit -> E2: layer-2 batches into buffer b), doneF (commit ->
+// E2: the accB batch).  Every waiter is at most one phase behind its barrier: each
+// arrival of a producer is separated from its next one by a wait on the consumer.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -149,11 +153,14 @@ struct TbLayout {
   static constexpr int CH_A1 = 0;                     // 2 buffers x A1_PL planes
   static constexpr int CH_E0 = CH_A1 + 2 * A1_PL * PL;          // 2 buffers x C0/8 planes
   static constexpr int CH_TAU = CH_E0 + 2 * (C0 / 8) * PL;      // H/8 planes (f16)
-  static constexpr int CH_MROW = CH_TAU + (H / 8) * PL;         // 128 x u8: the rows' valid counts
-  static constexpr int CH_B = CH_MROW + 128;
-  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 12 mbarrier slots; then the tmem ptr
-  static constexpr int OFF_RED = OFF_BAR + 4 * 96 + 16;     // per chain 8 ints: warp max counts, Kt, tile ids
-  static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 127) / 128 * 128;
+  static constexpr int CH_ROWS = CH_TAU + (H / 8) * PL;         // [2] x 128 int64: pixel | count << 32 (E2)
+  static constexpr int CH_NROWS = CH_ROWS + 2 * 128 * 8;        // [2] x 128 int64: the next tile's (E1's fill)
+  static constexpr int CH_KT = CH_NROWS + 2 * 128 * 8;          // [2] int: Kt per tile parity; [2..5] warp max
+  static constexpr int CH_B = CH_KT + 64;
+  static constexpr int NBAR = 16;                     // mbarrier slots per chain
+  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;
+  static constexpr int OFF_RED = OFF_BAR + 4 * NBAR * 8 + 16;   // per chain 8 ints: tile ids; then the tmem ptr
+  static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 16 + 127) / 128 * 128;
   static constexpr int TCOLS = (3 * H + C0 + H / 2 + 31) / 32 * 32;   // acc1, acc2 x2, accB, A2 (packed)
   static constexpr int NCH_T = 512 / TCOLS;
   static constexpr int NCH_S = (232448 - 1024 - OFF_CH) / CH_B;
@@ -170,6 +177,15 @@ __device__ __forceinline__ void cp_async16z(uint32_t dst, const void* src, uint3
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(tc::smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 
 template <int K, int H, int C0, int POOL>
 __global__ void __launch_bounds__(TbLayout<K, H, C0>::THREADS, 1)
@@ -185,17 +201,20 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   const int wg = threadIdx.x >> 5;
   const int role = wg < 4 * NCH ? 0 : wg < 8 * NCH ? 1 : 2;   // E1, E2, MMA
   const int g = role == 2 ? wg - 8 * NCH : (wg >> 2) % NCH;    // chain
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * g;
-  uint64_t* loaded = bars + 0;     // [2]
-  uint64_t* rdyA = bars + 2;
-  uint64_t* rdyF = bars + 3;
-  uint64_t* free2 = bars + 4;      // [2]
-  uint64_t* done1 = bars + 6;
-  uint64_t* done2 = bars + 7;      // [2]
-  uint64_t* tstart = bars + 9;
-  uint64_t* doneF = bars + 10;
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 4 * 96);
-  volatile int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 8 * g;   // [0..3] warp max, [4] Kt, [5..7] tile ids
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + S::NBAR * g;
+  uint64_t* loadedA = bars + 0;    // [2]
+  uint64_t* loadedE = bars + 2;    // [2]
+  uint64_t* rdyP = bars + 4;
+  uint64_t* rdyA = bars + 5;
+  uint64_t* rdyF = bars + 6;
+  uint64_t* free2 = bars + 7;      // [2]
+  uint64_t* done1 = bars + 9;
+  uint64_t* done2 = bars + 10;     // [2]
+  uint64_t* doneF = bars + 12;
+  uint64_t* tstart = bars + 13;
+  uint64_t* tack = bars + 14;
+  volatile int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 8 * g;   // [5..7] tile ids
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_RED + 4 * 32);
 
   TBP_INIT();
   for (int i = threadIdx.x; i < S::WIMG_B / 16; i += blockDim.x)
@@ -208,13 +227,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     }
   if (threadIdx.x == 0) {
     for (int c = 0; c < NCH; ++c) {
-      uint64_t* b = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * c;
-      tc::mbar_init(b + 0, 128); tc::mbar_init(b + 1, 128);   // loaded[2]
-      tc::mbar_init(b + 2, 128); tc::mbar_init(b + 3, 128);   // rdyA, rdyF
-      tc::mbar_init(b + 4, 128); tc::mbar_init(b + 5, 128);   // free2[2]
-      tc::mbar_init(b + 6, 1); tc::mbar_init(b + 7, 1); tc::mbar_init(b + 8, 1);   // done1, done2[2]
-      tc::mbar_init(b + 9, 128);                              // tstart
-      tc::mbar_init(b + 10, 1);                               // doneF
+      uint64_t* b = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + S::NBAR * c;
+      for (int i = 0; i < 4; ++i) tc::mbar_init(b + i, 128);   // loadedA[2], loadedE[2]
+      tc::mbar_init(b + 4, 128); tc::mbar_init(b + 5, 128); tc::mbar_init(b + 6, 128);   // rdyP, rdyA, rdyF
+      tc::mbar_init(b + 7, 128); tc::mbar_init(b + 8, 128);    // free2[2]
+      for (int i = 9; i < 13; ++i) tc::mbar_init(b + i, 1);    // done1, done2[2], doneF
+      tc::mbar_init(b + 13, 128); tc::mbar_init(b + 14, 128);  // tstart, tack
     }
     tc::fence_mbar_init();
   }
@@ -226,10 +244,14 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   const uint32_t tmem = *tptr + g * S::TCOLS;
   const uint32_t t_acc1 = tmem, t_acc2 = tmem + H, t_accB = tmem + 3 * H, t_a2 = tmem + 3 * H + C0;
   uint8_t* chs = smem + S::OFF_CH + g * S::CH_B;
-  volatile uint8_t* mrow = chs + S::CH_MROW;
+  volatile long long* rows = reinterpret_cast<long long*>(chs + S::CH_ROWS);     // [2][128]
+  volatile long long* nrows = reinterpret_cast<long long*>(chs + S::CH_NROWS);   // [2][128]
+  volatile int* ktv = reinterpret_cast<int*>(chs + S::CH_KT);        // [0..1] Kt, [2..5] warp max
   const uint32_t sA1 = tc::smem_u32(chs + S::CH_A1), sE0 = tc::smem_u32(chs + S::CH_E0);
   const uint32_t sTAU = tc::smem_u32(chs + S::CH_TAU);
   const long ntiles = (P + TB_SBP - 1) / TB_SBP * TB_SBT;
+  // a row's pixel is packed with its valid count: pixel | count << 32, -1 if absent
+  constexpr int PXB = 32;
 
   if (role == 2) {
     // ------------------------------------------------------------------ MMA warp of chain g
@@ -248,66 +270,119 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         if (o > 5)
           tc::mma_f16_ss(t_acc1, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
       };
-      uint32_t aph = 0, fph = 0, lph[2] = {0, 0}, f2ph[2] = {0, 0};
-      for (int buf = 0;; buf ^= 1) {
-        tc::mbar_wait(rdyA, aph); aph ^= 1;        // the tile's counts
-        const int Kt = red[4];
-        if (Kt < 0) break;
-        tc::mbar_wait(loaded + buf, lph[buf]); lph[buf] ^= 1;   // its records and e0 (cp.async)
+      uint32_t pph = 0, aph = 0, fph = 0, lph[2] = {0, 0}, eph[2] = {0, 0}, f2ph[2] = {0, 0};
+      int uses[2] = {0, 0};
+      int nb = 0;            // running layer-2 batch count (acc2 buffer = nb & 1)
+      int pend = -1;         // tile parity whose accB batch is pending (-1: none)
+      int pendKt = 0;
+      auto issue_accB = [&]() {
+        tc::mbar_wait(loadedE + pend, eph[pend]); eph[pend] ^= 1;   // its e0
         tc::fence_after_sync();
         tc::fence_proxy_async();
-        if (Kt > 0) { layer1(0, buf); tc::mma_commit(done1); }
-        for (int t = 0; t < Kt; ++t) {
-          tc::mbar_wait(rdyA, aph); aph ^= 1;      // A2 of slot t in TMEM (acc1 read)
-          if (t >= 2) { tc::mbar_wait(free2 + (t & 1), f2ph[t & 1]); f2ph[t & 1] ^= 1; }   // acc2[t&1] read
-          tc::fence_after_sync();
-#pragma unroll
-          for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ts(t_acc2 + (t & 1) * H, t_a2 + q * 8, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T,
-                           q > 0);
-          if (t + 1 < Kt) { layer1(t + 1, buf); tc::mma_commit(done1); }
-          tc::mma_commit(done2 + (t & 1));
-        }
-        if (Kt >= 2) { tc::mbar_wait(free2 + ((Kt - 2) & 1), f2ph[(Kt - 2) & 1]); f2ph[(Kt - 2) & 1] ^= 1; }
-        if (Kt >= 1) { tc::mbar_wait(free2 + ((Kt - 1) & 1), f2ph[(Kt - 1) & 1]); f2ph[(Kt - 1) & 1] ^= 1; }
-        tc::mbar_wait(rdyF, fph); fph ^= 1;        // tau written
-        tc::fence_after_sync();
-        tc::fence_proxy_async();
-        const uint32_t e0b = sE0 + buf * (C0 / 8) * PL;
+        const uint32_t e0b = sE0 + pend * (C0 / 8) * PL;
 #pragma unroll
         for (int q = 0; q < C0 / 16; ++q)
           tc::mma_f16_ss(t_accB, tc::smem_desc(e0b + 2 * q * PL, PL, 128),
                          tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-        if (Kt > 0) {
+        if (pendKt > 0) {
 #pragma unroll
           for (int q = 0; q < H / 16; ++q)
             tc::mma_f16_ss(t_accB, tc::smem_desc(sTAU + 2 * q * PL, PL, 128),
                            tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
         }
         tc::mma_commit(doneF);
+        pend = -1;
+      };
+      // wait for (bar, phase) while issuing the pending accB batch as soon as its tau is ready
+      auto wait_service = [&](uint64_t* bar, uint32_t phase) {
+        for (;;) {
+          if (mbar_try(bar, phase)) return;
+          if (pend >= 0 && mbar_try(rdyF, fph)) { fph ^= 1; issue_accB(); }
+        }
+      };
+      for (int v = 0;; ++v) {
+        const int buf = v & 1;
+        wait_service(rdyP, pph); pph ^= 1;         // the tile's counts
+        const int Kt = ktv[buf];
+        if (Kt < 0) break;
+        wait_service(loadedA + buf, lph[buf]); lph[buf] ^= 1;   // its records (cp.async)
+        tc::fence_after_sync();
+        tc::fence_proxy_async();
+        if (Kt > 0) layer1(0, buf);
+        tc::mma_commit(done1);
+        for (int t = 0; t < Kt; ++t) {
+          wait_service(rdyA, aph); aph ^= 1;       // A2 of slot t in TMEM (acc1 read)
+          const int b = nb & 1;
+          if (uses[b] > 0) { wait_service(free2 + b, f2ph[b]); f2ph[b] ^= 1; }   // acc2[b] read
+          ++uses[b];
+          tc::fence_after_sync();
+#ifndef GN_ABL_NO_L2
+#pragma unroll
+          for (int q = 0; q < H / 16; ++q)
+            tc::mma_f16_ts(t_acc2 + b * H, t_a2 + q * 8, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
+#endif
+          if (t + 1 < Kt) { layer1(t + 1, buf); tc::mma_commit(done1); }
+          tc::mma_commit(done2 + b);
+          ++nb;
+        }
+        if (pend >= 0) {   // the previous tile's accB is still pending: finish it first
+          tc::mbar_wait(rdyF, fph); fph ^= 1;
+          issue_accB();
+        }
+        pend = buf;
+        pendKt = Kt;
       }
+      if (pend >= 0) { tc::mbar_wait(rdyF, fph); fph ^= 1; issue_accB(); }
     }
   } else if (role == 1) {
-    // ------------------------------------------------------------------ E2: the pool
+    // ------------------------------------------------------------------ E2: e0, pool, tau, phi, psi
     const int r = threadIdx.x & 127, warp = r >> 5;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    uint32_t tph = 0, d2ph[2] = {0, 0};
-    for (;;) {
+    uint32_t tph = 0, fph = 0, d2ph[2] = {0, 0};
+    int nb = 0;
+    for (int v = 0;; ++v) {
+      const int buf = v & 1;
       tc::mbar_wait(tstart, tph); tph ^= 1;
-      const int Kt = red[4];
+      const int Kt = ktv[buf];
       if (Kt < 0) break;
-      const int m = mrow[r];
+      const long long rw = rows[buf * 128 + r];
+      // e0 of the tile's rows -> its operand buffer (coalesced: consecutive threads take
+      // consecutive 16-byte chunks); the buffer was last read by tile v-2's accB batch
+      {
+        constexpr int NC = C0 / 8;
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          const int c = i * 128 + r, pr = c / NC, j = c % NC;
+          const long long x = rows[buf * 128 + pr];
+          const bool ok = x >= 0;
+          const uint16_t* src = ok ? e0 + (x & 0xFFFFFFFFll) * C0 + 8 * j : e0;
+          cp_async16z(sE0 + (buf * NC + j) * PL + pr * 16, src, ok ? 16u : 0u);
+        }
+        cp_async_arrive(loadedE + buf);
+      }
+      tc::mbar_arrive(tack);   // rows read
+      const bool pv = rw >= 0;
+      const long p = pv ? (long)(rw & 0xFFFFFFFFll) : 0;
+      const int m = pv ? (int)(rw >> PXB) : 0;
+      float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;   // consumed after the pool (latency hidden)
+      if (pv) {
+        ld0 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 0) << 16);
+        ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
+        ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
+      }
       uint32_t pool[H];
 #pragma unroll
       for (int j = 0; j < H; ++j) pool[j] = 0;
 #pragma unroll 1
       for (int s = 0; s < Kt; ++s) {
-        const int b = s & 1;
+        const int b = nb & 1;
+        ++nb;
         tc::mbar_wait(done2 + b, d2ph[b]); d2ph[b] ^= 1;
         tc::fence_after_sync();
         // pool += Q(acc2 + b2): acc2 carries the 2^12 scale (folded into W2), so x = acc2 + q2
         // is 2^23 + (v + b2) 2^12 rounded; masked slots clamp to exactly 2^23 (0)
         const float hi = (s < m) ? TB_QMAX : TB_QMAGIC;
+#ifndef GN_ABL_NO_POOL
 #pragma unroll
         for (int c = 0; c < H / 16; ++c) {
           uint32_t u[16];
@@ -320,10 +395,11 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
             pool[c * 16 + i] += __float_as_uint(x);
           }
         }
+#endif
         tc::fence_before_sync();
         tc::mbar_arrive(free2 + b);
       }
-      if (Kt > 0) {   // tau = pool (f16) -> its operand
+      if (Kt > 0) {   // tau = pool (f16) -> its operand (last read by the previous tile's accB batch)
         const uint32_t off = (uint32_t)Kt * TB_QBITS;
         const float sc = (POOL == 1 && m > 0) ? (1.f / TB_QSCALE) / (float)m : 1.f / TB_QSCALE;
 #pragma unroll
@@ -339,127 +415,16 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         }
       }
       tc::mbar_arrive(rdyF);   // release; the MMA thread fences the proxies
-    }
-  } else {
-    // ------------------------------------------------------------------ E1: operands, A2, phi, psi
-    const int r = threadIdx.x & 127, warp = r >> 5, lane = r & 31;
-    const int bar_id = 1 + g;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    uint32_t d1ph = 0, dfph = 0;
-    auto decode = [&](long tl, int pe, long& pp, int& mm, bool& ok) {   // this thread's pixel of tile tl
-      pp = tl / TB_SBT * TB_SBP + (pe & 2047);
-      ok = tl < ntiles && pp < P;
-      mm = ok ? (pe >> 11) : 0;
-    };
-    // copy row r's operands of a tile (pixel pp, mm valid records) into operand buffer `buf`
-    auto fill = [&](int buf, long pp, int mm, bool ok) {
-      const uint32_t a = sA1 + buf * S::A1_PL * PL + r * 16;
-      const int vb = ok ? mm * 22 : 0;            // valid bytes of the row
-      if (S::ASYNC) {
-        const char* src = ok ? reinterpret_cast<const char*>(tbuf + pp * (K * 11)) : reinterpret_cast<const char*>(tbuf);
-#pragma unroll
-        for (int i = 0; i < S::NPL; ++i)
-          cp_async16z(a + i * PL, src + 16 * i, (uint32_t)min(max(vb - 16 * i, 0), 16));
-      } else {   // rows not 16-byte aligned in global memory: through registers
-        const uint16_t* src = tbuf + pp * (K * 11);
-#pragma unroll
-        for (int i = 0; i < S::NPL; ++i) {
-          uint32_t w[4];
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int e = 8 * i + 2 * h;
-            const uint32_t lo = 2 * e < vb ? __ldg(src + e) : 0u, hi = 2 * e + 2 < vb ? __ldg(src + e + 1) : 0u;
-            w[h] = lo | (hi << 16);
-          }
-          tc::sts128(a + i * PL, w[0], w[1], w[2], w[3]);
-        }
-      }
-      const uint32_t eb = sE0 + buf * (C0 / 8) * PL + r * 16;
-      const uint16_t* es = ok ? e0 + pp * C0 : e0;
-#pragma unroll
-      for (int j = 0; j < C0 / 8; ++j) cp_async16z(eb + j * PL, es + 8 * j, ok ? 16u : 0u);
-      cp_async_arrive(loaded + buf);
-    };
-
-    // Tile pipeline: tile ids are claimed three ahead (atomics), the perm entry of the tile
-    // after next is loaded one tile ahead, and the next tile's operands are copied during
-    // this one, so no global latency sits on a critical path.
-    int claim = 0;
-    if (r == 0) { red[5] = atomicAdd(sched, 1); red[6] = atomicAdd(sched, 1); claim = atomicAdd(sched, 1); }
-    tc::bar_sync(bar_id, 128);
-    long tile = red[5], ntile = red[6];
-    long p, np;
-    int m, nm;
-    bool pv, npv;
-    decode(tile, tile < ntiles ? (int)__ldg(perm + tile * 128 + r) : 0, p, m, pv);
-    if (tile < ntiles) fill(0, p, m, pv);
-    decode(ntile, ntile < ntiles ? (int)__ldg(perm + ntile * 128 + r) : 0, np, nm, npv);
-    for (int it = 0; tile < ntiles; ++it) {
-      TBP_NOW(tp_t0);
-      const int buf = it & 1;
-      // ---- prologue: publish the counts; copy the next tile's operands
-      mrow[r] = (uint8_t)m;
-      {
-        const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
-        if (lane == 0) red[warp] = wm;
-        if (r == 0) { red[5 + (it + 2) % 3] = claim; claim = atomicAdd(sched, 1); }
-      }
-      tc::bar_sync(bar_id, 128);
-      const int Kt = max(max(red[0], red[1]), max(red[2], red[3]));
-      const long nntile = red[5 + (it + 2) % 3];
-      if (r == 0) red[4] = Kt;
-      tc::mbar_arrive(rdyA);
-      tc::mbar_arrive(tstart);
-      float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;   // consumed after the slot rounds (latency hidden)
-      if (pv) {
-        ld0 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 0) << 16);
-        ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
-        ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
-      }
-      if (ntile < ntiles) fill(buf ^ 1, np, nm, npv);   // buffer buf^1 was last read by the previous tile's MMAs
-      const int nnpe = nntile < ntiles ? (int)__ldg(perm + nntile * 128 + r) : 0;   // decoded next iteration
-      TBP_NOW(tp_t1);
-      TBP_ADD(1, tp_t0, tp_t1);
-      TBP_ADD(10, 0, Kt + 1);
-      TBP_ADD(11, 0, 1);
-      // ---- slot rounds: A2 of slot t -> TMEM
-#pragma unroll 1
-      for (int t = 0; t < Kt; ++t) {
-        TBP_NOW(tp_r0);
-        tc::mbar_wait(done1, d1ph); d1ph ^= 1;   // batch t-1: acc1 holds slot t
-        tc::fence_after_sync();
-        TBP_NOW(tp_r1);
-        TBP_ADD(3, tp_r0, tp_r1);
-        uint32_t u[H];
-#pragma unroll
-        for (int c = 0; c < H / 32; ++c)
-          tc::tmem_ld32(t_acc1 + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c));
-        tc::tmem_ld_wait();
-        uint32_t o[H / 2];
-#pragma unroll
-        for (int i = 0; i < H / 2; ++i)
-          o[i] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * i]) + prm.b1[2 * i],
-                                     __uint_as_float(u[2 * i + 1]) + prm.b1[2 * i + 1]);
-#pragma unroll
-        for (int c = 0; c < H / 32; ++c) tc::tmem_st16(t_a2 + lane_off + 16 * c, o + 16 * c);
-        tc::tmem_st_wait();
-        tc::fence_before_sync();
-        tc::mbar_arrive(rdyA);
-        TBP_NOW(tp_r2);
-        TBP_ADD(4, tp_r1, tp_r2);
-      }
-      // ---- final
-      TBP_NOW(tp_f0);
-      tc::mbar_wait(doneF, dfph); dfph ^= 1;     // accB
+      tc::mbar_wait(doneF, fph); fph ^= 1;
       tc::fence_after_sync();
-      TBP_NOW(tp_f1);
-      TBP_ADD(6, tp_f0, tp_f1);
+      // ---- phi and psi
       const float* WO = prm.WO;
       float ps0 = prm.bO[0], ps1 = prm.bO[1], ps2 = prm.bO[2];
       ps0 = fmaf(WO[0 * NO + C0 + 0], ld0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], ld1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], ld2, ps0);
       ps1 = fmaf(WO[1 * NO + C0 + 0], ld0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], ld1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], ld2, ps1);
       ps2 = fmaf(WO[2 * NO + C0 + 0], ld0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], ld1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], ld2, ps2);
       const float fm = (float)m;
+#ifndef GN_ABL_NO_EPI3
 #pragma unroll
       for (int c = 0; c < C0 / 16; ++c) {
         uint32_t u[16];
@@ -474,21 +439,135 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           ps2 = fmaf(WO[2 * NO + o], phi, ps2);
         }
       }
-      if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
+#endif
       tc::fence_before_sync();
+      if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
+    }
+  } else {
+    // ------------------------------------------------------------------ E1: records, A2
+    const int r = threadIdx.x & 127, warp = r >> 5, lane = r & 31;
+    const int bar_id = 1 + g;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    uint32_t d1ph = 0, kph = 0;
+    auto rowword = [&](long tl, int pe) -> long long {   // this thread's row of tile tl: pixel | count << 32, -1 if absent
+      const long long pp = tl / TB_SBT * TB_SBP + (pe & 2047);
+      return (tl < ntiles && pp < P) ? (pp | ((long long)(pe >> 11) << PXB)) : -1ll;
+    };
+    // copy the records of tile rows `nr` (pixel | count) into operand buffer `buf`:
+    // chunk c = i*128 + r is 16-byte piece c % NPL of row c / NPL, zero beyond the valid records
+    auto fill = [&](int buf, const volatile long long* nr) {
+      const uint32_t a = sA1 + buf * S::A1_PL * PL;
+#pragma unroll
+      for (int i = 0; i < S::NPL; ++i) {
+        const int c = i * 128 + r, pr = c / S::NPL, j = c % S::NPL;
+        const long long x = nr[pr];
+        const int vb = x >= 0 ? (int)(x >> PXB) * 22 : 0;
+        const long pp = x >= 0 ? (long)(x & 0xFFFFFFFFll) : 0;
+#ifdef GN_ABL_NO_FILL
+        if (false) {
+#else
+        if (S::ASYNC) {
+#endif
+          const char* src = reinterpret_cast<const char*>(tbuf + pp * (K * 11)) + 16 * j;
+          cp_async16z(a + j * PL + pr * 16, src, (uint32_t)min(max(vb - 16 * j, 0), 16));
+        } else {   // rows not 16-byte aligned in global memory: through registers
+          const uint16_t* src = tbuf + pp * (K * 11);
+          uint32_t w[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int e = 8 * j + 2 * h;
+            const uint32_t lo = 2 * e < vb ? __ldg(src + e) : 0u, hi = 2 * e + 2 < vb ? __ldg(src + e + 1) : 0u;
+            w[h] = lo | (hi << 16);
+          }
+          tc::sts128(a + j * PL + pr * 16, w[0], w[1], w[2], w[3]);
+        }
+      }
+      cp_async_arrive(loadedA + buf);
+    };
+
+    // Tile pipeline: tile ids are claimed three ahead (atomics), the perm entry of the tile
+    // after next is loaded one tile ahead, and the next tile's records are copied during
+    // this one, so no global latency sits on a critical path.
+    int claim = 0;
+    if (r == 0) { red[5] = atomicAdd(sched, 1); red[6] = atomicAdd(sched, 1); claim = atomicAdd(sched, 1); }
+    tc::bar_sync(bar_id, 128);
+    long tile = red[5], ntile = red[6];
+    long long cur = rowword(tile, tile < ntiles ? (int)__ldg(perm + tile * 128 + r) : 0);
+    long long nxt = rowword(ntile, ntile < ntiles ? (int)__ldg(perm + ntile * 128 + r) : 0);
+    if (tile < ntiles) {   // tile 0's records
+      nrows[128 + r] = cur;
+      tc::bar_sync(bar_id, 128);
+      fill(0, nrows + 128);
+    }
+    int it = 0;
+    for (; tile < ntiles; ++it) {
+      TBP_NOW(tp_t0);
+      const int buf = it & 1;
+      const int m = cur >= 0 ? (int)(cur >> PXB) : 0;
+      // ---- prologue: publish this tile's rows (E2) and the next tile's (the fill)
+      if (it >= 1) { tc::mbar_wait(tack, kph); kph ^= 1; }   // E2 has read tile it-1's rows
+      rows[buf * 128 + r] = cur;
+      nrows[buf * 128 + r] = nxt;
+      {
+        const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
+        if (lane == 0) ktv[2 + warp] = wm;
+        if (r == 0) { red[5 + (it + 2) % 3] = claim; claim = atomicAdd(sched, 1); }
+      }
+      tc::bar_sync(bar_id, 128);
+      const int Kt = max(max(ktv[2], ktv[3]), max(ktv[4], ktv[5]));
+      const long nntile = red[5 + (it + 2) % 3];
+      if (r == 0) ktv[buf] = Kt;
+      tc::bar_sync(bar_id, 128);   // ktv[2..5] read by all before the next tile rewrites them
+      tc::mbar_arrive(rdyP);
+      tc::mbar_arrive(tstart);
+      if (ntile < ntiles) fill(buf ^ 1, nrows + buf * 128);   // buffer buf^1: last read by tile it-1's layer 1
+      const int nnpe = nntile < ntiles ? (int)__ldg(perm + nntile * 128 + r) : 0;   // used next iteration
+      TBP_NOW(tp_t1);
+      TBP_ADD(1, tp_t0, tp_t1);
+      TBP_ADD(10, 0, Kt + 1);
+      TBP_ADD(11, 0, 1);
+      if (Kt == 0) { tc::mbar_wait(done1, d1ph); d1ph ^= 1; }   // the (empty) prologue batch
+      // ---- slot rounds: A2 of slot t -> TMEM
+#pragma unroll 1
+      for (int t = 0; t < Kt; ++t) {
+        TBP_NOW(tp_r0);
+        tc::mbar_wait(done1, d1ph); d1ph ^= 1;   // the batch holding layer 1 of slot t
+        tc::fence_after_sync();
+        TBP_NOW(tp_r1);
+        TBP_ADD(3, tp_r0, tp_r1);
+#ifndef GN_ABL_NO_EPI1
+        uint32_t u[H];
+#pragma unroll
+        for (int c = 0; c < H / 32; ++c)
+          tc::tmem_ld32(t_acc1 + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c));
+        tc::tmem_ld_wait();
+        uint32_t o[H / 2];
+#pragma unroll
+        for (int i = 0; i < H / 2; ++i)
+          o[i] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * i]) + prm.b1[2 * i],
+                                     __uint_as_float(u[2 * i + 1]) + prm.b1[2 * i + 1]);
+#pragma unroll
+        for (int c = 0; c < H / 32; ++c) tc::tmem_st16(t_a2 + lane_off + 16 * c, o + 16 * c);
+        tc::tmem_st_wait();
+#endif
+        tc::fence_before_sync();
+        tc::mbar_arrive(rdyA);
+        TBP_NOW(tp_r2);
+        TBP_ADD(4, tp_r1, tp_r2);
+      }
       TBP_NOW(tp_end);
-      TBP_ADD(8, tp_f1, tp_end);
       TBP_ADD(9, tp_t0, tp_end);
       // advance the tile pipeline
-      tile = ntile; p = np; m = nm; pv = npv;
+      tile = ntile; cur = nxt;
       ntile = nntile;
-      decode(ntile, nnpe, np, nm, npv);
+      nxt = rowword(ntile, nnpe);
     }
     // stop the MMA warp and E2
+    if (it >= 1) { tc::mbar_wait(tack, kph); kph ^= 1; }
     tc::bar_sync(bar_id, 128);
-    if (r == 0) red[4] = -1;
+    if (r == 0) ktv[it & 1] = -1;
     tc::bar_sync(bar_id, 128);
-    tc::mbar_arrive(rdyA);
+    tc::mbar_arrive(rdyP);
     tc::mbar_arrive(tstart);
   }
   tc::fence_before_sync();

@@ -410,8 +410,12 @@ static int launch_tb_tc_h(glassnet* net, const __nv_bfloat16* tbuf, const uint8_
                           const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   switch (net->d.k_slots) {
 #define KCASE(k) case k: return launch_tb_tc_k<k, H, C0>(net, tbuf, tcount, e0, direct, psi, P, st);
+#ifdef GN_DIAG_K8_ONLY   // diagnostic builds: the bench configuration only (fast to compile)
+    KCASE(8)
+#else
     KCASE(1) KCASE(2) KCASE(3) KCASE(4) KCASE(5) KCASE(6) KCASE(7) KCASE(8)
     KCASE(9) KCASE(10) KCASE(11) KCASE(12) KCASE(13) KCASE(14) KCASE(15) KCASE(16)
+#endif
 #undef KCASE
   }
   return gn_fail(GLASSNET_ERR_UNSUPPORTED, "k_slots");
@@ -421,9 +425,11 @@ inline int tc_launch_tb(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t*
                         const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   const int H = net->d.t_hidden, C0 = net->d.widths[0];
   if (H == 64 && C0 == 32) return launch_tb_tc_h<64, 32>(net, tbuf, tcount, e0, direct, psi, P, st);
+#ifndef GN_DIAG_K8_ONLY
   if (H == 32 && C0 == 16) return launch_tb_tc_h<32, 16>(net, tbuf, tcount, e0, direct, psi, P, st);
   if (H == 32 && C0 == 32) return launch_tb_tc_h<32, 32>(net, tbuf, tcount, e0, direct, psi, P, st);
   if (H == 64 && C0 == 16) return launch_tb_tc_h<64, 16>(net, tbuf, tcount, e0, direct, psi, P, st);
+#endif
   return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core T kernel: (t_hidden, widths[0]) = (%d, %d)", H, C0);
 }
 

@@ -21,9 +21,8 @@ net.forward(g, d, t, n); torch.cuda.synchronize()
 L.glassnet_debug_tb_prof(buf, 0)
 v = list(buf)
 tiles, rounds = v[11], v[10] - v[11]
-names = {1: "E1 prologue (counts, next tile's cp.async)", 3: "E1 round: wait for acc1 (layer-1 batch)",
-         4: "E1 round: epilogue 1 (acc1 -> A2 in TMEM) + arrive", 6: "E1 final: wait for accB",
-         8: "E1 epilogue 3 (phi, psi)", 9: "tile total"}
+names = {1: "E1 prologue (rows, next tile's records cp.async)", 3: "E1 round: wait for acc1 (layer-1 batch)",
+         4: "E1 round: epilogue 1 (acc1 -> A2 in TMEM) + arrive", 9: "E1 tile total"}
 print(f"tiles={tiles} rounds={rounds} rounds/tile={rounds / max(tiles, 1):.2f}")
 for i, nm in names.items():
     print(f"{nm:50s} {v[i] / max(tiles, 1):8.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):6.0f} cyc/round" if i in (3, 4) else ""))
