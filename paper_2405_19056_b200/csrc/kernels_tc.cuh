@@ -389,8 +389,8 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   auto kfn = k_tb_tc<K, H, C0, POOL>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   const long ntiles = nsb * TB_SBT;
-  long grid = net->num_sms;
-  if (grid * S::NCH > ntiles) grid = (ntiles + S::NCH - 1) / S::NCH;
+  long grid = net->num_sms;   // one streaming pipeline per SM; tiles are claimed dynamically
+  if (grid > ntiles) grid = ntiles;
   cudaMemsetAsync(s->sched, 0, sizeof(int), st);
   kfn<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), reinterpret_cast<const uint16_t*>(e0),

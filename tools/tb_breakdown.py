@@ -21,8 +21,9 @@ net.forward(g, d, t, n); torch.cuda.synchronize()
 L.glassnet_debug_tb_prof(buf, 0)
 v = list(buf)
 tiles, rounds = v[11], v[10] - v[11]
-names = {1: "E1 prologue (rows, next tile's records cp.async)", 3: "E1 round: wait for acc1 (layer-1 batch)",
-         4: "E1 round: epilogue 1 (acc1 -> A2 in TMEM) + arrive", 9: "E1 tile total"}
+names = {1: "E1 publish next tile (+ tile ids)", 3: "E1 slot: wait for L1 (d1)",
+         4: "E1 slot: epilogue 1 (acc1 -> A2 in TMEM) + arrive", 9: "E1 tile total",
+         12: "MMA slot: wait rdyA (E1)", 13: "MMA slot: wait free2 (E2)", 14: "MMA slot: issue L2", 15: "MMA slot: issue L1"}
 print(f"tiles={tiles} rounds={rounds} rounds/tile={rounds / max(tiles, 1):.2f}")
 for i, nm in names.items():
-    print(f"{nm:50s} {v[i] / max(tiles, 1):8.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):6.0f} cyc/round" if i in (3, 4) else ""))
+    print(f"{nm:50s} {v[i] / max(tiles, 1):8.0f} cyc/tile" + (f"  {v[i] / max(rounds, 1):6.0f} cyc/round" if i in (3, 4, 12, 13, 14, 15) else ""))
