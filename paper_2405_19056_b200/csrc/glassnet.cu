@@ -568,11 +568,6 @@ extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int
   return GLASSNET_OK;
 }
 
-#ifdef GN_TB_DEBUG
-extern "C" int glassnet_debug_tb_hang(int* dev_mapped) {   // device pointer of mapped host memory
-  return cudaMemcpyToSymbol(gn::gn_tb_hang, &dev_mapped, sizeof(int*)) == cudaSuccess ? 0 : 3;
-}
-#endif
 #ifdef GN_PROFILE_TB
 extern "C" int glassnet_debug_tb_prof(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();

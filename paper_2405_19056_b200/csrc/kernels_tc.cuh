@@ -389,8 +389,8 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   auto kfn = k_tb_tc<K, H, C0, POOL>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   const long ntiles = nsb * TB_SBT;
-  long grid = net->num_sms;   // one streaming pipeline per SM; tiles are claimed dynamically
-  if (grid > ntiles) grid = ntiles;
+  long grid = net->num_sms;
+  if (grid * S::NCH > ntiles) grid = (ntiles + S::NCH - 1) / S::NCH;
   cudaMemsetAsync(s->sched, 0, sizeof(int), st);
   kfn<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), reinterpret_cast<const uint16_t*>(e0),
@@ -425,11 +425,9 @@ inline int tc_launch_tb(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t*
                         const __nv_bfloat16* direct, float* psi, long P, cudaStream_t st) {
   const int H = net->d.t_hidden, C0 = net->d.widths[0];
   if (H == 64 && C0 == 32) return launch_tb_tc_h<64, 32>(net, tbuf, tcount, e0, direct, psi, P, st);
-#ifndef GN_DIAG_K8_ONLY
   if (H == 32 && C0 == 16) return launch_tb_tc_h<32, 16>(net, tbuf, tcount, e0, direct, psi, P, st);
   if (H == 32 && C0 == 32) return launch_tb_tc_h<32, 32>(net, tbuf, tcount, e0, direct, psi, P, st);
   if (H == 64 && C0 == 16) return launch_tb_tc_h<64, 16>(net, tbuf, tcount, e0, direct, psi, P, st);
-#endif
   return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tensor-core T kernel: (t_hidden, widths[0]) = (%d, %d)", H, C0);
 }
 

@@ -28,6 +28,10 @@ __global__ void k_issue(long long* out, int nrep, int mode) {
     long long c0 = clock64();
     for (int it = 0; it < nrep; ++it) {
       const int b = it & 1;
+      if (mode >= 4) {   // an already-completed mbarrier wait (+ fence) before each batch
+        tc::mbar_wait(&bar[3], 1);
+        if (mode == 5) tc::fence_after_sync();
+      }
       if (mode != 2)
         for (int q = 0; q < 4; ++q)
           tc::mma_f16_ts(tmem + 192 + b * 64, tmem + 128 + b * 32 + q * 8, tc::smem_desc(sW2 + 2 * q * 1024, 1024, 128), ID, q > 0);
@@ -53,8 +57,9 @@ int main() {
   long long h[256];
   const int nsm = 148, nrep = 2000;
   cudaFuncSetAttribute(k_issue, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  const char* names[] = {"4 TS + commit + 1 SS + commit", "4 TS + commits only", "1 SS + commits only", "4 TS + 1 SS, no commits"};
-  for (int mode = 0; mode < 4; ++mode) {
+  const char* names[] = {"4 TS + commit + 1 SS + commit", "4 TS + commits only", "1 SS + commits only", "4 TS + 1 SS, no commits",
+                         "mode0 + completed mbar wait", "mode0 + mbar wait + fence"};
+  for (int mode = 0; mode < 6; ++mode) {
     k_issue<<<nsm, 128, 140 * 1024>>>(d, nrep, mode);
     k_issue<<<nsm, 128, 140 * 1024>>>(d, nrep, mode);
     cudaError_t e = cudaDeviceSynchronize();
