@@ -276,3 +276,30 @@ def test_weight_count_matches_survey():
     assert oracle.weight_count(oracle.make_dims(64, 64, 4, (16, 32, 64), 32)) == 50700
     assert oracle.weight_count(oracle.make_dims(64, 64, 8, (32, 64, 128, 256), 64)) == 787340
     assert synth.weight_count((16, 32, 64), 3, 32) == 50700
+
+
+# ----------------------------------------------------------------------------- R5 range
+def test_R5_pool_fixed_point_range():
+    """Reading R5: the GPU pools each fragment's layer-2 output as a fixed-point
+    integer round(a2 * 2^12) saturated at 2^23 (a2 < 2048), which makes the sum exact and
+    order-independent.  Pin that the saturation never binds for the workloads: the oracle's
+    per-fragment a2 (T_pixel with n = 1 returns one fragment's h(b)) over a sample of
+    records drawn as in BJ.configs (K = 16, the c4 slot count; the c1-c4 network, seed-0
+    He weights; records in bf16) stays far below 2048."""
+    cfg = synth.Config("r5", 24, 32, 1, 16, 4, (32, 64, 128, 256), 64, "bf16")
+    fr = synth.gen_frames(cfg, seed=3)
+    _, _, t64, _ = fr.as64()
+    wts = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True).astype(np.float64)
+    d = oracle.make_dims(1, 1, 16, cfg.widths, cfg.t_hidden)
+    w = oracle.split_weights(d, wts)
+    recs = t64[0].reshape(-1, 16, 11)
+    amax = 0.0
+    for px in range(0, recs.shape[0], 3):
+        for k in range(16):
+            one = np.zeros((16, 11))
+            one[0] = recs[px, k]
+            tau = oracle.T_pixel(d, w["T1.W"], w["T1.b"], w["T2.W"], w["T2.b"], one, 1)
+            amax = max(amax, float(tau[:64].max()))
+    assert tau[64] == 1.0
+    print(f"max per-fragment a2 over {recs.shape[0] // 3 * 16} records: {amax:.3f} (saturation 2048)")
+    assert 0.0 < amax < 2048.0 / 16
