@@ -9,8 +9,11 @@
 // memory (zero fill outside the image = the conv's zero padding) in the K-major
 // "interleaved" core-matrix layout, and each of the 9 taps is a shifted UMMA descriptor
 // into that halo (stride 2 uses even/odd de-interleaved halos so every tap is affine).
-// The weights of the CTA's N-split stay resident in shared memory for the whole
-// persistent kernel.  Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner),
+// Weights: either resident in shared memory for the whole persistent kernel (the CTA's
+// N-split), or -- when a full-width layer does not fit (WS = 1: F3, R3) -- streamed with the
+// halo: each pipeline stage then carries the 16-channel chunk's 9 x 16 x Cout weights too
+// (one bulk copy), so N = Cout in one pass instead of re-reading the halo per N-split.
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner),
 // 2..5 = epilogue (TMEM -> bias/ReLU -> bf16 NHWC store, or the z projection of R_1).
 // Accumulators are double-buffered in TMEM so the epilogue overlaps the next tile.
 #pragma once
@@ -56,7 +59,7 @@ __device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* m, int c
 }
 
 struct ConvArgs {
-  const uint8_t* wimg;   // [nsplit][9][Cin/8][NS][8] bf16 (K-major planes)
+  const uint8_t* wimg;   // resident: [nsplit][9][Cin/8][NS][8]; streamed: [Cin/16][9][2][NS][8] bf16 (K-major planes)
   const float* bias;     // [Cout]
   uint16_t* out;         // [B][Ho][Wo][Cout] bf16 (EPI 0)
   const float* wz;       // [3][Cout] (EPI 1)
@@ -68,16 +71,18 @@ struct ConvArgs {
   int out_rows_buf;      // output buffer rows per frame
 };
 
-template <int S, int NS, int EPI>
+template <int S, int NS, int EPI, int WS = 0>
 __global__ void __launch_bounds__(192, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
-  constexpr int SB = 2 * HL::PLANE;                 // one stage = 16 channels = 2 planes
+  constexpr int SBA = 2 * HL::PLANE;                // a stage's halo: 16 channels = 2 planes
+  constexpr int SBW = WS ? 9 * 2 * NS * 16 : 0;     // a stage's streamed weights (9 taps x 2 K-planes)
+  constexpr int SB = SBA + SBW;
   constexpr int TMEM_COLS = (2 * NS) <= 32 ? 32 : (2 * NS) <= 64 ? 64 : (2 * NS) <= 128 ? 128 : (2 * NS) <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Cin = a.Cin, NST = a.nstage;
-  const int wbytes = 9 * Cin * NS * 2;
+  const int wbytes = WS ? 0 : 9 * Cin * NS * 2;
   uint8_t* sW = smem;
   uint8_t* sA = smem + ((wbytes + 1023) / 1024) * 1024;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sA + NST * SB);
@@ -88,7 +93,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int split = blockIdx.x % a.nsplit;
-  {  // resident weights of this split
+  if (!WS) {  // resident weights of this split
     const int4* src = reinterpret_cast<const int4*>(a.wimg + (size_t)split * wbytes);
     int4* dst = reinterpret_cast<int4*>(sW);
     for (int i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
@@ -122,8 +127,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int x0 = xt * TILE_M;
         for (int c = 0; c < nchunk; ++c) {
           tc::mbar_wait(empty + stage, ph ^ 1);
-          tc::mbar_arrive_expect_tx(full + stage, 2 * HL::TX);
+          tc::mbar_arrive_expect_tx(full + stage, 2 * HL::TX + SBW);
           const uint32_t dst = tc::smem_u32(sA + stage * SB);
+          if (WS) tc::bulk_g2s(sA + stage * SB + SBA, a.wimg + (size_t)c * SBW, SBW, full + stage);
           for (int j = 0; j < 2; ++j) {
             const int ch = (2 * c + j) * 8;
             const int iy = S * oy - 1 + a.in_row_off;
@@ -159,7 +165,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (S == 1) aoff = (ky * Halo<1>::SLOTS + kx) * 16;
             else aoff = kx == 1 ? ky * TILE_M * 16 : Halo<2>::ODD_OFF + (ky * (TILE_M + 1) + (kx == 2 ? 1 : 0)) * 16;
             const uint64_t ad = tc::smem_desc(base + aoff, HL::PLANE, 128);
-            const uint64_t bd = tc::smem_desc(sWa + (uint32_t)((tap * (Cin / 8) + 2 * c) * NS * 16), NS * 16, 128);
+            const uint64_t bd = WS ? tc::smem_desc(base + SBA + tap * 2 * NS * 16, NS * 16, 128)
+                                   : tc::smem_desc(sWa + (uint32_t)((tap * (Cin / 8) + 2 * c) * NS * 16), NS * 16, 128);
             tc::mma_f16_ss(d, ad, bd, IDESC, (c | tap) != 0);
           }
           tc::mma_commit(empty + stage);

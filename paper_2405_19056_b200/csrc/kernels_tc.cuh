@@ -19,7 +19,7 @@ namespace gn {
 // Weights-level description of one conv layer (packed once per handle).
 struct TcConv {
   bool used = false;
-  int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0;
+  int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0, ws = 0;   // ws: weights streamed
   size_t smem = 0;
   int ctas_per_sm = 1;
   uint8_t* wimg = nullptr;
@@ -204,9 +204,10 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C) {
   return 0;
 }
 
-static size_t conv_smem(int S, int Cin, int NS, int nstage) {
-  const size_t sb = 2 * (S == 1 ? conv::Halo<1>::PLANE : conv::Halo<2>::PLANE);
-  return (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024 + nstage * sb + (2 * nstage + 4) * 8 + 16;
+static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0) {
+  const size_t sb = 2 * (S == 1 ? conv::Halo<1>::PLANE : conv::Halo<2>::PLANE) + (ws ? (size_t)9 * 2 * NS * 16 : 0);
+  const size_t w = ws ? 0 : (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024;
+  return w + nstage * sb + (2 * nstage + 4) * 8 + 16;
 }
 
 // One conv layer: choose the N split so the split's weights stay resident, pack them.
@@ -215,20 +216,26 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
   constexpr size_t LIMIT = 232448 - 1024;
   L.used = true; L.S = S; L.Cin = Cin; L.Cout = Cout; L.epi = epi;
   int NS = Cout;
-  while (NS > 16 && conv_smem(S, Cin, NS, 2) > LIMIT) NS /= 2;
-  if (conv_smem(S, Cin, NS, 2) > LIMIT || (epi == 1 && NS != Cout))
+  // full width with resident weights if they fit; else full width with the weights streamed
+  // per channel chunk (no N-split: an N-split re-reads the halo and multiplies the MMA count)
+  L.ws = (conv_smem(S, Cin, Cout, 2) > LIMIT && Cout <= 256 && conv_smem(S, Cin, Cout, 2, 1) <= LIMIT && epi == 0 &&
+          !getenv("GN_CONV_NO_STREAM")) ? 1 : 0;
+  if (!L.ws)
+    while (NS > 16 && conv_smem(S, Cin, NS, 2) > LIMIT) NS /= 2;
+  if (conv_smem(S, Cin, NS, 2, L.ws) > LIMIT || (epi == 1 && NS != Cout))
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv %d->%d does not fit shared memory", Cin, Cout);
   L.NS = NS;
   L.nsplit = Cout / NS;
   L.nstage = 4;
-  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage) > LIMIT) --L.nstage;
-  L.smem = conv_smem(S, Cin, NS, L.nstage);
+  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws) > LIMIT) --L.nstage;
+  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws);
   const int tcols = 2 * NS <= 32 ? 32 : 2 * NS <= 64 ? 64 : 2 * NS <= 128 ? 128 : 2 * NS <= 256 ? 256 : 512;
   L.ctas_per_sm = (int)(232448 / (L.smem + 1024));
   if (L.ctas_per_sm > 2) L.ctas_per_sm = 2;
   if (L.ctas_per_sm * tcols > 512) L.ctas_per_sm = 512 / tcols;
   if (L.ctas_per_sm < 1) L.ctas_per_sm = 1;
-  // weights: [split][tap][Cin/8][NS][8] bf16
+  // weights: resident [split][tap][Cin/8][NS][8]; streamed [Cin/16][tap][2][NS][8] (one
+  // contiguous block per 16-channel chunk) -- bf16
   std::vector<uint16_t> img((size_t)L.nsplit * 9 * Cin * NS, 0);
   for (int sp = 0; sp < L.nsplit; ++sp)
     for (int t = 0; t < 9; ++t)
@@ -237,7 +244,9 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
           for (int kk = 0; kk < 8; ++kk) {
             const int co = sp * NS + n, ci = 8 * j + kk;
             const float v = ci < cin_real ? W[((size_t)co * 9 + t) * cin_real + ci] : 0.f;
-            img[((((size_t)sp * 9 + t) * (Cin / 8) + j) * NS + n) * 8 + kk] = h_bf16(v);
+            const size_t idx = L.ws ? (((((size_t)(j / 2) * 9 + t) * 2 + (j % 2)) * NS + n) * 8 + kk)
+                                    : (((((size_t)sp * 9 + t) * (Cin / 8) + j) * NS + n) * 8 + kk);
+            img[idx] = h_bf16(v);
           }
   if (cudaMalloc(&L.wimg, img.size() * 2) != cudaSuccess)
     return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "conv weight image");
@@ -337,9 +346,9 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
   return 0;
 }
 
-template <int S, int NS, int EPI>
+template <int S, int NS, int EPI, int WS = 0>
 static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
-  auto kfn = conv::k_conv_tc<S, NS, EPI>;
+  auto kfn = conv::k_conv_tc<S, NS, EPI, WS>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   conv::ConvArgs a;
   a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
@@ -354,7 +363,11 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
 #define CONV_CASE(S_, NS_, E_) \
-  if (L.S == S_ && L.NS == NS_ && L.epi == E_) { launch_conv_k<S_, NS_, E_>(net, L, G, B, st); return 0; }
+  if (L.S == S_ && L.NS == NS_ && L.epi == E_ && !L.ws) { launch_conv_k<S_, NS_, E_>(net, L, G, B, st); return 0; }
+#define CONV_CASE_WS(S_, NS_) \
+  if (L.S == S_ && L.NS == NS_ && L.epi == 0 && L.ws) { launch_conv_k<S_, NS_, 0, 1>(net, L, G, B, st); return 0; }
+  CONV_CASE_WS(1, 64) CONV_CASE_WS(1, 128) CONV_CASE_WS(1, 256) CONV_CASE_WS(2, 64) CONV_CASE_WS(2, 128) CONV_CASE_WS(2, 256)
+#undef CONV_CASE_WS
   CONV_CASE(1, 16, 0) CONV_CASE(1, 32, 0) CONV_CASE(1, 64, 0) CONV_CASE(1, 128, 0) CONV_CASE(1, 256, 0)
   CONV_CASE(2, 16, 0) CONV_CASE(2, 32, 0) CONV_CASE(2, 64, 0) CONV_CASE(2, 128, 0) CONV_CASE(2, 256, 0)
   CONV_CASE(1, 16, 1) CONV_CASE(1, 32, 1)
