@@ -71,7 +71,18 @@ struct ConvArgs {
   int out_rows_buf;      // output buffer rows per frame
 };
 
-template <int S, int NS, int EPI, int WS = 0>
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+
+// OST = 1: the epilogue stages each warp's 32 output pixels (32 x NS bf16, contiguous in NHWC)
+// in shared memory and writes them with one bulk copy (full, coalesced lines) instead of
+// 16-byte per-thread stores that touch every sector twice.
+template <int S, int NS, int EPI, int WS = 0, int OST = 0>
 __global__ void __launch_bounds__(192, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
@@ -91,6 +102,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sBias = reinterpret_cast<float*>(tempty + 4);                        // NS floats
+  uint8_t* sOut = reinterpret_cast<uint8_t*>(sBias) + ((NS * 4 + 127) / 128) * 128;   // OST: [4 warps][2][32][NS] bf16
 
   const int split = blockIdx.x % a.nsplit;
   if (!WS) {  // resident weights of this split
@@ -98,6 +111,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int4* dst = reinterpret_cast<int4*>(sW);
     for (int i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
   }
+  for (int i = tid; i < NS; i += blockDim.x) sBias[i] = a.bias[split * NS + i];
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(tfull + i, 1); tc::mbar_init(tempty + i, 128); }
@@ -180,8 +194,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int q = warp & 3;               // TMEM lane quarter of this warp
     const int m = q * 32 + lane;
     const int co0 = split * NS;
-    int acc = 0;
+    int acc = 0, sb = 0;
     uint32_t aph = 0;
+    constexpr uint32_t WBUF = 32 * NS * 2;     // one warp's staged output (OST)
     for (long t = cta; t < ntiles; t += ncta) {
       const int xt = (int)(t % ntx);
       const long r = t / ntx;
@@ -193,6 +208,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       tc::mbar_wait(tfull + acc, aph);
       tc::fence_after_sync();
       const uint32_t taddr = tmem + acc * NS + ((uint32_t)(q * 32) << 16);
+      const uint32_t stg = tc::smem_u32(sOut) + (q * 2 + sb) * WBUF;
+      if (OST) {   // this warp's staging buffer sb: its bulk copy (two tiles ago) has read it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+      }
       float z0 = 0.f, z1 = 0.f, z2 = 0.f;
 #pragma unroll 1
       for (int c = 0; c < NS / 16; ++c) {
@@ -201,8 +221,15 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc::tmem_ld_wait();
         float y[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) y[i] = relu(__uint_as_float(v[i]) + __ldg(a.bias + co0 + c * 16 + i));
-        if (EPI == 0) {
+        for (int i = 0; i < 16; ++i) y[i] = relu(__uint_as_float(v[i]) + sBias[c * 16 + i]);
+        if (EPI == 0 && OST) {
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) w[i] = tc::cvt_bf16x2(y[2 * i], y[2 * i + 1]);
+          const uint32_t dst = stg + lane * (NS * 2) + c * 32;
+          tc::sts128(dst, w[0], w[1], w[2], w[3]);
+          tc::sts128(dst + 16, w[4], w[5], w[6], w[7]);
+        } else if (EPI == 0) {
           if (valid) {
             uint32_t w[8];
 #pragma unroll
@@ -226,8 +253,23 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
       tc::fence_before_sync();
       tc::mbar_arrive(tempty + acc);
+      if (OST) {   // the warp's 32 pixels are contiguous in NHWC: one bulk copy
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int px0 = xt * TILE_M + q * 32;
+          const int nv = min(32, a.Wo - px0);
+          if (nv > 0) {
+            const long opix0 = ((long)b * a.out_rows_buf + oy + a.out_row_off) * a.Wo + px0;
+            bulk_s2g(a.out + opix0 * a.Cout, stg, (uint32_t)(nv * NS * 2));
+          }
+          bulk_commit();
+        }
+        sb ^= 1;
+      }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    if (OST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc::fence_before_sync();
   __syncthreads();

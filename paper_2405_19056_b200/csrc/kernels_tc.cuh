@@ -19,7 +19,7 @@ namespace gn {
 // Weights-level description of one conv layer (packed once per handle).
 struct TcConv {
   bool used = false;
-  int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0, ws = 0;   // ws: weights streamed
+  int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0, ws = 0, ost = 0;   // ws: weights streamed, ost: staged output
   size_t smem = 0;
   int ctas_per_sm = 1;
   uint8_t* wimg = nullptr;
@@ -204,10 +204,11 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C) {
   return 0;
 }
 
-static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0) {
+static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost = 0) {
   const size_t sb = 2 * (S == 1 ? conv::Halo<1>::PLANE : conv::Halo<2>::PLANE) + (ws ? (size_t)9 * 2 * NS * 16 : 0);
   const size_t w = ws ? 0 : (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024;
-  return w + nstage * sb + (2 * nstage + 4) * 8 + 16;
+  const size_t bias = ((size_t)NS * 4 + 127) / 128 * 128;
+  return w + nstage * sb + (2 * nstage + 4) * 8 + bias + (ost ? (size_t)4 * 2 * 32 * NS * 2 : 0) + 128;
 }
 
 // One conv layer: choose the N split so the split's weights stay resident, pack them.
@@ -228,7 +229,9 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
   L.nsplit = Cout / NS;
   L.nstage = 4;
   while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws) > LIMIT) --L.nstage;
-  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws);
+  // staged (bulk-copied) output when it fits without giving up pipeline depth
+  L.ost = (epi == 0 && conv_smem(S, Cin, NS, L.nstage, L.ws, 1) <= LIMIT && !getenv("GN_CONV_NO_OST")) ? 1 : 0;
+  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws, L.ost);
   const int tcols = 2 * NS <= 32 ? 32 : 2 * NS <= 64 ? 64 : 2 * NS <= 128 ? 128 : 2 * NS <= 256 ? 256 : 512;
   L.ctas_per_sm = (int)(232448 / (L.smem + 1024));
   if (L.ctas_per_sm > 2) L.ctas_per_sm = 2;
@@ -346,9 +349,9 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
   return 0;
 }
 
-template <int S, int NS, int EPI, int WS = 0>
+template <int S, int NS, int EPI, int WS = 0, int OST = 0>
 static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
-  auto kfn = conv::k_conv_tc<S, NS, EPI, WS>;
+  auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   conv::ConvArgs a;
   a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
@@ -363,7 +366,12 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
 #define CONV_CASE(S_, NS_, E_) \
-  if (L.S == S_ && L.NS == NS_ && L.epi == E_ && !L.ws) { launch_conv_k<S_, NS_, E_>(net, L, G, B, st); return 0; }
+  if (L.S == S_ && L.NS == NS_ && L.epi == E_ && !L.ws && !L.ost) { launch_conv_k<S_, NS_, E_>(net, L, G, B, st); return 0; }
+#define CONV_CASE_OST(S_, NS_) \
+  if (L.S == S_ && L.NS == NS_ && L.epi == 0 && !L.ws && L.ost) { launch_conv_k<S_, NS_, 0, 0, 1>(net, L, G, B, st); return 0; }
+  CONV_CASE_OST(1, 16) CONV_CASE_OST(1, 32) CONV_CASE_OST(1, 64) CONV_CASE_OST(1, 128)
+  CONV_CASE_OST(2, 16) CONV_CASE_OST(2, 32) CONV_CASE_OST(2, 64) CONV_CASE_OST(2, 128)
+#undef CONV_CASE_OST
 #define CONV_CASE_WS(S_, NS_) \
   if (L.S == S_ && L.NS == NS_ && L.epi == 0 && L.ws) { launch_conv_k<S_, NS_, 0, 1>(net, L, G, B, st); return 0; }
   CONV_CASE_WS(1, 64) CONV_CASE_WS(1, 128) CONV_CASE_WS(1, 256) CONV_CASE_WS(2, 64) CONV_CASE_WS(2, 128) CONV_CASE_WS(2, 256)
