@@ -31,7 +31,9 @@ constexpr int TILE_M = 128;
 template <int S> struct Halo;
 template <> struct Halo<1> {
   static constexpr int SLOTS = TILE_M + 2;                       // x0-1 .. x0+128
-  static constexpr int PLANE = (3 * SLOTS * 16 + 127) / 128 * 128;
+  // both 8-channel planes of a 16-channel chunk come from ONE box (a 5-D view whose 4th
+  // dimension is the plane, stride 16 B), so each 32-byte sector is requested once
+  static constexpr int PLANE = 3 * SLOTS * 16;
   static constexpr int TX = 3 * SLOTS * 16;                      // bytes TMA writes per plane
 };
 template <> struct Halo<2> {
@@ -86,7 +88,7 @@ template <int S, int NS, int EPI, int WS = 0, int OST = 0>
 __global__ void __launch_bounds__(192, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
-  constexpr int SBA = 2 * HL::PLANE;                // a stage's halo: 16 channels = 2 planes
+  constexpr int SBA = (2 * HL::PLANE + 127) / 128 * 128;   // a stage's halo: 16 channels = 2 planes (TMA dst: 128-B aligned)
   constexpr int SBW = WS ? 9 * 2 * NS * 16 : 0;     // a stage's streamed weights (9 taps x 2 K-planes)
   constexpr int SB = SBA + SBW;
   constexpr int TMEM_COLS = (2 * NS) <= 32 ? 32 : (2 * NS) <= 64 ? 64 : (2 * NS) <= 128 ? 128 : (2 * NS) <= 256 ? 256 : 512;
@@ -148,7 +150,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const int ch = (2 * c + j) * 8;
             const int iy = S * oy - 1 + a.in_row_off;
             if (S == 1) {
-              tma_4d(dst + j * HL::PLANE, &tmA, ch, x0 - 1, iy, b, full + stage);
+              if (j == 0) tma_5d(dst, &tmA, 0, x0 - 1, iy, 2 * c, b, full + stage);   // both planes
             } else {
               tma_5d(dst + j * HL::PLANE, &tmA, ch, 0, x0, iy, b, full + stage);
               tma_5d(dst + j * HL::PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, iy, b, full + stage);
