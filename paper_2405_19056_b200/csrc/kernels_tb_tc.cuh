@@ -68,7 +68,7 @@ constexpr float TB_QSCALE = 4096.0f;            // pool fixed point: 2^12 per un
 constexpr float TB_QMAGIC = 8388608.0f;         // 2^23
 constexpr float TB_QMAX = 16777215.0f;          // 2^24 - 1 (saturation at 2048 - 2^-12)
 constexpr uint32_t TB_QBITS = 0x4B000000u;      // bits of 2^23
-constexpr int TB_SBT = 8;                       // tiles per superblock (the count sort's window)
+constexpr int TB_SBT = 16;                      // tiles per superblock (the count sort's window)
 constexpr int TB_SBP = TB_SBT * 128;
 
 // Small per-network constants, passed by value so the epilogues read them from the
