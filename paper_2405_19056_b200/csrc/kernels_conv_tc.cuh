@@ -32,9 +32,10 @@ template <int S> struct Halo;
 template <> struct Halo<1> {
   static constexpr int SLOTS = TILE_M + 2;                       // x0-1 .. x0+128
   // both 8-channel planes of a 16-channel chunk come from ONE box (a 5-D view whose 4th
-  // dimension is the plane, stride 16 B), so each 32-byte sector is requested once
-  static constexpr int PLANE = 3 * SLOTS * 16;
-  static constexpr int TX = 3 * SLOTS * 16;                      // bytes TMA writes per plane
+  // dimension is the plane, stride 16 B), so each 32-byte sector is requested once.
+  // A tile of RR output rows reads RR + 2 input rows (planes are RR + 2 rows deep).
+  static constexpr int PLANE = 3 * SLOTS * 16;                   // (RR = 1)
+  static constexpr int TX = 3 * SLOTS * 16;
 };
 template <> struct Halo<2> {
   static constexpr int EVEN = 3 * TILE_M * 16;                   // pixels 2(x0+i)
@@ -84,14 +85,21 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 // OST = 1: the epilogue stages each warp's 32 output pixels (32 x NS bf16, contiguous in NHWC)
 // in shared memory and writes them with one bulk copy (full, coalesced lines) instead of
 // 16-byte per-thread stores that touch every sector twice.
-template <int S, int NS, int EPI, int WS = 0, int OST = 0>
+// RR: output rows per tile (stride 1 only): the RR rows share RR + 2 halo rows (each input
+// row is read from L2 (RR + 2) / RR times instead of 3 times); RR accumulators of NS columns.
+template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1>
 __global__ void __launch_bounds__(192, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
-  constexpr int SBA = (2 * HL::PLANE + 127) / 128 * 128;   // a stage's halo: 16 channels = 2 planes (TMA dst: 128-B aligned)
+  static_assert(S == 1 || RR == 1, "multi-row tiles are stride-1 only");
+  constexpr int PLANE = S == 1 ? (RR + 2) * Halo<1>::SLOTS * 16 : HL::PLANE;
+  constexpr int TXB = S == 1 ? 2 * PLANE : 2 * HL::TX;     // bytes the TMA writes per stage
+  constexpr int SBA = (2 * PLANE + 127) / 128 * 128;   // a stage's halo: 16 channels = 2 planes (TMA dst: 128-B aligned)
   constexpr int SBW = WS ? 9 * 2 * NS * 16 : 0;     // a stage's streamed weights (9 taps x 2 K-planes)
   constexpr int SB = SBA + SBW;
-  constexpr int TMEM_COLS = (2 * NS) <= 32 ? 32 : (2 * NS) <= 64 ? 64 : (2 * NS) <= 128 ? 128 : (2 * NS) <= 256 ? 256 : 512;
+  constexpr int ACC = RR * NS;                      // TMEM columns of one tile's accumulators
+  constexpr int TMEM_COLS = (2 * ACC) <= 32 ? 32 : (2 * ACC) <= 64 ? 64 : (2 * ACC) <= 128 ? 128 : (2 * ACC) <= 256 ? 256 : 512;
+  static_assert(2 * ACC <= 512, "TMEM");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Cin = a.Cin, NST = a.nstage;
@@ -127,7 +135,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const uint32_t tmem = *tptr;
 
   const int ntx = (a.Wo + TILE_M - 1) / TILE_M;
-  const long ntiles = (long)a.B * a.Ho * ntx;
+  const int nry = (a.Ho + RR - 1) / RR;             // row tiles per frame
+  const long ntiles = (long)a.B * nry * ntx;
   const int cta = blockIdx.x / a.nsplit, ncta = gridDim.x / a.nsplit;
   const int nchunk = Cin / 16;
 
@@ -138,12 +147,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (long t = cta; t < ntiles; t += ncta) {
         const int xt = (int)(t % ntx);
         const long r = t / ntx;
-        const int oy = (int)(r % a.Ho);
-        const int b = (int)(r / a.Ho);
+        const int oy = (int)(r % nry) * RR;
+        const int b = (int)(r / nry);
         const int x0 = xt * TILE_M;
         for (int c = 0; c < nchunk; ++c) {
           tc::mbar_wait(empty + stage, ph ^ 1);
-          tc::mbar_arrive_expect_tx(full + stage, 2 * HL::TX + SBW);
+          tc::mbar_arrive_expect_tx(full + stage, TXB + SBW);
           const uint32_t dst = tc::smem_u32(sA + stage * SB);
           if (WS) tc::bulk_g2s(sA + stage * SB + SBA, a.wimg + (size_t)c * SBW, SBW, full + stage);
           for (int j = 0; j < 2; ++j) {
@@ -152,8 +161,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (S == 1) {
               if (j == 0) tma_5d(dst, &tmA, 0, x0 - 1, iy, 2 * c, b, full + stage);   // both planes
             } else {
-              tma_5d(dst + j * HL::PLANE, &tmA, ch, 0, x0, iy, b, full + stage);
-              tma_5d(dst + j * HL::PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, iy, b, full + stage);
+              tma_5d(dst + j * PLANE, &tmA, ch, 0, x0, iy, b, full + stage);
+              tma_5d(dst + j * PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, iy, b, full + stage);
             }
           }
           if (++stage == NST) { stage = 0; ph ^= 1; }
@@ -169,7 +178,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (long t = cta; t < ntiles; t += ncta) {
         tc::mbar_wait(tempty + acc, aph ^ 1);
         tc::fence_after_sync();
-        const uint32_t d = tmem + acc * NS;
+        const uint32_t d0 = tmem + acc * ACC;
         for (int c = 0; c < nchunk; ++c) {
           tc::mbar_wait(full + stage, ph);
           tc::fence_after_sync();
@@ -177,13 +186,16 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int ky = tap / 3, kx = tap % 3;
-            uint32_t aoff;
-            if (S == 1) aoff = (ky * Halo<1>::SLOTS + kx) * 16;
-            else aoff = kx == 1 ? ky * TILE_M * 16 : Halo<2>::ODD_OFF + (ky * (TILE_M + 1) + (kx == 2 ? 1 : 0)) * 16;
-            const uint64_t ad = tc::smem_desc(base + aoff, HL::PLANE, 128);
             const uint64_t bd = WS ? tc::smem_desc(base + SBA + tap * 2 * NS * 16, NS * 16, 128)
                                    : tc::smem_desc(sWa + (uint32_t)((tap * (Cin / 8) + 2 * c) * NS * 16), NS * 16, 128);
-            tc::mma_f16_ss(d, ad, bd, IDESC, (c | tap) != 0);
+#pragma unroll
+            for (int rr = 0; rr < RR; ++rr) {
+              uint32_t aoff;
+              if (S == 1) aoff = ((rr + ky) * Halo<1>::SLOTS + kx) * 16;
+              else aoff = kx == 1 ? ky * TILE_M * 16 : Halo<2>::ODD_OFF + (ky * (TILE_M + 1) + (kx == 2 ? 1 : 0)) * 16;
+              const uint64_t ad = tc::smem_desc(base + aoff, PLANE, 128);
+              tc::mma_f16_ss(d0 + rr * NS, ad, bd, IDESC, (c | tap) != 0);
+            }
           }
           tc::mma_commit(empty + stage);
           if (++stage == NST) { stage = 0; ph ^= 1; }
@@ -202,73 +214,79 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (long t = cta; t < ntiles; t += ncta) {
       const int xt = (int)(t % ntx);
       const long r = t / ntx;
-      const int oy = (int)(r % a.Ho);
-      const int b = (int)(r / a.Ho);
+      const int oy0 = (int)(r % nry) * RR;
+      const int b = (int)(r / nry);
       const int px = xt * TILE_M + m;
-      const bool valid = px < a.Wo;
-      const long opix = ((long)b * a.out_rows_buf + oy + a.out_row_off) * a.Wo + px;
+      const bool pvalid = px < a.Wo;
       tc::mbar_wait(tfull + acc, aph);
       tc::fence_after_sync();
-      const uint32_t taddr = tmem + acc * NS + ((uint32_t)(q * 32) << 16);
-      const uint32_t stg = tc::smem_u32(sOut) + (q * 2 + sb) * WBUF;
-      if (OST) {   // this warp's staging buffer sb: its bulk copy (two tiles ago) has read it
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-      }
-      float z0 = 0.f, z1 = 0.f, z2 = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < NS / 16; ++c) {
-        uint32_t v[16];
-        tc::tmem_ld16(taddr + c * 16, v);
-        tc::tmem_ld_wait();
-        float y[16];
+      for (int rr = 0; rr < RR; ++rr) {
+        const int oy = oy0 + rr;
+        const bool rvalid = oy < a.Ho;
+        const bool valid = pvalid && rvalid;
+        const long opix = ((long)b * a.out_rows_buf + oy + a.out_row_off) * a.Wo + px;
+        const uint32_t taddr = tmem + acc * ACC + rr * NS + ((uint32_t)(q * 32) << 16);
+        const uint32_t stg = tc::smem_u32(sOut) + (q * 2 + sb) * WBUF;
+        if (OST) {   // this warp's staging buffer sb: its bulk copy (two rows ago) has read it
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+        }
+        float z0 = 0.f, z1 = 0.f, z2 = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < NS / 16; ++c) {
+          uint32_t v[16];
+          tc::tmem_ld16(taddr + c * 16, v);
+          tc::tmem_ld_wait();
+          float y[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) y[i] = relu(__uint_as_float(v[i]) + sBias[c * 16 + i]);
-        if (EPI == 0 && OST) {
-          uint32_t w[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) w[i] = tc::cvt_bf16x2(y[2 * i], y[2 * i + 1]);
-          const uint32_t dst = stg + lane * (NS * 2) + c * 32;
-          tc::sts128(dst, w[0], w[1], w[2], w[3]);
-          tc::sts128(dst + 16, w[4], w[5], w[6], w[7]);
-        } else if (EPI == 0) {
-          if (valid) {
+          for (int i = 0; i < 16; ++i) y[i] = relu(__uint_as_float(v[i]) + sBias[c * 16 + i]);
+          if (EPI == 0 && OST) {
             uint32_t w[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) w[i] = tc::cvt_bf16x2(y[2 * i], y[2 * i + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(a.out + opix * a.Cout + co0 + c * 16);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          }
-        } else {
+            const uint32_t dst = stg + lane * (NS * 2) + c * 32;
+            tc::sts128(dst, w[0], w[1], w[2], w[3]);
+            tc::sts128(dst + 16, w[4], w[5], w[6], w[7]);
+          } else if (EPI == 0) {
+            if (valid) {
+              uint32_t w[8];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int o = c * 16 + i;
-            z0 = fmaf(__ldg(a.wz + o), y[i], z0);
-            z1 = fmaf(__ldg(a.wz + NS + o), y[i], z1);
-            z2 = fmaf(__ldg(a.wz + 2 * NS + o), y[i], z2);
+              for (int i = 0; i < 8; ++i) w[i] = tc::cvt_bf16x2(y[2 * i], y[2 * i + 1]);
+              uint4* dst = reinterpret_cast<uint4*>(a.out + opix * a.Cout + co0 + c * 16);
+              dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int o = c * 16 + i;
+              z0 = fmaf(__ldg(a.wz + o), y[i], z0);
+              z1 = fmaf(__ldg(a.wz + NS + o), y[i], z1);
+              z2 = fmaf(__ldg(a.wz + 2 * NS + o), y[i], z2);
+            }
           }
         }
-      }
-      if (EPI == 1 && valid) {
-        a.zout[opix * 3 + 0] = z0; a.zout[opix * 3 + 1] = z1; a.zout[opix * 3 + 2] = z2;
+        if (EPI == 1 && valid) {
+          a.zout[opix * 3 + 0] = z0; a.zout[opix * 3 + 1] = z1; a.zout[opix * 3 + 2] = z2;
+        }
+        if (OST) {   // the warp's 32 pixels of this row are contiguous in NHWC: one bulk copy
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            const int px0 = xt * TILE_M + q * 32;
+            const int nv = min(32, a.Wo - px0);
+            if (nv > 0 && rvalid) {
+              const long opix0 = ((long)b * a.out_rows_buf + oy + a.out_row_off) * a.Wo + px0;
+              bulk_s2g(a.out + opix0 * a.Cout, stg, (uint32_t)(nv * NS * 2));
+            }
+            bulk_commit();
+          }
+          sb ^= 1;
+        }
       }
       tc::fence_before_sync();
       tc::mbar_arrive(tempty + acc);
-      if (OST) {   // the warp's 32 pixels are contiguous in NHWC: one bulk copy
-        tc::fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          const int px0 = xt * TILE_M + q * 32;
-          const int nv = min(32, a.Wo - px0);
-          if (nv > 0) {
-            const long opix0 = ((long)b * a.out_rows_buf + oy + a.out_row_off) * a.Wo + px0;
-            bulk_s2g(a.out + opix0 * a.Cout, stg, (uint32_t)(nv * NS * 2));
-          }
-          bulk_commit();
-        }
-        sb ^= 1;
-      }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (OST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

@@ -20,6 +20,7 @@ namespace gn {
 struct TcConv {
   bool used = false;
   int S = 1, Cin = 0, Cout = 0, NS = 0, nsplit = 1, nstage = 2, epi = 0, ws = 0, ost = 0;   // ws: weights streamed, ost: staged output
+  int rr = 1;                    // output rows per tile (stride 1)
   size_t smem = 0;
   int ctas_per_sm = 1;
   uint8_t* wimg = nullptr;
@@ -176,7 +177,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 // Halo tensor maps over an NHWC bf16 activation [B][Hbuf][W][C] (zero fill out of bounds).
-static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C) {
+static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C, int rr) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return gn_fail(GLASSNET_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
@@ -185,7 +186,7 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C) {
     // (8 channels, x, row, 8-channel plane, frame): a box of 2 planes = one 16-channel chunk
     const cuuint64_t dims[5] = {8, (cuuint64_t)G.Wi, (cuuint64_t)G.Hi_buf, (cuuint64_t)C / 8, (cuuint64_t)B};
     const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)G.Wi * C * 2, 16, (cuuint64_t)G.Hi_buf * G.Wi * C * 2};
-    const cuuint32_t box[5] = {8, conv::Halo<1>::SLOTS, 3, 2, 1};
+    const cuuint32_t box[5] = {8, conv::Halo<1>::SLOTS, (cuuint32_t)(rr + 2), 2, 1};
     r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     G.mO = G.mA;
@@ -205,9 +206,9 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C) {
   return 0;
 }
 
-static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost = 0) {
-  const size_t sb = (2 * (S == 1 ? conv::Halo<1>::PLANE : conv::Halo<2>::PLANE) + 127) / 128 * 128 +
-                    (ws ? (size_t)9 * 2 * NS * 16 : 0);
+static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost = 0, int rr = 1) {
+  const size_t plane = S == 1 ? (size_t)(rr + 2) * conv::Halo<1>::SLOTS * 16 : conv::Halo<2>::PLANE;
+  const size_t sb = (2 * plane + 127) / 128 * 128 + (ws ? (size_t)9 * 2 * NS * 16 : 0);
   const size_t w = ws ? 0 : (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024;
   const size_t bias = ((size_t)NS * 4 + 127) / 128 * 128;
   return w + nstage * sb + (2 * nstage + 4) * 8 + bias + (ost ? (size_t)4 * 2 * 32 * NS * 2 : 0) + 128;
@@ -229,12 +230,21 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv %d->%d does not fit shared memory", Cin, Cout);
   L.NS = NS;
   L.nsplit = Cout / NS;
+  // multi-row tiles (stride 1): as many rows (4, 2) as TMEM (2 x rr x NS columns) and shared
+  // memory (>= 2 stages) allow
+  L.rr = 1;
+  if (S == 1)
+    for (int rr : {4, 2})
+      if (2 * rr * NS <= 512 && conv_smem(S, Cin, NS, 2, L.ws, 0, rr) <= LIMIT) { L.rr = rr; break; }
+  if (const char* e = getenv("GN_CONV_RR")) if (S == 1) L.rr = atoi(e);
   L.nstage = 4;
-  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws) > LIMIT) --L.nstage;
+  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws, 0, L.rr) > LIMIT) --L.nstage;
   // staged (bulk-copied) output when it fits without giving up pipeline depth
-  L.ost = (epi == 0 && conv_smem(S, Cin, NS, L.nstage, L.ws, 1) <= LIMIT && !getenv("GN_CONV_NO_OST")) ? 1 : 0;
-  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws, L.ost);
-  const int tcols = 2 * NS <= 32 ? 32 : 2 * NS <= 64 ? 64 : 2 * NS <= 128 ? 128 : 2 * NS <= 256 ? 256 : 512;
+  L.ost = (epi == 0 && !L.ws && conv_smem(S, Cin, NS, L.nstage, L.ws, 1, L.rr) <= LIMIT && !getenv("GN_CONV_NO_OST"))
+              ? 1 : 0;
+  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws, L.ost, L.rr);
+  const int acc2 = 2 * L.rr * NS;
+  const int tcols = acc2 <= 32 ? 32 : acc2 <= 64 ? 64 : acc2 <= 128 ? 128 : acc2 <= 256 ? 256 : 512;
   L.ctas_per_sm = (int)(232448 / (L.smem + 1024));
   if (L.ctas_per_sm > 2) L.ctas_per_sm = 2;
   if (L.ctas_per_sm * tcols > 512) L.ctas_per_sm = 512 / tcols;
@@ -285,7 +295,7 @@ static int geom_convs(glassnet* net, Geom& G) {
     g.in_row_off = h; g.out_row_off = h; g.out_rows_buf = G.rows[lout] + 2 * h;
     g.out = reinterpret_cast<uint16_t*>(out);
     g.zout = zout;
-    return make_halo_maps(S, g, in, G.Bmax, cin);
+    return make_halo_maps(S, g, in, G.Bmax, cin, s->conv[idx].rr);
   };
   int rc = set(0, 0, 1, G.x16, 16, 0, G.e[0], nullptr);
   for (int l = 1; l < L && !rc; ++l) rc = set(l, l - 1, 2, G.e[l - 1], c[l - 1], l, G.e[l], nullptr);
@@ -351,15 +361,15 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
   return 0;
 }
 
-template <int S, int NS, int EPI, int WS = 0, int OST = 0>
+template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1>
 static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
-  auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST>;
+  auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST, RR>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   conv::ConvArgs a;
   a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
   a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
   a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
-  const long ntiles = (long)B * G.Ho * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
+  const long ntiles = (long)B * ((G.Ho + RR - 1) / RR) * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
   long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
   if (per_split > ntiles) per_split = ntiles;
   if (per_split < 1) per_split = 1;
@@ -367,22 +377,23 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
 }
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
-#define CONV_CASE(S_, NS_, E_) \
-  if (L.S == S_ && L.NS == NS_ && L.epi == E_ && !L.ws && !L.ost) { launch_conv_k<S_, NS_, E_>(net, L, G, B, st); return 0; }
-#define CONV_CASE_OST(S_, NS_) \
-  if (L.S == S_ && L.NS == NS_ && L.epi == 0 && !L.ws && L.ost) { launch_conv_k<S_, NS_, 0, 0, 1>(net, L, G, B, st); return 0; }
-  CONV_CASE_OST(1, 16) CONV_CASE_OST(1, 32) CONV_CASE_OST(1, 64) CONV_CASE_OST(1, 128)
-  CONV_CASE_OST(2, 16) CONV_CASE_OST(2, 32) CONV_CASE_OST(2, 64) CONV_CASE_OST(2, 128)
-#undef CONV_CASE_OST
-#define CONV_CASE_WS(S_, NS_) \
-  if (L.S == S_ && L.NS == NS_ && L.epi == 0 && L.ws) { launch_conv_k<S_, NS_, 0, 1>(net, L, G, B, st); return 0; }
-  CONV_CASE_WS(1, 64) CONV_CASE_WS(1, 128) CONV_CASE_WS(1, 256) CONV_CASE_WS(2, 64) CONV_CASE_WS(2, 128) CONV_CASE_WS(2, 256)
-#undef CONV_CASE_WS
-  CONV_CASE(1, 16, 0) CONV_CASE(1, 32, 0) CONV_CASE(1, 64, 0) CONV_CASE(1, 128, 0) CONV_CASE(1, 256, 0)
-  CONV_CASE(2, 16, 0) CONV_CASE(2, 32, 0) CONV_CASE(2, 64, 0) CONV_CASE(2, 128, 0) CONV_CASE(2, 256, 0)
-  CONV_CASE(1, 16, 1) CONV_CASE(1, 32, 1)
-#undef CONV_CASE
-  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv variant S=%d NS=%d epi=%d", L.S, L.NS, L.epi);
+#define CONV_K(S_, NS_, E_, WS_, OST_, RR_)                                                              \
+  if (L.S == S_ && L.NS == NS_ && L.epi == E_ && L.ws == WS_ && L.ost == OST_ && L.rr == RR_) {         \
+    launch_conv_k<S_, NS_, E_, WS_, OST_, RR_>(net, L, G, B, st);                                       \
+    return 0;                                                                                           \
+  }
+#define CONV_S1(NS_, RR_) CONV_K(1, NS_, 0, 0, 0, RR_) CONV_K(1, NS_, 0, 0, 1, RR_) CONV_K(1, NS_, 1, 0, 0, RR_)
+  CONV_S1(16, 1) CONV_S1(16, 2) CONV_S1(16, 4) CONV_S1(32, 1) CONV_S1(32, 2) CONV_S1(32, 4)
+  CONV_S1(64, 1) CONV_S1(64, 2) CONV_S1(64, 4) CONV_S1(128, 1) CONV_S1(128, 2) CONV_S1(256, 1)
+  CONV_K(1, 64, 0, 1, 0, 1) CONV_K(1, 64, 0, 1, 0, 2) CONV_K(1, 64, 0, 1, 0, 4)
+  CONV_K(1, 128, 0, 1, 0, 1) CONV_K(1, 128, 0, 1, 0, 2) CONV_K(1, 256, 0, 1, 0, 1)
+  CONV_K(2, 16, 0, 0, 0, 1) CONV_K(2, 32, 0, 0, 0, 1) CONV_K(2, 64, 0, 0, 0, 1) CONV_K(2, 128, 0, 0, 0, 1)
+  CONV_K(2, 256, 0, 0, 0, 1) CONV_K(2, 16, 0, 0, 1, 1) CONV_K(2, 32, 0, 0, 1, 1) CONV_K(2, 64, 0, 0, 1, 1)
+  CONV_K(2, 128, 0, 0, 1, 1) CONV_K(2, 64, 0, 1, 0, 1) CONV_K(2, 128, 0, 1, 0, 1) CONV_K(2, 256, 0, 1, 0, 1)
+#undef CONV_S1
+#undef CONV_K
+  return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv variant S=%d NS=%d epi=%d ws=%d ost=%d rr=%d", L.S, L.NS, L.epi, L.ws,
+                 L.ost, L.rr);
 }
 
 inline bool tc_supported(const glassnet_dims& d) {
