@@ -245,6 +245,15 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
   L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws, L.ost, L.rr);
   const int acc2 = 2 * L.rr * NS;
   const int tcols = acc2 <= 32 ? 32 : acc2 <= 64 ? 64 : acc2 <= 128 ? 128 : acc2 <= 256 ? 256 : 512;
+  // a tcgen05.mma issue blocks its thread for about one MMA, so two CTAs per SM (two MMA
+  // issuers) beat a deeper pipeline: trade stages for a second CTA when TMEM allows it
+  if (2 * tcols <= 512)
+    for (int ns = L.nstage; ns >= 2; --ns)
+      if (2 * (conv_smem(S, Cin, NS, ns, L.ws, L.ost, L.rr) + 1024) <= 232448) {
+        L.nstage = ns;
+        L.smem = conv_smem(S, Cin, NS, ns, L.ws, L.ost, L.rr);
+        break;
+      }
   L.ctas_per_sm = (int)(232448 / (L.smem + 1024));
   if (L.ctas_per_sm > 2) L.ctas_per_sm = 2;
   if (L.ctas_per_sm * tcols > 512) L.ctas_per_sm = 512 / tcols;
