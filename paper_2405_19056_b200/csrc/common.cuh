@@ -31,4 +31,10 @@ __device__ __forceinline__ void up2_taps(int J, int n, int& a, int& b, float& wa
   else { a = i; b = i + 1 < n ? i + 1 : n - 1; wa = 0.75f; wb = 0.25f; }
 }
 
+struct Up2Rows {
+  int rows_f, rows_f_buf, grow0_f;   // fine level (skip, d, psi, out)
+  int rows_c_buf, grow0_c, Hc_full;  // coarse level (y or z)
+  int halo;
+};
+
 }  // namespace gn

@@ -399,8 +399,9 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
   switch (sp.kind) {
     case ST_PREP: {
       bf* x = (bf*)G.x16 + (size_t)h * G.W[0] * 16;
-      k_prep_x<bf><<<nblk(P0, 256), 256, 0, st>>>((const bf*)gbuf, (const bf*)direct, x, P0,
-                                                   (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
+      const dim3 grid((unsigned)((G.W[0] + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
+      ew::k_prep_x<<<grid, 256, 0, st>>>((const bf*)gbuf, (const bf*)direct, x, G.W[0], G.rows[0],
+                                         (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
       net->prof.mark("prep_x", st);
       return 0;
     }
@@ -420,9 +421,10 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       Up2Rows g;
       g.rows_f = G.rows[l - 1]; g.rows_f_buf = G.rows[l - 1] + 2 * h; g.grow0_f = G.grow0[l - 1];
       g.rows_c_buf = G.rows[l] + 2 * h; g.grow0_c = G.grow0[l]; g.Hc_full = G.Hfull[l]; g.halo = h;
-      const long nvec = (long)B * G.rows[l - 1] * G.W[l - 1] * (c[l - 1] / 8);
-      k_up2add<bf><<<nblk(nvec, 256), 256, 0, st>>>((const bf*)G.y[l], G.W[l], (const bf*)G.e[l - 1], (bf*)G.dd[l - 1],
-                                                     G.W[l - 1], c[l - 1], g, nvec);
+      const int cv = c[l - 1] / 8, lcv = __builtin_ctz((unsigned)cv);
+      const dim3 grid((unsigned)(((long)G.W[l - 1] * cv + 255) / 256), (unsigned)G.rows[l - 1], (unsigned)B);
+      ew::k_up2add<<<grid, 256, 0, st>>>((const bf*)G.y[l], G.W[l], (const bf*)G.e[l - 1], (bf*)G.dd[l - 1],
+                                         G.W[l - 1], c[l - 1], lcv, g);
       net->prof.mark("up2add", st);
       return 0;
     }
@@ -430,7 +432,8 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       Up2Rows g;
       g.rows_f = G.rows[0]; g.rows_f_buf = G.rows[0] + 2 * h; g.grow0_f = G.grow0[0];
       g.rows_c_buf = G.rows[1] + 2 * h; g.grow0_c = G.grow0[1]; g.Hc_full = G.Hfull[1]; g.halo = h;
-      k_output<<<nblk(P0, 256), 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g, P0);
+      const dim3 grid((unsigned)((G.W[0] + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
+      ew::k_output<<<grid, 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g);
       net->prof.mark("output", st);
       return 0;
     }

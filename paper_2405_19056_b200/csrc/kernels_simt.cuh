@@ -233,11 +233,6 @@ __global__ void __launch_bounds__(128) k_tb_simt(
 //   fine interior row Y (0..rows_f) is global row grow0_f + Y; its bilinear taps are
 //   clamped in GLOBAL coarse rows [0, Hc_full) and read from local buffer row
 //   (tap - grow0_c + halo).  Full frame: grow0 = 0, halo = 0, buffers = interior.
-struct Up2Rows {
-  int rows_f, rows_f_buf, grow0_f;   // fine level (skip, d, psi, out)
-  int rows_c_buf, grow0_c, Hc_full;  // coarse level (y or z)
-  int halo;
-};
 
 // d = up2(y) + skip (bilinear x2, half-pixel, edge clamp, cropped), 8 channels/thread.
 template <typename T>

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "kernels_conv_tc.cuh"
+#include "kernels_ew.cuh"
 #include "kernels_tb_tc.cuh"
 #include "net.h"
 #include "tc_ptx.cuh"
@@ -406,6 +407,8 @@ static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B,
 }
 
 inline bool tc_supported(const glassnet_dims& d) {
+  for (int l = 0; l < d.levels; ++l)   // the elementwise kernels index channel vectors with shifts
+    if (d.widths[l] & (d.widths[l] - 1)) return false;
   return (d.t_hidden == 32 || d.t_hidden == 64) && (d.widths[0] == 16 || d.widths[0] == 32);
 }
 
