@@ -37,11 +37,17 @@ template <> struct Halo<1> {
   static constexpr int PLANE = 3 * SLOTS * 16;                   // (RR = 1)
   static constexpr int TX = 3 * SLOTS * 16;
 };
+// Stride 2: the halo is de-interleaved into even pixels 2(x0+i) and odd pixels 2(x0+i)-1 so
+// every tap is an affine window.  Each region is one TMA box of [3 rows][2 planes][x] over a
+// 5-D view (8 ch, parity, x/2, plane, frame*rows): both 8-channel planes of a chunk come from
+// one box (each 32-byte sector requested once), planes are LBO apart.
 template <> struct Halo<2> {
-  static constexpr int EVEN = 3 * TILE_M * 16;                   // pixels 2(x0+i)
-  static constexpr int ODD_OFF = EVEN;                           // pixels 2(x0+i)-1, i = 0..128
-  static constexpr int PLANE = (EVEN + 3 * (TILE_M + 1) * 16 + 127) / 128 * 128;
-  static constexpr int TX = EVEN + 3 * (TILE_M + 1) * 16;
+  static constexpr int EVEN_LBO = TILE_M * 16;                   // plane stride, even region
+  static constexpr int ODD_LBO = (TILE_M + 1) * 16;              // plane stride, odd region
+  static constexpr int EVEN_ROW = 2 * EVEN_LBO, ODD_ROW = 2 * ODD_LBO;
+  static constexpr int ODD_OFF = 3 * EVEN_ROW;
+  static constexpr int TX = 3 * EVEN_ROW + 3 * ODD_ROW;          // bytes per 16-channel chunk
+  static constexpr int PLANE = TX / 2;                           // (stage sizing: 2 x PLANE = TX)
 };
 
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
@@ -70,6 +76,7 @@ struct ConvArgs {
   int Cin, Cout, Ho, Wo, B, nsplit, nstage;
   // row geometry (row tiles carry one halo row above/below; full frame: 0, 0, Ho)
   int in_row_off;        // input buffer row of global-relative row 0
+  int in_rows_buf;       // input buffer rows per frame (stride-2 view stacks frames along rows)
   int out_row_off;       // output buffer row of output row 0
   int out_rows_buf;      // output buffer rows per frame
 };
@@ -93,7 +100,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   using HL = Halo<S>;
   static_assert(S == 1 || RR == 1, "multi-row tiles are stride-1 only");
   constexpr int PLANE = S == 1 ? (RR + 2) * Halo<1>::SLOTS * 16 : HL::PLANE;
-  constexpr int TXB = S == 1 ? 2 * PLANE : 2 * HL::TX;     // bytes the TMA writes per stage
+  constexpr int TXB = S == 1 ? 2 * PLANE : HL::TX;         // bytes the TMA writes per stage
   constexpr int SBA = (2 * PLANE + 127) / 128 * 128;   // a stage's halo: 16 channels = 2 planes (TMA dst: 128-B aligned)
   constexpr int SBW = WS ? 9 * 2 * NS * 16 : 0;     // a stage's streamed weights (9 taps x 2 K-planes)
   constexpr int SB = SBA + SBW;
@@ -155,15 +162,13 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           tc::mbar_arrive_expect_tx(full + stage, TXB + SBW);
           const uint32_t dst = tc::smem_u32(sA + stage * SB);
           if (WS) tc::bulk_g2s(sA + stage * SB + SBA, a.wimg + (size_t)c * SBW, SBW, full + stage);
-          for (int j = 0; j < 2; ++j) {
-            const int ch = (2 * c + j) * 8;
-            const int iy = S * oy - 1 + a.in_row_off;
-            if (S == 1) {
-              if (j == 0) tma_5d(dst, &tmA, 0, x0 - 1, iy, 2 * c, b, full + stage);   // both planes
-            } else {
-              tma_5d(dst + j * PLANE, &tmA, ch, 0, x0, iy, b, full + stage);
-              tma_5d(dst + j * PLANE + Halo<2>::ODD_OFF, &tmO, ch, 1, x0 - 1, iy, b, full + stage);
-            }
+          const int iy = S * oy - 1 + a.in_row_off;
+          if (S == 1) {
+            tma_5d(dst, &tmA, 0, x0 - 1, iy, 2 * c, b, full + stage);   // both planes
+          } else {   // frames are stacked along the row dimension: row b*Hbuf + iy (iy = -1: see the MMA)
+            const int row = b * a.in_rows_buf + iy;
+            tma_5d(dst, &tmA, 0, 0, x0, 2 * c, row, full + stage);
+            tma_5d(dst + Halo<2>::ODD_OFF, &tmO, 0, 1, x0 - 1, 2 * c, row, full + stage);
           }
           if (++stage == NST) { stage = 0; ph ^= 1; }
         }
@@ -179,6 +184,14 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc::mbar_wait(tempty + acc, aph ^ 1);
         tc::fence_after_sync();
         const uint32_t d0 = tmem + acc * ACC;
+        // stride 2, first output row of a frame: its ky = 0 taps read the zero padding above
+        // the image (the stacked view holds the previous frame's last row there): skip them
+        bool skip_top = false;
+        if (S == 2) {
+          const long r = t / ntx;
+          skip_top = (int)(r % nry) == 0 && a.in_row_off == 0;
+        }
+        bool first = true;
         for (int c = 0; c < nchunk; ++c) {
           tc::mbar_wait(full + stage, ph);
           tc::fence_after_sync();
@@ -186,16 +199,19 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int ky = tap / 3, kx = tap % 3;
+            if (S == 2 && ky == 0 && skip_top) continue;
             const uint64_t bd = WS ? tc::smem_desc(base + SBA + tap * 2 * NS * 16, NS * 16, 128)
                                    : tc::smem_desc(sWa + (uint32_t)((tap * (Cin / 8) + 2 * c) * NS * 16), NS * 16, 128);
 #pragma unroll
             for (int rr = 0; rr < RR; ++rr) {
-              uint32_t aoff;
-              if (S == 1) aoff = ((rr + ky) * Halo<1>::SLOTS + kx) * 16;
-              else aoff = kx == 1 ? ky * TILE_M * 16 : Halo<2>::ODD_OFF + (ky * (TILE_M + 1) + (kx == 2 ? 1 : 0)) * 16;
-              const uint64_t ad = tc::smem_desc(base + aoff, PLANE, 128);
-              tc::mma_f16_ss(d0 + rr * NS, ad, bd, IDESC, (c | tap) != 0);
+              uint32_t aoff, lbo;
+              if (S == 1) { aoff = ((rr + ky) * Halo<1>::SLOTS + kx) * 16; lbo = PLANE; }
+              else if (kx == 1) { aoff = ky * Halo<2>::EVEN_ROW; lbo = Halo<2>::EVEN_LBO; }
+              else { aoff = Halo<2>::ODD_OFF + ky * Halo<2>::ODD_ROW + (kx == 2 ? 16 : 0); lbo = Halo<2>::ODD_LBO; }
+              const uint64_t ad = tc::smem_desc(base + aoff, lbo, 128);
+              tc::mma_f16_ss(d0 + rr * NS, ad, bd, IDESC, first ? 0u : 1u);
             }
+            first = false;
           }
           tc::mma_commit(empty + stage);
           if (++stage == NST) { stage = 0; ph ^= 1; }

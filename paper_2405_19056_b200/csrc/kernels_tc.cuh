@@ -192,11 +192,11 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C, int rr) {
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     G.mO = G.mA;
   } else {
-    const cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)G.Wi / 2, (cuuint64_t)G.Hi_buf, (cuuint64_t)B};
-    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, (cuuint64_t)G.Wi * C * 2,
-                               (cuuint64_t)G.Hi_buf * G.Wi * C * 2};
-    const cuuint32_t boxE[5] = {8, 1, conv::TILE_M, 3, 1};
-    const cuuint32_t boxO[5] = {8, 1, conv::TILE_M + 1, 3, 1};
+    // (8 channels, parity, x/2, 8-channel plane, frame*rows)
+    const cuuint64_t dims[5] = {8, 2, (cuuint64_t)G.Wi / 2, (cuuint64_t)C / 8, (cuuint64_t)G.Hi_buf * B};
+    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, 16, (cuuint64_t)G.Wi * C * 2};
+    const cuuint32_t boxE[5] = {8, 1, conv::TILE_M, 2, 3};
+    const cuuint32_t boxO[5] = {8, 1, conv::TILE_M + 1, 2, 3};
     r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS)
@@ -379,6 +379,7 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
   a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
   a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
   a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
+  a.in_rows_buf = G.Hi_buf;
   const long ntiles = (long)B * ((G.Ho + RR - 1) / RR) * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
   long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
   if (per_split > ntiles) per_split = ntiles;
