@@ -572,11 +572,11 @@ extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int
 }
 
 #ifdef GN_PROFILE_TB
-extern "C" int glassnet_debug_tb_prof(unsigned long long* out16, int reset) {
+extern "C" int glassnet_debug_tb_prof(unsigned long long* out32, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out16, gn::gn_tb_prof, 16 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out32, gn::gn_tb_prof, 32 * sizeof(unsigned long long));
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[32] = {};
     cudaMemcpyToSymbol(gn::gn_tb_prof, z, sizeof z);
   }
   return 0;

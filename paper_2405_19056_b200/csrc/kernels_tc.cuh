@@ -442,6 +442,8 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   kfn<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(
       reinterpret_cast<const uint16_t*>(tbuf), reinterpret_cast<const uint16_t*>(e0),
       reinterpret_cast<const uint16_t*>(direct), s->tb_wimg, s->tb_prm, s->perm, psi, P, s->sched);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "T kernel launch: %s", cudaGetErrorString(e));
   return 0;
 }
 

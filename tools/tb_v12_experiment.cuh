@@ -1,3 +1,8 @@
+// EXPERIMENT (not built, not part of the product): round-1 'v12' variant of k_tb_tc with
+// double-buffered acc1 (A2 written over its own acc1 buffer), an acc2 ring shared by the
+// layer-2 and accB batches, and GN_ABL_* ablation switches.  Parity-green on B200 but
+// 11.07 ms vs v8's 10.48 ms at c3; its ablations showed the hand-off
+// skeleton alone costs 6.75 ms.  Kept as the starting point for the next T redesign.
 // kernels_tb_tc.cuh -- the fused T + B + psi kernel on tcgen05.
 //
 // PAPER.md Eq. eq:SymmetricNN: tau = sum_i h(b_i), h shared; B;
@@ -21,23 +26,28 @@
 //
 // Warp specialisation.  A CTA runs NCH independent "chains"; a chain has three roles, all
 // indexed by tile row r = TMEM lane r:
-//   E1 (4 warps)  per tile: publish the rows' counts; issue the cp.asyncs of the NEXT
-//                 tile's records and e0 (double-buffered operands; completion tracked by
-//                 the `loaded` mbarrier, so E1 never waits for global memory);
+//   E1 (4 warps)  per tile: publish the rows' counts; issue the cp.asyncs of this tile's e0
+//                 and the NEXT tile's records (double-buffered operands; completion tracked
+//                 by mbarriers, so E1 never waits for global memory);
 //                 round t: A2 = ReLU(acc1 + b1) -> bf16 -> TMEM
 //                                                    -> MMA: acc2[t&1] = A2 W2^T, acc1 = layer 1 of slot t+1
-//                 final: phi = ReLU(accB + b_B + w_Bn n), psi = W_O,d0 phi + W_O,L L_d + b_O -> HBM
+//                 after round 1: the PREVIOUS tile's final epilogue,
+//                   phi = ReLU(accB + b_B + w_Bn n), psi = W_O,d0 phi + W_O,L L_d + b_O -> HBM
 //   E2 (4 warps)  pool += Q(acc2[s&1] + b2) for every slot s as its batch completes (acc2
 //                 is double-buffered, so this runs beside E1's next slot); then
 //                 tau = pool (f16)                   -> MMA: accB = e0 W_B,e0^T + tau W_B,tau^T
 //   MMA (1 warp)  one thread issues every tcgen05.mma of the chain, and executes the
-//                 generic -> async proxy fence for the operands the others wrote.
-// Hand-offs are mbarriers: loaded[b] (cp.async completion of operand buffer b), rdyA
-// (E1 -> MMA: counts published / A2 written), tstart (E1 -> E2), free2[b] (E2 -> MMA: acc2
-// buffer b read), rdyF (E2 -> MMA: tau written), done1 (commit -> E1, batches holding a
-// layer-1 MMA), done2[b] (commit -> E2, layer-2 batches into buffer b) and doneF (commit ->
-// E1, the accB batch).  Each waiter can be at most one
-// phase behind its barrier by construction.
+//                 generic -> async proxy fence for the operands the others wrote.  A tile's
+//                 accB batch is issued inside the NEXT tile's first slot round, so the pool's
+//                 tail, the B MMAs and the final epilogue overlap the next tile's rounds.
+// Hand-offs are mbarriers: loaded[b] / e0ld[b] (cp.async completion of operand buffer b's
+// records / e0), rdyC (E1 -> MMA: counts published; also orders E1's accB reads before the
+// next accB batch), rdyA (E1 -> MMA: A2 written), tstart (E1 -> E2), e2rd (E2 -> E1: counts
+// read, so E1 may overwrite them), free2[b] (E2 -> MMA: acc2 buffer b read), rdyF (E2 -> MMA:
+// tau written), done1 (commit -> E1, batches holding a layer-1 MMA), done2[b] (commit -> E2,
+// layer-2 batches into buffer b) and doneF (commit -> E1, E2: the accB batch).  Each waiter
+// can be at most one phase behind its barrier by construction (E1's e2rd wait bounds tstart;
+// done1 / doneF / rdyF bound the rest).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -49,13 +59,13 @@ namespace gn {
 
 #ifdef GN_PROFILE_TB
 // clock64 breakdown of chain 0 of CTA 0 (diagnostic build only): counters 0-15 are kept by
-// E1's thread 0 (16-31 are reserved for the other roles); accumulated in shared memory (a
-// global read-modify-write would itself stall the chain) and flushed at exit
+// E1's thread 0, 16-23 by E2's first thread, 24-31 by the MMA thread; accumulated in shared
+// memory (a global read-modify-write would itself stall the chain) and flushed at exit
 __device__ unsigned long long gn_tb_prof[32];
 __shared__ unsigned long long gn_tb_sprof[32];
 #define TBP_NOW(v) const long long v = clock64()
 #define TBP_ADD(i, a, b) \
-  if (threadIdx.x == 0) gn_tb_sprof[i] += (unsigned long long)((b) - (a))
+  if (threadIdx.x == 0 || threadIdx.x == 4 * NCH * 32 || threadIdx.x == 8 * NCH * 32) gn_tb_sprof[i] += (unsigned long long)((b) - (a))
 #define TBP_INIT() if (threadIdx.x < 32) gn_tb_sprof[threadIdx.x] = 0
 #define TBP_FLUSH() if (blockIdx.x == 0 && threadIdx.x < 32) gn_tb_prof[threadIdx.x] += gn_tb_sprof[threadIdx.x]
 #else
@@ -151,11 +161,14 @@ struct TbLayout {
   static constexpr int CH_E0 = CH_A1 + 2 * A1_PL * PL;          // 2 buffers x C0/8 planes
   static constexpr int CH_TAU = CH_E0 + 2 * (C0 / 8) * PL;      // H/8 planes (f16)
   static constexpr int CH_MROW = CH_TAU + (H / 8) * PL;         // 128 x u8: the rows' valid counts
-  static constexpr int CH_B = CH_MROW + 128;
-  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 12 mbarrier slots; then the tmem ptr
-  static constexpr int OFF_RED = OFF_BAR + 4 * 96 + 16;     // per chain 8 ints: warp max counts, Kt, tile ids
+  static constexpr int CH_PROW = CH_MROW + 128;                 // 128 x i64: the rows' pixels (-1: none)
+  static constexpr int CH_B = CH_PROW + 128 * 8;
+  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 24 mbarrier slots; then the tmem ptr
+  static constexpr int OFF_RED = OFF_BAR + 4 * 192 + 16;    // per chain 8 ints: warp max counts, Kt, tile ids
   static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 127) / 128 * 128;
-  static constexpr int TCOLS = (3 * H + C0 + H / 2 + 31) / 32 * 32;   // acc1, acc2 x2, accB, A2 (packed)
+  // TMEM per chain: acc1 x2 (A2 of a slot is written over the first H/2 columns of its own
+  // acc1 buffer) and acc2 x2 (the accB batches take their turn in this ring)
+  static constexpr int TCOLS = 4 * H;
   static constexpr int NCH_T = 512 / TCOLS;
   static constexpr int NCH_S = (232448 - 1024 - OFF_CH) / CH_B;
   static constexpr int NCH = NCH_T < NCH_S ? (NCH_T < 3 ? NCH_T : 3) : (NCH_S < 3 ? NCH_S : 3);
@@ -182,20 +195,24 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   constexpr int NCH = S::NCH;
   constexpr uint32_t PL = S::PL;
   constexpr int NO = C0 + 3;
-  static_assert(C0 <= 32 && H <= 64 && H % 32 == 0, "TbParams sizes / epilogue chunks");
+  static_assert(C0 <= 32 && C0 <= H && H <= 64 && H % 32 == 0, "TbParams sizes / epilogue chunks / accB in acc2");
   const int wg = threadIdx.x >> 5;
   const int role = wg < 4 * NCH ? 0 : wg < 8 * NCH ? 1 : 2;   // E1, E2, MMA
   const int g = role == 2 ? wg - 8 * NCH : (wg >> 2) % NCH;    // chain
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * g;
-  uint64_t* loaded = bars + 0;     // [2]
-  uint64_t* rdyA = bars + 2;
-  uint64_t* rdyF = bars + 3;
-  uint64_t* free2 = bars + 4;      // [2]
-  uint64_t* done1 = bars + 6;
-  uint64_t* done2 = bars + 7;      // [2]
-  uint64_t* tstart = bars + 9;
-  uint64_t* doneF = bars + 10;
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 4 * 96);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 24 * g;
+  uint64_t* loaded = bars + 0;     // [2] records of operand buffer b (cp.async)
+  uint64_t* e0ld = bars + 2;       // [2] e0 of operand buffer b (cp.async)
+  uint64_t* rdyC = bars + 4;       // E1 -> MMA: a tile's counts published
+  uint64_t* rdyA = bars + 5;       // [2] E1 -> MMA: A2 written over acc1[b]
+  uint64_t* tstart = bars + 7;     // E1 -> E2: a tile's counts and pixels published
+  uint64_t* e2rd = bars + 8;       // E2 -> E1: the tile's counts and pixels read
+  uint64_t* free2 = bars + 9;      // [2] E2 -> MMA: acc2[b] read
+  uint64_t* done1 = bars + 11;     // [2] commit -> E1: layer 1 into acc1[b]
+  uint64_t* done2 = bars + 13;     // [2] commit -> E2: a layer-2 or accB batch into acc2[b]
+  uint64_t* rdyF = bars + 15;      // E2 -> MMA: tau written
+  uint64_t* bdone = bars + 16;     // E2 -> E1: an accB batch consumed (its e0 buffer is free)
+  uint64_t* cack = bars + 17;      // MMA -> E1: a tile's counts read
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 4 * 192);
   volatile int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 8 * g;   // [0..3] warp max, [4] Kt, [5..7] tile ids
 
   TBP_INIT();
@@ -209,13 +226,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     }
   if (threadIdx.x == 0) {
     for (int c = 0; c < NCH; ++c) {
-      uint64_t* b = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * c;
-      tc::mbar_init(b + 0, 128); tc::mbar_init(b + 1, 128);   // loaded[2]
-      tc::mbar_init(b + 2, 128); tc::mbar_init(b + 3, 128);   // rdyA, rdyF
-      tc::mbar_init(b + 4, 128); tc::mbar_init(b + 5, 128);   // free2[2]
-      tc::mbar_init(b + 6, 1); tc::mbar_init(b + 7, 1); tc::mbar_init(b + 8, 1);   // done1, done2[2]
-      tc::mbar_init(b + 9, 128);                              // tstart
-      tc::mbar_init(b + 10, 1);                               // doneF
+      uint64_t* b = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 24 * c;
+      for (int i = 0; i < 11; ++i) tc::mbar_init(b + i, 128);   // loaded, e0ld, rdyC, rdyA, tstart, e2rd, free2
+      tc::mbar_init(b + 11, 1); tc::mbar_init(b + 12, 1);       // done1[2]
+      tc::mbar_init(b + 13, 1); tc::mbar_init(b + 14, 1);       // done2[2]
+      tc::mbar_init(b + 15, 128); tc::mbar_init(b + 16, 128);   // rdyF, bdone
+      tc::mbar_init(b + 17, 1);                                 // cack
     }
     tc::fence_mbar_init();
   }
@@ -225,9 +241,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tptr + g * S::TCOLS;
-  const uint32_t t_acc1 = tmem, t_acc2 = tmem + H, t_accB = tmem + 3 * H, t_a2 = tmem + 3 * H + C0;
+  const uint32_t t_acc1 = tmem, t_acc2 = tmem + 2 * H;   // [2] each, H columns apart
   uint8_t* chs = smem + S::OFF_CH + g * S::CH_B;
   volatile uint8_t* mrow = chs + S::CH_MROW;
+  volatile long long* prow = reinterpret_cast<volatile long long*>(chs + S::CH_PROW);
   const uint32_t sA1 = tc::smem_u32(chs + S::CH_A1), sE0 = tc::smem_u32(chs + S::CH_E0);
   const uint32_t sTAU = tc::smem_u32(chs + S::CH_TAU);
   const long ntiles = (P + TB_SBP - 1) / TB_SBP * TB_SBT;
@@ -240,80 +257,203 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
       constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
       constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
-      // layer 1 of slot k from operand buffer `buf`: the record's K-window starts in plane
-      // j = 11k/8 at column offset o = 11k mod 8 (W1 copy o); a third plane needs a 2nd MMA
+      uint32_t cph = 0, fph = 0, lph[2] = {0, 0}, eph[2] = {0, 0}, aph[2] = {0, 0}, f2ph[2] = {0, 0};
+      bool used2[2] = {false, false};
+      int ring = 0;              // acc2 ring position (layer-2 and accB batches, in issue order)
+      // layer 1 of slot k from operand buffer `buf` into acc1[k&1]: the record's K-window
+      // starts in plane j = 11k/8 at column offset o = 11k mod 8 (W1 copy o); a third plane
+      // needs a 2nd MMA
       auto layer1 = [&](int k, int buf) {
         const int j = (11 * k) >> 3, o = (11 * k) & 7;
         const uint32_t a = sA1 + (buf * S::A1_PL + j) * PL, w = sW1 + o * 4 * H * 16;
-        tc::mma_f16_ss(t_acc1, tc::smem_desc(a, PL, 128), tc::smem_desc(w, H * 16, 128), ID_T, 0);
+#ifndef GN_ABL_NO_L1
+        const uint32_t d = t_acc1 + (k & 1) * H;
+        tc::mma_f16_ss(d, tc::smem_desc(a, PL, 128), tc::smem_desc(w, H * 16, 128), ID_T, 0);
         if (o > 5)
-          tc::mma_f16_ss(t_acc1, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
+          tc::mma_f16_ss(d, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
+#endif
+        tc::mma_commit(done1 + (k & 1));
       };
-      uint32_t aph = 0, fph = 0, lph[2] = {0, 0}, f2ph[2] = {0, 0};
-      for (int buf = 0;; buf ^= 1) {
-        tc::mbar_wait(rdyA, aph); aph ^= 1;        // the tile's counts
-        const int Kt = red[4];
-        if (Kt < 0) break;
-        tc::mbar_wait(loaded + buf, lph[buf]); lph[buf] ^= 1;   // its records and e0 (cp.async)
+      auto ring_take = [&]() {   // the next acc2 buffer, once E2 has read its previous batch
+        const int b = ring & 1;
+        if (used2[b]) { tc::mbar_wait(free2 + b, f2ph[b]); f2ph[b] ^= 1; }
+        used2[b] = true;
+        ++ring;
+        return b;
+      };
+      int pendB = -1, ktB = 0;   // operand buffer (and Kt) of the tile whose accB batch is pending
+      auto issueB = [&]() {
+        TBP_NOW(b0);
+        tc::mbar_wait(rdyF, fph); fph ^= 1;   // tau written
+        tc::mbar_wait(e0ld + pendB, eph[pendB]); eph[pendB] ^= 1;
+        TBP_NOW(b1);
+        TBP_ADD(31, b0, b1);
+        const int b = ring_take();
         tc::fence_after_sync();
         tc::fence_proxy_async();
-        if (Kt > 0) { layer1(0, buf); tc::mma_commit(done1); }
-        for (int t = 0; t < Kt; ++t) {
-          tc::mbar_wait(rdyA, aph); aph ^= 1;      // A2 of slot t in TMEM (acc1 read)
-          if (t >= 2) { tc::mbar_wait(free2 + (t & 1), f2ph[t & 1]); f2ph[t & 1] ^= 1; }   // acc2[t&1] read
-          tc::fence_after_sync();
-#pragma unroll
-          for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ts(t_acc2 + (t & 1) * H, t_a2 + q * 8, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T,
-                           q > 0);
-          if (t + 1 < Kt) { layer1(t + 1, buf); tc::mma_commit(done1); }
-          tc::mma_commit(done2 + (t & 1));
-        }
-        if (Kt >= 2) { tc::mbar_wait(free2 + ((Kt - 2) & 1), f2ph[(Kt - 2) & 1]); f2ph[(Kt - 2) & 1] ^= 1; }
-        if (Kt >= 1) { tc::mbar_wait(free2 + ((Kt - 1) & 1), f2ph[(Kt - 1) & 1]); f2ph[(Kt - 1) & 1] ^= 1; }
-        tc::mbar_wait(rdyF, fph); fph ^= 1;        // tau written
-        tc::fence_after_sync();
-        tc::fence_proxy_async();
-        const uint32_t e0b = sE0 + buf * (C0 / 8) * PL;
+        const uint32_t d = t_acc2 + b * H, e0b = sE0 + pendB * (C0 / 8) * PL;
+#ifdef GN_ABL_NO_B
+        if (0)
+#endif
 #pragma unroll
         for (int q = 0; q < C0 / 16; ++q)
-          tc::mma_f16_ss(t_accB, tc::smem_desc(e0b + 2 * q * PL, PL, 128),
+          tc::mma_f16_ss(d, tc::smem_desc(e0b + 2 * q * PL, PL, 128),
                          tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-        if (Kt > 0) {
+#ifdef GN_ABL_NO_B
+        if (0)
+#endif
+        if (ktB > 0) {
 #pragma unroll
           for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ss(t_accB, tc::smem_desc(sTAU + 2 * q * PL, PL, 128),
+            tc::mma_f16_ss(d, tc::smem_desc(sTAU + 2 * q * PL, PL, 128),
                            tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
         }
-        tc::mma_commit(doneF);
+        tc::mma_commit(done2 + b);
+        pendB = -1;
+      };
+      for (int buf = 0;; buf ^= 1) {
+        TBP_NOW(m0);
+        tc::mbar_wait(rdyC, cph); cph ^= 1;        // the tile's counts
+        const int Kt = red[4];
+        tc::mbar_arrive(cack);
+        if (Kt < 0) break;
+        TBP_NOW(m1);
+        tc::mbar_wait(loaded + buf, lph[buf]); lph[buf] ^= 1;   // its records (cp.async)
+        tc::fence_after_sync();
+        tc::fence_proxy_async();
+        TBP_NOW(m2);
+        TBP_ADD(24, m0, m1);
+        TBP_ADD(25, m1, m2);
+        if (Kt > 0) layer1(0, buf);
+        if (Kt > 1) layer1(1, buf);
+        if (Kt == 0 && pendB >= 0) issueB();
+        TBP_NOW(m3);
+        TBP_ADD(26, m2, m3);
+        for (int t = 0; t < Kt; ++t) {
+          const int a = t & 1;
+          TBP_NOW(r0);
+          tc::mbar_wait(rdyA + a, aph[a]); aph[a] ^= 1;   // A2 of slot t over acc1[a]
+          TBP_NOW(r1);
+          const int b = ring_take();
+          tc::fence_after_sync();
+          TBP_NOW(r2);
+#ifndef GN_ABL_NO_L2
+#pragma unroll
+          for (int q = 0; q < H / 16; ++q)
+            tc::mma_f16_ts(t_acc2 + b * H, t_acc1 + a * H + q * 8, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128),
+                           ID_T, q > 0);
+#endif
+          tc::mma_commit(done2 + b);
+          // acc1[a] is overwritten only after the layer-2 MMAs above have read A2 (in order)
+          if (t + 2 < Kt) layer1(t + 2, buf);
+          TBP_NOW(r3);
+          if (t == 0 && pendB >= 0) issueB();
+          TBP_NOW(r4);
+          TBP_ADD(27, r0, r1);
+          TBP_ADD(28, r1, r2);
+          TBP_ADD(29, r2, r3);
+          TBP_ADD(30, r3, r4);
+        }
+        pendB = buf; ktB = Kt;
       }
+      if (pendB >= 0) issueB();
     }
   } else if (role == 1) {
-    // ------------------------------------------------------------------ E2: the pool
+    // ------------------------------------------------------------------ E2: the pool, phi, psi
+    // E2 consumes the acc2 ring in the MMA thread's issue order: for tile v, slot 0, then the
+    // accB batch of tile v-1 (its final epilogue), then slots 1.. (just the accB batch when
+    // Kt = 0); after the pool, tau(v) -> smem (the accB batch that read tau(v-1) is complete).
     const int r = threadIdx.x & 127, warp = r >> 5;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     uint32_t tph = 0, d2ph[2] = {0, 0};
+    int ring = 0;
+    bool prev = false;                      // a tile whose final epilogue is pending
+    int fm_m = 0;
+    long fp = -1;
+    float fl0 = 0.f, fl1 = 0.f, fl2 = 0.f;
+    auto ring_wait = [&]() {
+      const int b = ring & 1;
+      TBP_NOW(p0);
+      tc::mbar_wait(done2 + b, d2ph[b]); d2ph[b] ^= 1;
+      tc::fence_after_sync();
+      TBP_NOW(p1);
+      TBP_ADD(17, p0, p1);
+      return b;
+    };
+    auto ring_free = [&](int b) {
+      tc::fence_before_sync();
+      tc::mbar_arrive(free2 + b);
+      ++ring;
+    };
+    // final epilogue of the previous tile from its accB batch (the next ring entry):
+    // phi = ReLU(accB + b_B + w_Bn n), psi = W_O,d0 phi + W_O,L L_d + b_O -> HBM
+    auto final_prev = [&]() {
+      const int b = ring_wait();
+      TBP_NOW(f1);
+      const float* WO = prm.WO;
+      float ps0 = prm.bO[0], ps1 = prm.bO[1], ps2 = prm.bO[2];
+      ps0 = fmaf(WO[0 * NO + C0 + 0], fl0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], fl1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], fl2, ps0);
+      ps1 = fmaf(WO[1 * NO + C0 + 0], fl0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], fl1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], fl2, ps1);
+      ps2 = fmaf(WO[2 * NO + C0 + 0], fl0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], fl1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], fl2, ps2);
+      const float fm = (float)fm_m;
+#pragma unroll
+      for (int c = 0; c < C0 / 16; ++c) {
+        uint32_t u[16];
+        tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 16, u);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int o = c * 16 + i;
+          const float phi = relu(__uint_as_float(u[i]) + prm.bB[o] + prm.wBn[o] * fm);
+          ps0 = fmaf(WO[0 * NO + o], phi, ps0);
+          ps1 = fmaf(WO[1 * NO + o], phi, ps1);
+          ps2 = fmaf(WO[2 * NO + o], phi, ps2);
+        }
+      }
+      ring_free(b);
+      tc::mbar_arrive(bdone);
+      if (fp >= 0) { psi[fp * 3 + 0] = ps0; psi[fp * 3 + 1] = ps1; psi[fp * 3 + 2] = ps2; }
+      prev = false;
+      TBP_NOW(f2);
+      TBP_ADD(21, f1, f2);
+    };
     for (;;) {
+      TBP_NOW(e0t);
       tc::mbar_wait(tstart, tph); tph ^= 1;
+      TBP_NOW(e1t);
+      TBP_ADD(16, e0t, e1t);
       const int Kt = red[4];
-      if (Kt < 0) break;
       const int m = mrow[r];
+      const long p = (long)prow[r];
+      tc::mbar_arrive(e2rd);
+      if (Kt < 0) break;
+      float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;   // consumed by this tile's final, a tile later
+      if (p >= 0) {
+        ld0 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 0) << 16);
+        ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
+        ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
+      }
+      if (Kt == 0 && prev) final_prev();
       uint32_t pool[H];
 #pragma unroll
       for (int j = 0; j < H; ++j) pool[j] = 0;
 #pragma unroll 1
       for (int s = 0; s < Kt; ++s) {
-        const int b = s & 1;
-        tc::mbar_wait(done2 + b, d2ph[b]); d2ph[b] ^= 1;
-        tc::fence_after_sync();
+        const int b = ring_wait();
+        TBP_NOW(q1);
         // pool += Q(acc2 + b2): acc2 carries the 2^12 scale (folded into W2), so x = acc2 + q2
         // is 2^23 + (v + b2) 2^12 rounded; masked slots clamp to exactly 2^23 (0)
         const float hi = (s < m) ? TB_QMAX : TB_QMAGIC;
+#ifdef GN_ABL_NO_E2
+        ring_free(b);
+        if (0)
+#endif
 #pragma unroll
         for (int c = 0; c < H / 16; ++c) {
           uint32_t u[16];
           tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 16, u);
           tc::tmem_ld_wait();
+          if (c == H / 16 - 1) ring_free(b);   // all of this batch is in registers
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x = __uint_as_float(u[i]) + prm.q2[c * 16 + i];
@@ -321,8 +461,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
             pool[c * 16 + i] += __float_as_uint(x);
           }
         }
-        tc::fence_before_sync();
-        tc::mbar_arrive(free2 + b);
+        TBP_NOW(q2);
+        TBP_ADD(18, q1, q2);
+        if (s == 0 && prev) final_prev();
       }
       if (Kt > 0) {   // tau = pool (f16) -> its operand
         const uint32_t off = (uint32_t)Kt * TB_QBITS;
@@ -340,27 +481,33 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         }
       }
       tc::mbar_arrive(rdyF);   // release; the MMA thread fences the proxies
+      TBP_NOW(e2t);
+      TBP_ADD(22, e1t, e2t);
+      prev = true; fm_m = m; fp = p; fl0 = ld0; fl1 = ld1; fl2 = ld2;
     }
+    if (prev) final_prev();
   } else {
-    // ------------------------------------------------------------------ E1: operands, A2, phi, psi
+    // ------------------------------------------------------------------ E1: operands, A2
     const int r = threadIdx.x & 127, warp = r >> 5, lane = r & 31;
     const int bar_id = 1 + g;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    uint32_t d1ph = 0, dfph = 0;
+    uint32_t d1ph[2] = {0, 0}, e2ph = 0, bdph = 0, ckph = 0;
     auto decode = [&](long tl, int pe, long& pp, int& mm, bool& ok) {   // this thread's pixel of tile tl
       pp = tl / TB_SBT * TB_SBP + (pe & 2047);
       ok = tl < ntiles && pp < P;
       mm = ok ? (pe >> 11) : 0;
     };
-    // copy row r's operands of a tile (pixel pp, mm valid records) into operand buffer `buf`
-    auto fill = [&](int buf, long pp, int mm, bool ok) {
+    // copy row r's records of a tile (pixel pp, mm valid records) into operand buffer `buf`
+    auto fill_rec = [&](int buf, long pp, int mm, bool ok) {
       const uint32_t a = sA1 + buf * S::A1_PL * PL + r * 16;
       const int vb = ok ? mm * 22 : 0;            // valid bytes of the row
       if (S::ASYNC) {
+#ifndef GN_ABL_NO_FILL
         const char* src = ok ? reinterpret_cast<const char*>(tbuf + pp * (K * 11)) : reinterpret_cast<const char*>(tbuf);
 #pragma unroll
         for (int i = 0; i < S::NPL; ++i)
           cp_async16z(a + i * PL, src + 16 * i, (uint32_t)min(max(vb - 16 * i, 0), 16));
+#endif
       } else {   // rows not 16-byte aligned in global memory: through registers
         const uint16_t* src = tbuf + pp * (K * 11);
 #pragma unroll
@@ -375,16 +522,21 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           tc::sts128(a + i * PL, w[0], w[1], w[2], w[3]);
         }
       }
+      cp_async_arrive(loaded + buf);
+    };
+    auto fill_e0 = [&](int buf, long pp, bool ok) {
       const uint32_t eb = sE0 + buf * (C0 / 8) * PL + r * 16;
       const uint16_t* es = ok ? e0 + pp * C0 : e0;
 #pragma unroll
       for (int j = 0; j < C0 / 8; ++j) cp_async16z(eb + j * PL, es + 8 * j, ok ? 16u : 0u);
-      cp_async_arrive(loaded + buf);
+      cp_async_arrive(e0ld + buf);
     };
 
     // Tile pipeline: tile ids are claimed three ahead (atomics), the perm entry of the tile
-    // after next is loaded one tile ahead, and the next tile's operands are copied during
-    // this one, so no global latency sits on a critical path.
+    // after next is loaded one tile ahead, the next tile's records are copied during this
+    // one, and a tile's e0 in its own prologue (its buffer was last read by the accB batch of
+    // the tile two back, consumed by E2 during the previous tile), so no global latency sits
+    // on a critical path.
     int claim = 0;
     if (r == 0) { red[5] = atomicAdd(sched, 1); red[6] = atomicAdd(sched, 1); claim = atomicAdd(sched, 1); }
     tc::bar_sync(bar_id, 128);
@@ -393,48 +545,53 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     int m, nm;
     bool pv, npv;
     decode(tile, tile < ntiles ? (int)__ldg(perm + tile * 128 + r) : 0, p, m, pv);
-    if (tile < ntiles) fill(0, p, m, pv);
+    if (tile < ntiles) { fill_rec(0, p, m, pv); fill_e0(0, p, pv); }
     decode(ntile, ntile < ntiles ? (int)__ldg(perm + ntile * 128 + r) : 0, np, nm, npv);
-    for (int it = 0; tile < ntiles; ++it) {
+    int it = 0;
+    for (; tile < ntiles; ++it) {
       TBP_NOW(tp_t0);
       const int buf = it & 1;
-      // ---- prologue: publish the counts; copy the next tile's operands
-      mrow[r] = (uint8_t)m;
-      {
-        const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
-        if (lane == 0) red[warp] = wm;
-        if (r == 0) { red[5 + (it + 2) % 3] = claim; claim = atomicAdd(sched, 1); }
+      // ---- prologue: publish the counts and pixels; copy this tile's e0, the next tile's records
+      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
+      if (it > 0) {   // E2 and the MMA thread have read the previous tile's counts
+        tc::mbar_wait(e2rd, e2ph); e2ph ^= 1;
+        tc::mbar_wait(cack, ckph); ckph ^= 1;
       }
+      mrow[r] = (uint8_t)m;
+      prow[r] = pv ? (long long)p : -1ll;
+      if (lane == 0) red[warp] = wm;
+      if (r == 0) { red[5 + (it + 2) % 3] = claim; claim = atomicAdd(sched, 1); }
       tc::bar_sync(bar_id, 128);
       const int Kt = max(max(red[0], red[1]), max(red[2], red[3]));
       const long nntile = red[5 + (it + 2) % 3];
       if (r == 0) red[4] = Kt;
-      tc::mbar_arrive(rdyA);
+      tc::mbar_arrive(rdyC);
       tc::mbar_arrive(tstart);
-      float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;   // consumed after the slot rounds (latency hidden)
-      if (pv) {
-        ld0 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 0) << 16);
-        ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
-        ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
+      if (it > 0) {
+        if (it > 1) { tc::mbar_wait(bdone, bdph); bdph ^= 1; }   // accB batch of tile it-2 consumed
+        fill_e0(buf, p, pv);
       }
-      if (ntile < ntiles) fill(buf ^ 1, np, nm, npv);   // buffer buf^1 was last read by the previous tile's MMAs
+      if (ntile < ntiles) fill_rec(buf ^ 1, np, nm, npv);   // buffer buf^1's records were last read by tile it-1's MMAs
       const int nnpe = nntile < ntiles ? (int)__ldg(perm + nntile * 128 + r) : 0;   // decoded next iteration
       TBP_NOW(tp_t1);
       TBP_ADD(1, tp_t0, tp_t1);
       TBP_ADD(10, 0, Kt + 1);
       TBP_ADD(11, 0, 1);
-      // ---- slot rounds: A2 of slot t -> TMEM
+      // ---- slot rounds: A2 of slot t -> TMEM, over acc1[t&1]
 #pragma unroll 1
       for (int t = 0; t < Kt; ++t) {
+        const int a = t & 1;
         TBP_NOW(tp_r0);
-        tc::mbar_wait(done1, d1ph); d1ph ^= 1;   // batch t-1: acc1 holds slot t
+        tc::mbar_wait(done1 + a, d1ph[a]); d1ph[a] ^= 1;   // acc1[a] holds slot t
         tc::fence_after_sync();
         TBP_NOW(tp_r1);
         TBP_ADD(3, tp_r0, tp_r1);
+#ifndef GN_ABL_NO_E1
+        const uint32_t t1 = t_acc1 + a * H + lane_off;
         uint32_t u[H];
 #pragma unroll
         for (int c = 0; c < H / 32; ++c)
-          tc::tmem_ld32(t_acc1 + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c));
+          tc::tmem_ld32(t1 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c));
         tc::tmem_ld_wait();
         uint32_t o[H / 2];
 #pragma unroll
@@ -442,54 +599,30 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           o[i] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * i]) + prm.b1[2 * i],
                                      __uint_as_float(u[2 * i + 1]) + prm.b1[2 * i + 1]);
 #pragma unroll
-        for (int c = 0; c < H / 32; ++c) tc::tmem_st16(t_a2 + lane_off + 16 * c, o + 16 * c);
+        for (int c = 0; c < H / 32; ++c) tc::tmem_st16(t1 + 16 * c, o + 16 * c);
         tc::tmem_st_wait();
+#endif
         tc::fence_before_sync();
-        tc::mbar_arrive(rdyA);
+        tc::mbar_arrive(rdyA + a);
         TBP_NOW(tp_r2);
         TBP_ADD(4, tp_r1, tp_r2);
       }
-      // ---- final
-      TBP_NOW(tp_f0);
-      tc::mbar_wait(doneF, dfph); dfph ^= 1;     // accB
-      tc::fence_after_sync();
-      TBP_NOW(tp_f1);
-      TBP_ADD(6, tp_f0, tp_f1);
-      const float* WO = prm.WO;
-      float ps0 = prm.bO[0], ps1 = prm.bO[1], ps2 = prm.bO[2];
-      ps0 = fmaf(WO[0 * NO + C0 + 0], ld0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], ld1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], ld2, ps0);
-      ps1 = fmaf(WO[1 * NO + C0 + 0], ld0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], ld1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], ld2, ps1);
-      ps2 = fmaf(WO[2 * NO + C0 + 0], ld0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], ld1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], ld2, ps2);
-      const float fm = (float)m;
-#pragma unroll
-      for (int c = 0; c < C0 / 16; ++c) {
-        uint32_t u[16];
-        tc::tmem_ld16(t_accB + lane_off + c * 16, u);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int o = c * 16 + i;
-          const float phi = relu(__uint_as_float(u[i]) + prm.bB[o] + prm.wBn[o] * fm);
-          ps0 = fmaf(WO[0 * NO + o], phi, ps0);
-          ps1 = fmaf(WO[1 * NO + o], phi, ps1);
-          ps2 = fmaf(WO[2 * NO + o], phi, ps2);
-        }
-      }
-      if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
-      tc::fence_before_sync();
       TBP_NOW(tp_end);
-      TBP_ADD(8, tp_f1, tp_end);
       TBP_ADD(9, tp_t0, tp_end);
       // advance the tile pipeline
       tile = ntile; p = np; m = nm; pv = npv;
       ntile = nntile;
       decode(ntile, nnpe, np, nm, npv);
     }
-    // stop the MMA warp and E2
+    // stop the MMA warp and E2 (once both have read the last tile's counts)
+    if (it > 0) {
+      tc::mbar_wait(e2rd, e2ph); e2ph ^= 1;
+      tc::mbar_wait(cack, ckph); ckph ^= 1;
+    }
     tc::bar_sync(bar_id, 128);
     if (r == 0) red[4] = -1;
     tc::bar_sync(bar_id, 128);
-    tc::mbar_arrive(rdyA);
+    tc::mbar_arrive(rdyC);
     tc::mbar_arrive(tstart);
   }
   tc::fence_before_sync();
