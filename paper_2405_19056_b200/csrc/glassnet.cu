@@ -244,7 +244,9 @@ extern "C" int glassnet_launches_per_forward(glassnet_t net, int32_t batch) {
   if (!net) return 0;
   const int L = net->d.levels;
   (void)batch;
-  return 1 + L + 1 + 2 * (L - 2) + 1 + 1;
+  // prep, F_0..F_{L-1}, T (+ its count-sort pre-pass on the tensor-core family), R_{L-1}..R_1,
+  // up2add at levels L-2..1, output
+  return 1 + L + (net->tc ? 2 : 1) + (L - 1) + (L - 2) + 1;
 }
 
 // ------------------------------------------------------------------------ forward (SIMT family)
@@ -524,6 +526,7 @@ extern "C" int glassnet_profile_begin(glassnet_t net, int32_t max_launches) {
   p.stage.assign((size_t)max_launches, -1);
   for (auto& e : p.ev) CUDA_TRY(cudaEventCreate(&e));
   p.used = 0;
+  p.dropped = 0;
   p.on = true;
   return GLASSNET_OK;
 }
@@ -533,6 +536,9 @@ extern "C" int glassnet_profile_end(glassnet_t net, int32_t max_stages, char* na
   if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
   StageProfiler& p = net->prof;
   p.on = false;
+  if (p.dropped)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "profile: %zu stage marks exceeded the %zu reserved by profile_begin",
+                   p.dropped, p.ev.size());
   std::vector<double> tot(p.names.size(), 0.0);
   std::vector<int> cnt(p.names.size(), 0);
   if (p.used) CUDA_TRY(cudaEventSynchronize(p.ev[p.used - 1]));

@@ -6,9 +6,11 @@
 // GEMM view per CTA tile: M = 128 output pixels of one output row, N = NS output
 // channels (a split of C_out), K = 9 taps x C_in.  The A operand is never materialised:
 // TMA copies, per 16-channel chunk, the 3 input rows of the tile's halo into shared
-// memory (zero fill outside the image = the conv's zero padding) in the K-major
-// "interleaved" core-matrix layout, and each of the 9 taps is a shifted UMMA descriptor
-// into that halo (stride 2 uses even/odd de-interleaved halos so every tap is affine).
+// memory (zero fill outside the image = the conv's zero padding) as 32-byte pixel rows in
+// the SWIZZLE_32B K-major layout (each pixel's 16 channels are one full 32-byte sector of
+// the NHWC input, so every L2 sector is fetched once), and each of the 9 taps is a UMMA
+// descriptor shifted by whole pixel rows into that halo (stride 2 uses even/odd
+// de-interleaved halos so every tap is affine).
 // Weights: either resident in shared memory for the whole persistent kernel (the CTA's
 // N-split), or -- when a full-width layer does not fit (WS = 1: F3, R3) -- streamed with the
 // halo: each pipeline stage then carries the 16-channel chunk's 9 x 16 x Cout weights too
@@ -29,25 +31,19 @@ namespace conv {
 constexpr int TILE_M = 128;
 // bytes of one 8-channel plane of the halo in shared memory (128-byte aligned pieces)
 template <int S> struct Halo;
+// Stride 1: one TMA box {16 ch, 130 px, RR + 2 rows} over the 4-D view (C, W, H, frame); a
+// tile of RR output rows reads RR + 2 input rows.
 template <> struct Halo<1> {
   static constexpr int SLOTS = TILE_M + 2;                       // x0-1 .. x0+128
-  // both 8-channel planes of a 16-channel chunk come from ONE box (a 5-D view whose 4th
-  // dimension is the plane, stride 16 B), so each 32-byte sector is requested once.
-  // A tile of RR output rows reads RR + 2 input rows (planes are RR + 2 rows deep).
-  static constexpr int PLANE = 3 * SLOTS * 16;                   // (RR = 1)
-  static constexpr int TX = 3 * SLOTS * 16;
+  static constexpr int ROW = SLOTS * 32;                         // one halo row
 };
 // Stride 2: the halo is de-interleaved into even pixels 2(x0+i) and odd pixels 2(x0+i)-1 so
-// every tap is an affine window.  Each region is one TMA box of [3 rows][2 planes][x] over a
-// 5-D view (8 ch, parity, x/2, plane, frame*rows): both 8-channel planes of a chunk come from
-// one box (each 32-byte sector requested once), planes are LBO apart.
+// every tap is an affine window: one box {16 ch, 1, 128 | 129 px, 3 rows} per parity over the
+// 4-D view (C, parity, x/2, frame*rows).
 template <> struct Halo<2> {
-  static constexpr int EVEN_LBO = TILE_M * 16;                   // plane stride, even region
-  static constexpr int ODD_LBO = (TILE_M + 1) * 16;              // plane stride, odd region
-  static constexpr int EVEN_ROW = 2 * EVEN_LBO, ODD_ROW = 2 * ODD_LBO;
-  static constexpr int ODD_OFF = 3 * EVEN_ROW;
+  static constexpr int EVEN_ROW = TILE_M * 32, ODD_ROW = (TILE_M + 1) * 32;
+  static constexpr int ODD_OFF = 3 * EVEN_ROW;                   // 12288: 1024-aligned
   static constexpr int TX = 3 * EVEN_ROW + 3 * ODD_ROW;          // bytes per 16-channel chunk
-  static constexpr int PLANE = TX / 2;                           // (stage sizing: 2 x PLANE = TX)
 };
 
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
@@ -99,9 +95,8 @@ __global__ void __launch_bounds__(192, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
   static_assert(S == 1 || RR == 1, "multi-row tiles are stride-1 only");
-  constexpr int PLANE = S == 1 ? (RR + 2) * Halo<1>::SLOTS * 16 : HL::PLANE;
-  constexpr int TXB = S == 1 ? 2 * PLANE : HL::TX;         // bytes the TMA writes per stage
-  constexpr int SBA = (2 * PLANE + 127) / 128 * 128;   // a stage's halo: 16 channels = 2 planes (TMA dst: 128-B aligned)
+  constexpr int TXB = S == 1 ? (RR + 2) * Halo<1>::ROW : Halo<2>::TX;   // bytes the TMA writes per stage
+  constexpr int SBA = (TXB + 1023) / 1024 * 1024;   // a stage's halo (swizzled TMA dst: 1024-B aligned)
   constexpr int SBW = WS ? 9 * 2 * NS * 16 : 0;     // a stage's streamed weights (9 taps x 2 K-planes)
   constexpr int SB = SBA + SBW;
   constexpr int ACC = RR * NS;                      // TMEM columns of one tile's accumulators
@@ -164,11 +159,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if (WS) tc::bulk_g2s(sA + stage * SB + SBA, a.wimg + (size_t)c * SBW, SBW, full + stage);
           const int iy = S * oy - 1 + a.in_row_off;
           if (S == 1) {
-            tma_5d(dst, &tmA, 0, x0 - 1, iy, 2 * c, b, full + stage);   // both planes
+            tma_4d(dst, &tmA, 16 * c, x0 - 1, iy, b, full + stage);
           } else {   // frames are stacked along the row dimension: row b*Hbuf + iy (iy = -1: see the MMA)
             const int row = b * a.in_rows_buf + iy;
-            tma_5d(dst, &tmA, 0, 0, x0, 2 * c, row, full + stage);
-            tma_5d(dst + Halo<2>::ODD_OFF, &tmO, 0, 1, x0 - 1, 2 * c, row, full + stage);
+            tma_4d(dst, &tmA, 16 * c, 0, x0, row, full + stage);
+            tma_4d(dst + Halo<2>::ODD_OFF, &tmO, 16 * c, 1, x0 - 1, row, full + stage);
           }
           if (++stage == NST) { stage = 0; ph ^= 1; }
         }
@@ -204,11 +199,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                                    : tc::smem_desc(sWa + (uint32_t)((tap * (Cin / 8) + 2 * c) * NS * 16), NS * 16, 128);
 #pragma unroll
             for (int rr = 0; rr < RR; ++rr) {
-              uint32_t aoff, lbo;
-              if (S == 1) { aoff = ((rr + ky) * Halo<1>::SLOTS + kx) * 16; lbo = PLANE; }
-              else if (kx == 1) { aoff = ky * Halo<2>::EVEN_ROW; lbo = Halo<2>::EVEN_LBO; }
-              else { aoff = Halo<2>::ODD_OFF + ky * Halo<2>::ODD_ROW + (kx == 2 ? 16 : 0); lbo = Halo<2>::ODD_LBO; }
-              const uint64_t ad = tc::smem_desc(base + aoff, lbo, 128);
+              uint32_t aoff;
+              if (S == 1) aoff = (rr + ky) * Halo<1>::ROW + kx * 32;
+              else if (kx == 1) aoff = ky * Halo<2>::EVEN_ROW;
+              else aoff = Halo<2>::ODD_OFF + ky * Halo<2>::ODD_ROW + (kx == 2 ? 32 : 0);
+              const uint64_t ad = tc::smem_desc_sw32(base + aoff);
               tc::mma_f16_ss(d0 + rr * NS, ad, bd, IDESC, first ? 0u : 1u);
             }
             first = false;

@@ -184,32 +184,32 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C, int rr) {
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r;
   if (S == 1) {
-    // (8 channels, x, row, 8-channel plane, frame): a box of 2 planes = one 16-channel chunk
-    const cuuint64_t dims[5] = {8, (cuuint64_t)G.Wi, (cuuint64_t)G.Hi_buf, (cuuint64_t)C / 8, (cuuint64_t)B};
-    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)G.Wi * C * 2, 16, (cuuint64_t)G.Hi_buf * G.Wi * C * 2};
-    const cuuint32_t box[5] = {8, conv::Halo<1>::SLOTS, (cuuint32_t)(rr + 2), 2, 1};
-    r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // (C, x, row, frame): a box of {16 channels, 130 px, rr + 2 rows} = 32-byte pixel rows
+    const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)G.Wi, (cuuint64_t)G.Hi_buf, (cuuint64_t)B};
+    const cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)G.Wi * C * 2, (cuuint64_t)G.Hi_buf * G.Wi * C * 2};
+    const cuuint32_t box[4] = {16, conv::Halo<1>::SLOTS, (cuuint32_t)(rr + 2), 1};
+    r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     G.mO = G.mA;
   } else {
-    // (8 channels, parity, x/2, 8-channel plane, frame*rows)
-    const cuuint64_t dims[5] = {8, 2, (cuuint64_t)G.Wi / 2, (cuuint64_t)C / 8, (cuuint64_t)G.Hi_buf * B};
-    const cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, 16, (cuuint64_t)G.Wi * C * 2};
-    const cuuint32_t boxE[5] = {8, 1, conv::TILE_M, 2, 3};
-    const cuuint32_t boxO[5] = {8, 1, conv::TILE_M + 1, 2, 3};
-    r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // (C, parity, x/2, frame*rows)
+    const cuuint64_t dims[4] = {(cuuint64_t)C, 2, (cuuint64_t)G.Wi / 2, (cuuint64_t)G.Hi_buf * B};
+    const cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * 4, (cuuint64_t)G.Wi * C * 2};
+    const cuuint32_t boxE[4] = {16, 1, conv::TILE_M, 3};
+    const cuuint32_t boxO[4] = {16, 1, conv::TILE_M + 1, 3};
+    r = enc(&G.mA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in, dims, str, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS)
-      r = enc(&G.mO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, in, dims, str, boxO, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      r = enc(&G.mO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in, dims, str, boxO, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (r != CUDA_SUCCESS) return gn_fail(GLASSNET_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return 0;
 }
 
 static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost = 0, int rr = 1) {
-  const size_t plane = S == 1 ? (size_t)(rr + 2) * conv::Halo<1>::SLOTS * 16 : conv::Halo<2>::PLANE;
-  const size_t sb = (2 * plane + 127) / 128 * 128 + (ws ? (size_t)9 * 2 * NS * 16 : 0);
+  const size_t tx = S == 1 ? (size_t)(rr + 2) * conv::Halo<1>::ROW : conv::Halo<2>::TX;
+  const size_t sb = (tx + 1023) / 1024 * 1024 + (ws ? (size_t)9 * 2 * NS * 16 : 0);
   const size_t w = ws ? 0 : (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024;
   const size_t bias = ((size_t)NS * 4 + 127) / 128 * 128;
   return w + nstage * sb + (2 * nstage + 4) * 8 + bias + (ost ? (size_t)4 * 2 * 32 * NS * 2 : 0) + 128;

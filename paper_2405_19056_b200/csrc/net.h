@@ -24,8 +24,10 @@ struct StageProfiler {
     names.push_back(n);
     return (int)names.size() - 1;
   }
+  size_t dropped = 0;         // marks beyond the capacity given to profile_begin
   void mark(const char* n, cudaStream_t st) {
-    if (!on || used >= ev.size()) return;
+    if (!on) return;
+    if (used >= ev.size()) { ++dropped; return; }
     stage[used] = n ? id(n) : -1;
     cudaEventRecord(ev[used++], st);
   }

@@ -25,6 +25,22 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return d;
 }
 
+// K-major operand in the 32-byte swizzle layout: rows of 32 B (16 bf16 = one K=16 step), 8-row
+// atoms of 256 B (SBO), the two 16-byte halves of row r swapped when address bit 7 is set (the
+// pattern TMA's SWIZZLE_32B writes).  A start address may sit at any 32-byte row.
+__device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused: one K step per row)
+  d |= (uint64_t)(256 >> 4) << 32;        // SBO: 8 rows x 32 B
+  d |= (uint64_t)1 << 46;                 // version = 1 (tcgen05)
+#ifdef GN_SW32_BASE_OFFSET
+  d |= (uint64_t)((addr >> 7) & 7) << 49;
+#endif
+  d |= (uint64_t)6 << 61;                 // layout_type = SWIZZLE_32B
+  return d;
+}
+
 // ---- instruction descriptor, kind::f16, fp32 accumulator, K-major A and B ----
 // fmt: 0 = F16, 1 = BF16
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_fmt, int b_fmt) {
