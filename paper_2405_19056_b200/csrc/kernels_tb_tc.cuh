@@ -84,53 +84,79 @@ struct TbParams {
 };
 
 // ---------------------------------------------------------------------------------------
-// Pre-pass: per superblock of TB_SBP pixels, a stable counting sort by min(n, K) (absent
-// pixels, beyond P, last).  perm[sb*SBP + i] = (pixel offset in the superblock) | (count << 11).
+// Pre-pass: per superblock of TB_SBP pixels, a counting sort by min(n, K) (absent pixels,
+// beyond P, last).  perm[sb*SBP + i] = (pixel offset in the superblock) | (count << 11).
+// 256 threads x 8 consecutive pixels (one 8-byte load); the per-thread bin counts are packed
+// two 16-bit fields per word and prefix-summed across the block in one pass; the sorted
+// superblock is staged in shared memory and written with 16-byte stores.  The order inside
+// a bin is deterministic but irrelevant (every MMA row is independent).
 template <int K>
-__global__ void __launch_bounds__(128) k_tb_sort(const uint8_t* __restrict__ tcount, uint16_t* __restrict__ perm,
+__global__ void __launch_bounds__(256) k_tb_sort(const uint8_t* __restrict__ tcount, uint16_t* __restrict__ perm,
                                                  long P) {
-  __shared__ int wsum[4][K + 2];
-  const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
-  const long q0 = (long)blockIdx.x * TB_SBP;
-  int mj[TB_SBT];
+  static_assert(TB_SBP == 2048, "256 threads x 8 pixels");
+  constexpr int NB = K + 2, NV = (NB + 1) / 2;
+  __shared__ uint32_t wtot[8][NV];
+  __shared__ uint16_t soff[256][NB + 1];
+  __shared__ __align__(16) uint16_t sperm[TB_SBP];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const long q0 = (long)blockIdx.x * TB_SBP + 8 * t;
+  int bin[8];
+  if (q0 + 8 <= P && (reinterpret_cast<uintptr_t>(tcount + q0) & 7) == 0) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(tcount + q0));
 #pragma unroll
-  for (int j = 0; j < TB_SBT; ++j) {
-    const long q = q0 + j * 128 + r;
-    mj[j] = q < P ? min((int)__ldg(tcount + q), K) : K + 1;
+    for (int j = 0; j < 8; ++j) bin[j] = min((int)(((j < 4 ? u.x : u.y) >> (8 * (j & 3))) & 0xFF), K);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bin[j] = q0 + j < P ? min((int)__ldg(tcount + q0 + j), K) : K + 1;
   }
-  int cnt[K + 2], incl[K + 2];
+  uint32_t own[NV], v[NV];
 #pragma unroll
-  for (int b = 0; b < K + 2; ++b) {
-    int c = 0;
+  for (int i = 0; i < NV; ++i) {
+    uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < TB_SBT; ++j) c += mj[j] == b ? 1 : 0;
-    cnt[b] = c;
-    int x = c;
+    for (int j = 0; j < 8; ++j) c += (bin[j] >> 1) == i ? 1u << (16 * (bin[j] & 1)) : 0u;
+    own[i] = v[i] = c;
+  }
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if (lane >= o) x += y;
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v[i], o);
+      if (lane >= o) v[i] += y;
     }
-    incl[b] = x;
-    if (lane == 31) wsum[warp][b] = x;
-  }
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) wtot[warp][i] = v[i];
   __syncthreads();
+  uint32_t tot[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    uint32_t pre = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t x = wtot[w][i];
+      pre += w < warp ? x : 0u;
+      all += x;
+    }
+    v[i] = v[i] - own[i] + pre;   // exclusive prefix of this thread, per bin
+    tot[i] = all;
+  }
   int base = 0;
 #pragma unroll
-  for (int b = 0; b < K + 2; ++b) {
-    int woff = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int v = wsum[w][b];
-      woff += w < warp ? v : 0;
-      tot += v;
-    }
-    int pos = base + woff + incl[b] - cnt[b];
-#pragma unroll
-    for (int j = 0; j < TB_SBT; ++j)
-      if (mj[j] == b) perm[q0 + pos++] = (uint16_t)((j * 128 + r) | (b << 11));
-    base += tot;
+  for (int b = 0; b < NB; ++b) {
+    const int fld = 16 * (b & 1);
+    soff[t][b] = (uint16_t)(base + (int)((v[b >> 1] >> fld) & 0xFFFF));
+    base += (int)((tot[b >> 1] >> fld) & 0xFFFF);
   }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i < j; ++i) r += bin[i] == bin[j] ? 1 : 0;
+    sperm[soff[t][bin[j]] + r] = (uint16_t)((8 * t + j) | (bin[j] << 11));
+  }
+  __syncthreads();
+  reinterpret_cast<uint4*>(perm + (long)blockIdx.x * TB_SBP)[t] = reinterpret_cast<const uint4*>(sperm)[t];
 }
 
 template <int K, int H, int C0>

@@ -432,7 +432,7 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
   const long nsb = (P + TB_SBP - 1) / TB_SBP;
   if (nsb * TB_SBP > s->perm_cap) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "T kernel: %ld pixels exceed the workspace", P);
-  k_tb_sort<K><<<(unsigned)nsb, 128, 0, st>>>(tcount, s->perm, P);
+  k_tb_sort<K><<<(unsigned)nsb, 256, 0, st>>>(tcount, s->perm, P);
   auto kfn = k_tb_tc<K, H, C0, POOL>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   const long ntiles = nsb * TB_SBT;
