@@ -16,8 +16,9 @@
 // placed at column offset 11k - 8j (8 offset copies; two MMAs when the window crosses a
 // third plane).  Masked slots therefore never reach shared memory (reading R4: they may
 // hold any bits, NaN/Inf included) and the window's neighbouring columns are zeros or
-// finite valid records times zero weights.  The layer-1 bias is added in epilogue 1; A2
-// is written to TMEM (tcgen05.st) and layer 2 reads its A operand from TMEM.
+// finite valid records times zero weights.  The biases enter the accumulators through one
+// more MMA per layer (ONES x bias block; for layer 2 also the pool's magic 2^23); A2 is
+// written to TMEM (tcgen05.st) and layer 2 reads its A operand from TMEM.
 //
 // Warp specialisation.  A CTA runs NCH independent "chains"; a chain has three roles, all
 // indexed by tile row r = TMEM lane r:
@@ -79,8 +80,6 @@ struct TbParams {
   float wBn[32];         // B weight of the count channel n
   float WO[3 * 35];      // [3][C0+3]: output 1x1 over [d0 ; L_d] (L_d part zero if R does not take it)
   float bO[4];
-  float q2[64];          // 2^23 + b2 2^12 (fp32-rounded): the FFMA addend of the pool's fixed point
-  float b1[64];          // layer-1 bias (added in epilogue 1)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -170,8 +169,11 @@ struct TbLayout {
   static constexpr int W2_B = H * H * 2;
   static constexpr int WBT_B = C0 * H * 2;
   static constexpr int WBE_B = C0 * C0 * 2;
-  static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B;
+  static constexpr int ONES_B = 128 * 16 * 2;         // bias MMAs: A = ONES (columns 0..3 = 1)
+  static constexpr int BB_B = H * 16 * 2;              //            B = [b1 pieces] / [2^23, b2 2^12 pieces]
+  static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B + ONES_B + 2 * BB_B;
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBT = OFF_W2 + W2_B, OFF_WBE = OFF_WBT + WBT_B;
+  static constexpr int OFF_ONES = OFF_WBE + WBE_B, OFF_BB1 = OFF_ONES + ONES_B, OFF_BB2 = OFF_BB1 + BB_B;
   // one chain:
   static constexpr int CH_A1 = 0;                     // 2 buffers x A1_PL planes
   static constexpr int CH_E0 = CH_A1 + 2 * A1_PL * PL;          // 2 buffers x C0/8 planes
@@ -268,12 +270,16 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
       // layer 1 of slot k from operand buffer `buf`: the record's K-window starts in plane
       // j = 11k/8 at column offset o = 11k mod 8 (W1 copy o); a third plane needs a 2nd MMA
+      const uint64_t dONES = tc::smem_desc(tc::smem_u32(smem + S::OFF_ONES), PL, 128);
+      const uint64_t dBB1 = tc::smem_desc(tc::smem_u32(smem + S::OFF_BB1), H * 16, 128);
+      const uint64_t dBB2 = tc::smem_desc(tc::smem_u32(smem + S::OFF_BB2), H * 16, 128);
       auto layer1 = [&](int k, int buf) {
         const int j = (11 * k) >> 3, o = (11 * k) & 7;
         const uint32_t a = sA1 + (buf * S::A1_PL + j) * PL, w = sW1 + o * 4 * H * 16;
         tc::mma_f16_ss(t_acc1, tc::smem_desc(a, PL, 128), tc::smem_desc(w, H * 16, 128), ID_T, 0);
         if (o > 5)
           tc::mma_f16_ss(t_acc1, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
+        tc::mma_f16_ss(t_acc1, dONES, dBB1, ID_T, 1);   // + b1
       };
       uint32_t aph = 0, fph = 0, lph[2] = {0, 0}, f2ph[2] = {0, 0};
       for (int buf = 0;; buf ^= 1) {
@@ -292,6 +298,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           for (int q = 0; q < H / 16; ++q)
             tc::mma_f16_ts(t_acc2 + (t & 1) * H, t_a2 + q * 8, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T,
                            q > 0);
+          tc::mma_f16_ss(t_acc2 + (t & 1) * H, dONES, dBB2, ID_T, 1);   // + 2^23 + b2 2^12
           if (t + 1 < Kt) { layer1(t + 1, buf); tc::mma_commit(done1); }
           tc::mma_commit(done2 + (t & 1));
         }
@@ -332,8 +339,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         const int b = s & 1;
         tc::mbar_wait(done2 + b, d2ph[b]); d2ph[b] ^= 1;
         tc::fence_after_sync();
-        // pool += Q(acc2 + b2): acc2 carries the 2^12 scale (folded into W2), so x = acc2 + q2
-        // is 2^23 + (v + b2) 2^12 rounded; masked slots clamp to exactly 2^23 (0)
+        // pool += Q(a2): acc2 = 2^23 + (W2 a1 + b2) 2^12 (scale folded into W2, magic and bias
+        // added by the bias MMA), rounded to an integer in fp32; the clamps are the ReLU and the
+        // saturation, and masked slots clamp to exactly 2^23 (0)
         const float hi = (s < m) ? TB_QMAX : TB_QMAGIC;
 #pragma unroll
         for (int c = 0; c < H / 16; ++c) {
@@ -342,8 +350,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           tc::tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            float x = __uint_as_float(u[i]) + prm.q2[c * 16 + i];
-            x = fminf(fmaxf(x, TB_QMAGIC), hi);
+            const float x = fminf(fmaxf(__uint_as_float(u[i]), TB_QMAGIC), hi);
             pool[c * 16 + i] += __float_as_uint(x);
           }
         }
@@ -465,8 +472,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         uint32_t o[H / 2];
 #pragma unroll
         for (int i = 0; i < H / 2; ++i)
-          o[i] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * i]) + prm.b1[2 * i],
-                                     __uint_as_float(u[2 * i + 1]) + prm.b1[2 * i + 1]);
+          o[i] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));   // b1 is in acc1
 #pragma unroll
         for (int c = 0; c < H / 32; ++c) tc::tmem_st16(t_a2 + lane_off + 16 * c, o + 16 * c);
         tc::tmem_st_wait();

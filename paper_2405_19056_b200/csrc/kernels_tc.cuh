@@ -51,7 +51,7 @@ struct Geom {
 
 struct TcState {
   uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
-  TbParams tb_prm;              // bB, wBn, WO (c0+3 wide), bO, q2 (kernel parameters)
+  TbParams tb_prm;              // bB, wBn, WO (c0+3 wide), bO (kernel parameters)
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
@@ -117,8 +117,8 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   std::vector<uint8_t> img;
   // W1 in 8 column-offset copies [o][H][32]: the record's 11 weights at columns o..o+10
   // (depth column x 2^-7 when normalising; bf16-exact), zeros elsewhere.  Record k's K-window
-  // starts at halfword 11k = 8j + o of the row (kernels_tb_tc.cuh); the bias b1 is added in
-  // epilogue 1.
+  // starts at halfword 11k = 8j + o of the row (kernels_tb_tc.cuh); the bias b1 enters
+  // through the bias MMA below.
   for (int o = 0; o < 8; ++o) {
     std::vector<float> w1((size_t)H * 32, 0.f);
     for (int n = 0; n < H; ++n)
@@ -127,7 +127,7 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
     pack_kmajor(w1, H, 32, false, img);
   }
   // W2 [H][H], scaled by the pool's fixed-point scale 2^12 (exact: a power of two), so the
-  // accumulator is (W2 a1) 2^12; the layer-2 bias enters the conversion (q2 below)
+  // accumulator is (W2 a1) 2^12; the layer-2 bias enters through the bias MMA below
   std::vector<float> w2((size_t)H * H, 0.f);
   for (int o = 0; o < H; ++o)
     for (int i = 0; i < H; ++i) w2[(size_t)o * H + i] = rb(T2W[o * H + i]) * TB_QSCALE;
@@ -140,6 +140,21 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   }
   pack_kmajor(wbt, C0, H, true, img);
   pack_kmajor(wbe, C0, C0, false, img);
+  // The T biases enter the accumulators through one more MMA each, ONES (128 x 16, columns
+  // 0..3 = 1) times a bias block (H x 16): layer 1 += b1 (as three bf16 pieces, exact), and
+  // layer 2 += 2^23 + b2 2^12 (the pool's fixed-point magic and the pre-scaled bias, four
+  // exact pieces), issued after the weight MMAs so the products are summed in fp32 first.
+  std::vector<float> ones((size_t)128 * 16, 0.f), bb1((size_t)H * 16, 0.f), bb2((size_t)H * 16, 0.f);
+  for (int r = 0; r < 128; ++r)
+    for (int k = 0; k < 4; ++k) ones[(size_t)r * 16 + k] = 1.f;
+  for (int o = 0; o < H; ++o) {
+    split3(T1b[o], bb1[(size_t)o * 16 + 0], bb1[(size_t)o * 16 + 1], bb1[(size_t)o * 16 + 2]);
+    bb2[(size_t)o * 16 + 0] = TB_QMAGIC;
+    split3(T2b[o] * TB_QSCALE, bb2[(size_t)o * 16 + 1], bb2[(size_t)o * 16 + 2], bb2[(size_t)o * 16 + 3]);
+  }
+  pack_kmajor(ones, 128, 16, false, img);
+  pack_kmajor(bb1, H, 16, false, img);
+  pack_kmajor(bb2, H, 16, false, img);
   TbParams& prm = s->tb_prm;
   memset(&prm, 0, sizeof prm);
   for (int o = 0; o < C0; ++o) prm.bB[o] = Bb[o];
@@ -148,10 +163,6 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   for (int j = 0; j < 3; ++j)
     for (int i = 0; i < C0 + 3; ++i) prm.WO[j * (C0 + 3) + i] = i < NO ? rb(OW[(size_t)j * NO + i]) : 0.f;
   for (int j = 0; j < 3; ++j) prm.bO[j] = Ob[j];
-  // q2 = 2^23 + b2 2^12 rounded to fp32 (an integer): the FFMA addend of the pool's
-  // fixed-point conversion (kernels_tb_tc.cuh)
-  for (int o = 0; o < H; ++o) prm.q2[o] = TB_QMAGIC + T2b[o] * TB_QSCALE;
-  for (int o = 0; o < H; ++o) prm.b1[o] = T1b[o];
   s->perm_cap = ((long)d.max_batch * d.height * d.width + TB_SBP - 1) / TB_SBP * TB_SBP;
   if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess || cudaMalloc(&s->sched, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&s->perm, s->perm_cap * sizeof(uint16_t)) != cudaSuccess)
