@@ -424,7 +424,7 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       g.rows_f = G.rows[l - 1]; g.rows_f_buf = G.rows[l - 1] + 2 * h; g.grow0_f = G.grow0[l - 1];
       g.rows_c_buf = G.rows[l] + 2 * h; g.grow0_c = G.grow0[l]; g.Hc_full = G.Hfull[l]; g.halo = h;
       const int cv = c[l - 1] / 8, lcv = __builtin_ctz((unsigned)cv);
-      const dim3 grid((unsigned)(((long)G.W[l - 1] * cv + 255) / 256), (unsigned)G.rows[l - 1], (unsigned)B);
+      const dim3 grid((unsigned)(((long)(G.W[l - 1] / 2) * cv + 255) / 256), (unsigned)G.rows[l - 1], (unsigned)B);
       ew::k_up2add<<<grid, 256, 0, st>>>((const bf*)G.y[l], G.W[l], (const bf*)G.e[l - 1], (bf*)G.dd[l - 1],
                                          G.W[l - 1], c[l - 1], lcv, g);
       net->prof.mark("up2add", st);

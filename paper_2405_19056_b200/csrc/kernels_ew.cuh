@@ -12,6 +12,10 @@
 namespace gn {
 namespace ew {
 
+__device__ __forceinline__ uint32_t tc_cvt_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 __device__ __forceinline__ void bf8_to_f(const uint4& u, float v[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -56,35 +60,60 @@ __global__ void __launch_bounds__(256) k_prep_x(const __nv_bfloat16* __restrict_
 }
 
 // d[Y][X] = up2(y)[Y][X] + skip[Y][X] over C channels (reading R12/R14).  Thread = 8 channels
-// of one fine pixel; the 4 coarse taps and the skip are 16-byte loads.  lcv = log2(C / 8).
+// of the fine pixel pair X = 2i, 2i+1, which share coarse columns i-1, i, i+1 (edge-clamped):
+// 6 coarse + 2 skip 16-byte loads for two outputs, the bilinear weights applied separably
+// (rows, then columns) with packed fp32x2 FMAs.  lcv = log2(C / 8).
+__device__ __forceinline__ void bf8_to_f2(const uint4& u, float2 v[4]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+}
 __global__ void __launch_bounds__(256) k_up2add(const __nv_bfloat16* __restrict__ y, int w,
                                                 const __nv_bfloat16* __restrict__ skip, __nv_bfloat16* __restrict__ d,
                                                 int W2, int C, int lcv, Up2Rows g) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int X = t >> lcv;
-  if (X >= W2) return;
+  const int i = t >> lcv;
+  if (2 * i >= W2) return;
   const int c8 = (t & ((1 << lcv) - 1)) * 8;
   const int Y = blockIdx.y;
   const long b = blockIdx.z;
-  int ya, yb, xa, xb;
-  float wya, wyb, wxa, wxb;
+  int ya, yb;
+  float wya, wyb;
   up2_taps(g.grow0_f + Y, g.Hc_full, ya, yb, wya, wyb);
   ya += g.halo - g.grow0_c;
   yb += g.halo - g.grow0_c;
-  up2_taps(X, w, xa, xb, wxa, wxb);
+  const int xm = i > 0 ? i - 1 : 0, xp = i + 1 < w ? i + 1 : w - 1;
   const long yb0 = b * g.rows_c_buf;
-  const uint4 u00 = __ldg(reinterpret_cast<const uint4*>(y + ((yb0 + ya) * w + xa) * C + c8));
-  const uint4 u01 = __ldg(reinterpret_cast<const uint4*>(y + ((yb0 + ya) * w + xb) * C + c8));
-  const uint4 u10 = __ldg(reinterpret_cast<const uint4*>(y + ((yb0 + yb) * w + xa) * C + c8));
-  const uint4 u11 = __ldg(reinterpret_cast<const uint4*>(y + ((yb0 + yb) * w + xb) * C + c8));
-  const long q = ((b * g.rows_f_buf + Y + g.halo) * W2 + X) * C + c8;
-  const uint4 us = __ldg(reinterpret_cast<const uint4*>(skip + q));
-  float v00[8], v01[8], v10[8], v11[8], sk[8], o[8];
-  bf8_to_f(u00, v00); bf8_to_f(u01, v01); bf8_to_f(u10, v10); bf8_to_f(u11, v11); bf8_to_f(us, sk);
+  const __nv_bfloat16* ra = y + (yb0 + ya) * w * C + c8;
+  const __nv_bfloat16* rb = y + (yb0 + yb) * w * C + c8;
+  const uint4 am = __ldg(reinterpret_cast<const uint4*>(ra + (long)xm * C));
+  const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(ra + (long)i * C));
+  const uint4 ap = __ldg(reinterpret_cast<const uint4*>(ra + (long)xp * C));
+  const uint4 bm = __ldg(reinterpret_cast<const uint4*>(rb + (long)xm * C));
+  const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(rb + (long)i * C));
+  const uint4 bp = __ldg(reinterpret_cast<const uint4*>(rb + (long)xp * C));
+  const long q = ((b * g.rows_f_buf + Y + g.halo) * W2 + 2 * i) * C + c8;
+  const uint4 s0 = __ldg(reinterpret_cast<const uint4*>(skip + q));
+  const uint4 s1 = __ldg(reinterpret_cast<const uint4*>(skip + q + C));
+  float2 vam[4], va0[4], vap[4], vbm[4], vb0[4], vbp[4], vs0[4], vs1[4];
+  bf8_to_f2(am, vam); bf8_to_f2(a0, va0); bf8_to_f2(ap, vap);
+  bf8_to_f2(bm, vbm); bf8_to_f2(b0, vb0); bf8_to_f2(bp, vbp);
+  bf8_to_f2(s0, vs0); bf8_to_f2(s1, vs1);
+  const float2 WA = make_float2(wya, wya), WB = make_float2(wyb, wyb);
+  const float2 Q1 = make_float2(0.25f, 0.25f), Q3 = make_float2(0.75f, 0.75f);
+  uint32_t oe[4], oo[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    o[i] = (wya * wxa) * v00[i] + (wya * wxb) * v01[i] + (wyb * wxa) * v10[i] + (wyb * wxb) * v11[i] + sk[i];
-  *reinterpret_cast<uint4*>(d + q) = f_to_bf8(o);
+  for (int k = 0; k < 4; ++k) {
+    const float2 cm = __ffma2_rn(WB, vbm[k], __fmul2_rn(WA, vam[k]));   // rows blended, column i-1
+    const float2 c0 = __ffma2_rn(WB, vb0[k], __fmul2_rn(WA, va0[k]));   //                column i
+    const float2 cp = __ffma2_rn(WB, vbp[k], __fmul2_rn(WA, vap[k]));   //                column i+1
+    const float2 e = __ffma2_rn(Q3, c0, __ffma2_rn(Q1, cm, vs0[k]));    // X = 2i
+    const float2 o = __ffma2_rn(Q3, c0, __ffma2_rn(Q1, cp, vs1[k]));    // X = 2i+1
+    oe[k] = tc_cvt_bf16x2(e.x, e.y);
+    oo[k] = tc_cvt_bf16x2(o.x, o.y);
+  }
+  *reinterpret_cast<uint4*>(d + q) = make_uint4(oe[0], oe[1], oe[2], oe[3]);
+  *reinterpret_cast<uint4*>(d + q + C) = make_uint4(oo[0], oo[1], oo[2], oo[3]);
 }
 
 // out = sigmoid(up2(z) + psi) (reading R15: the output 1x1's level-1 part z is upsampled).

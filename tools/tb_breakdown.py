@@ -21,8 +21,9 @@ net.forward(g, d, t, n); torch.cuda.synchronize()
 L.glassnet_debug_tb_prof(buf, 0)
 v = list(buf)
 tiles, rounds = v[11], v[10] - v[11]
-names = {1: "E1 prologue (publish, e0, next records)", 3: "E1 slot: wait done1",
-         4: "E1 slot: epilogue 1 + arrive", 9: "E1 tile total",
+names = {12: "E1 prologue: to the named barrier", 13: "E1 prologue: named barrier", 14: "E1 prologue: Kt, arrives",
+         1: "E1 prologue (publish, e0, next records)", 3: "E1 slot: wait done1",
+         4: "E1 slot: epilogue 1 + arrive", 6: "E1 wait doneF", 8: "E1 final", 9: "E1 tile total",
          16: "E2 wait tstart", 17: "E2 ring entry: wait done2", 18: "E2 slot: pool", 21: "E2 final (accB entry)",
          22: "E2 tile total (after tstart)",
          24: "MMA wait rdyC", 25: "MMA wait loaded", 26: "MMA L1(0) issue (+B if Kt=0)",
