@@ -434,7 +434,7 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       Up2Rows g;
       g.rows_f = G.rows[0]; g.rows_f_buf = G.rows[0] + 2 * h; g.grow0_f = G.grow0[0];
       g.rows_c_buf = G.rows[1] + 2 * h; g.grow0_c = G.grow0[1]; g.Hc_full = G.Hfull[1]; g.halo = h;
-      const dim3 grid((unsigned)((G.W[0] + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
+      const dim3 grid((unsigned)((G.W[0] / 2 + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
       ew::k_output<<<grid, 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g);
       net->prof.mark("output", st);
       return 0;

@@ -117,31 +117,42 @@ __global__ void __launch_bounds__(256) k_up2add(const __nv_bfloat16* __restrict_
 }
 
 // out = sigmoid(up2(z) + psi) (reading R15: the output 1x1's level-1 part z is upsampled).
+// Thread = the fine pixel pair X = 2i, 2i+1 (coarse columns i-1, i, i+1 shared), separable
+// weights as in k_up2add; psi / out as 8-byte vectors.
 __global__ void __launch_bounds__(256) k_output(const float* __restrict__ z, int w, const float* __restrict__ psi,
                                                 float* __restrict__ out, int W, Up2Rows g) {
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= W) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * i >= W) return;
   const int Y = blockIdx.y;
   const long b = blockIdx.z;
-  const long p = (b * g.rows_f + Y) * W + X;
-  int ya, yb, xa, xb;
-  float wya, wyb, wxa, wxb;
+  const long p = (b * g.rows_f + Y) * W + 2 * i;
+  int ya, yb;
+  float wya, wyb;
   up2_taps(g.grow0_f + Y, g.Hc_full, ya, yb, wya, wyb);
   ya += g.halo - g.grow0_c;
   yb += g.halo - g.grow0_c;
-  up2_taps(X, w, xa, xb, wxa, wxb);
+  const int xm = i > 0 ? i - 1 : 0, xp = i + 1 < w ? i + 1 : w - 1;
   const long zb0 = b * g.rows_c_buf;
-  const float* z00 = z + ((zb0 + ya) * w + xa) * 3;
-  const float* z01 = z + ((zb0 + ya) * w + xb) * 3;
-  const float* z10 = z + ((zb0 + yb) * w + xa) * 3;
-  const float* z11 = z + ((zb0 + yb) * w + xb) * 3;
+  const float* za = z + (zb0 + ya) * w * 3;
+  const float* zb = z + (zb0 + yb) * w * 3;
+  const float2* ps = reinterpret_cast<const float2*>(psi + p * 3);   // 6 floats: 8-byte aligned (p even)
+  const float2 p01 = __ldg(ps), p23 = __ldg(ps + 1), p45 = __ldg(ps + 2);
+  const float pv[6] = {p01.x, p01.y, p23.x, p23.y, p45.x, p45.y};
+  float o[6];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    float l = (wya * wxa) * __ldg(z00 + c) + (wya * wxb) * __ldg(z01 + c) + (wyb * wxa) * __ldg(z10 + c) +
-              (wyb * wxb) * __ldg(z11 + c);
-    l += __ldg(psi + p * 3 + c);
-    out[p * 3 + c] = 1.f / (1.f + __expf(-l));
+    const float cm = wya * __ldg(za + xm * 3 + c) + wyb * __ldg(zb + xm * 3 + c);
+    const float c0 = wya * __ldg(za + i * 3 + c) + wyb * __ldg(zb + i * 3 + c);
+    const float cp = wya * __ldg(za + xp * 3 + c) + wyb * __ldg(zb + xp * 3 + c);
+    const float le = 0.25f * cm + 0.75f * c0 + pv[c];
+    const float lo = 0.75f * c0 + 0.25f * cp + pv[3 + c];
+    o[c] = 1.f / (1.f + __expf(-le));
+    o[3 + c] = 1.f / (1.f + __expf(-lo));
   }
+  float2* op = reinterpret_cast<float2*>(out + p * 3);
+  op[0] = make_float2(o[0], o[1]);
+  op[1] = make_float2(o[2], o[3]);
+  op[2] = make_float2(o[4], o[5]);
 }
 
 }  // namespace ew
