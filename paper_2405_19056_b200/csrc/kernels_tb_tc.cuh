@@ -179,7 +179,9 @@ struct TbLayout {
   static constexpr int CH_E0 = CH_A1 + 2 * A1_PL * PL;          // 2 buffers x C0/8 planes
   static constexpr int CH_TAU = CH_E0 + 2 * (C0 / 8) * PL;      // H/8 planes (f16)
   static constexpr int CH_MROW = CH_TAU + (H / 8) * PL;         // 128 x u8: the rows' valid counts
-  static constexpr int CH_B = CH_MROW + 128;
+  static constexpr int CH_NPIX = CH_MROW + 128;                 // 128 x i64: the NEXT tile's pixels (-1: none)
+  static constexpr int CH_NCNT = CH_NPIX + 128 * 8;             // 128 x u8 its counts; [128] = a next tile exists
+  static constexpr int CH_B = CH_NCNT + 144;
   static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 12 mbarrier slots; then the tmem ptr
   static constexpr int OFF_RED = OFF_BAR + 4 * 96 + 16;     // per chain 8 ints: warp max counts, Kt, tile ids
   static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 127) / 128 * 128;
@@ -238,7 +240,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   if (threadIdx.x == 0) {
     for (int c = 0; c < NCH; ++c) {
       uint64_t* b = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * c;
-      tc::mbar_init(b + 0, 128); tc::mbar_init(b + 1, 128);   // loaded[2]
+      tc::mbar_init(b + 0, 256); tc::mbar_init(b + 1, 256);   // loaded[2]: E2 (records) + E1 (e0)
       tc::mbar_init(b + 2, 128); tc::mbar_init(b + 3, 128);   // rdyA, rdyF
       tc::mbar_init(b + 4, 128); tc::mbar_init(b + 5, 128);   // free2[2]
       tc::mbar_init(b + 6, 1); tc::mbar_init(b + 7, 1); tc::mbar_init(b + 8, 1);   // done1, done2[2]
@@ -256,8 +258,35 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   const uint32_t t_acc1 = tmem, t_acc2 = tmem + H, t_accB = tmem + 3 * H, t_a2 = tmem + 3 * H + C0;
   uint8_t* chs = smem + S::OFF_CH + g * S::CH_B;
   volatile uint8_t* mrow = chs + S::CH_MROW;
+  volatile long long* nprow = reinterpret_cast<volatile long long*>(chs + S::CH_NPIX);
+  volatile uint8_t* ncnt = chs + S::CH_NCNT;
   const uint32_t sA1 = tc::smem_u32(chs + S::CH_A1), sE0 = tc::smem_u32(chs + S::CH_E0);
   const uint32_t sTAU = tc::smem_u32(chs + S::CH_TAU);
+  // copy row r's records of a tile (pixel pp, mm valid records) into operand buffer `buf`, zero
+  // fill beyond the valid bytes (E2 issues these for the next tile; E1 for the first)
+  auto fill_rec = [&](int r, int buf, long pp, int mm, bool ok) {
+    const uint32_t a = sA1 + buf * S::A1_PL * PL + r * 16;
+    const int vb = ok ? mm * 22 : 0;            // valid bytes of the row
+    if (S::ASYNC) {
+      const char* src = ok ? reinterpret_cast<const char*>(tbuf + pp * (K * 11)) : reinterpret_cast<const char*>(tbuf);
+#pragma unroll
+      for (int i = 0; i < S::NPL; ++i)
+        cp_async16z(a + i * PL, src + 16 * i, (uint32_t)min(max(vb - 16 * i, 0), 16));
+    } else {   // rows not 16-byte aligned in global memory: through registers
+      const uint16_t* src = tbuf + pp * (K * 11);
+#pragma unroll
+      for (int i = 0; i < S::NPL; ++i) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int e = 8 * i + 2 * h;
+          const uint32_t lo = 2 * e < vb ? __ldg(src + e) : 0u, hi = 2 * e + 2 < vb ? __ldg(src + e + 1) : 0u;
+          w[h] = lo | (hi << 16);
+        }
+        tc::sts128(a + i * PL, w[0], w[1], w[2], w[3]);
+      }
+    }
+  };
   const long ntiles = (P + TB_SBP - 1) / TB_SBP * TB_SBT;
 
   if (role == 2) {
@@ -326,11 +355,20 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     const int r = threadIdx.x & 127, warp = r >> 5;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     uint32_t tph = 0, d2ph[2] = {0, 0};
+    int nbuf = 1;                 // operand buffer of the next tile
+    tc::mbar_arrive(loaded + 0);  // the first tile's records are E1's
     for (;;) {
       tc::mbar_wait(tstart, tph); tph ^= 1;
       const int Kt = red[4];
       if (Kt < 0) break;
       const int m = mrow[r];
+      if (ncnt[128]) {   // the next tile's records into the other operand buffer (its last
+                         // reader, the tile before this one, has completed: E2 saw its last batch)
+        const long np = (long)nprow[r];
+        fill_rec(r, nbuf, np, ncnt[r], np >= 0);
+        cp_async_arrive(loaded + nbuf);
+      }
+      nbuf ^= 1;
       uint32_t pool[H];
 #pragma unroll
       for (int j = 0; j < H; ++j) pool[j] = 0;
@@ -385,29 +423,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       ok = tl < ntiles && pp < P;
       mm = ok ? (pe >> 11) : 0;
     };
-    // copy row r's operands of a tile (pixel pp, mm valid records) into operand buffer `buf`
-    auto fill = [&](int buf, long pp, int mm, bool ok) {
-      const uint32_t a = sA1 + buf * S::A1_PL * PL + r * 16;
-      const int vb = ok ? mm * 22 : 0;            // valid bytes of the row
-      if (S::ASYNC) {
-        const char* src = ok ? reinterpret_cast<const char*>(tbuf + pp * (K * 11)) : reinterpret_cast<const char*>(tbuf);
-#pragma unroll
-        for (int i = 0; i < S::NPL; ++i)
-          cp_async16z(a + i * PL, src + 16 * i, (uint32_t)min(max(vb - 16 * i, 0), 16));
-      } else {   // rows not 16-byte aligned in global memory: through registers
-        const uint16_t* src = tbuf + pp * (K * 11);
-#pragma unroll
-        for (int i = 0; i < S::NPL; ++i) {
-          uint32_t w[4];
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int e = 8 * i + 2 * h;
-            const uint32_t lo = 2 * e < vb ? __ldg(src + e) : 0u, hi = 2 * e + 2 < vb ? __ldg(src + e + 1) : 0u;
-            w[h] = lo | (hi << 16);
-          }
-          tc::sts128(a + i * PL, w[0], w[1], w[2], w[3]);
-        }
-      }
+    // copy row r's e0 of a tile into operand buffer `buf` (its records: fill_rec, by E2)
+    auto fill_e0 = [&](int buf, long pp, bool ok) {
       const uint32_t eb = sE0 + buf * (C0 / 8) * PL + r * 16;
       const uint16_t* es = ok ? e0 + pp * C0 : e0;
 #pragma unroll
@@ -426,13 +443,17 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     int m, nm;
     bool pv, npv;
     decode(tile, tile < ntiles ? (int)__ldg(perm + tile * 128 + r) : 0, p, m, pv);
-    if (tile < ntiles) fill(0, p, m, pv);
+    if (tile < ntiles) { fill_rec(r, 0, p, m, pv); fill_e0(0, p, pv); }
     decode(ntile, ntile < ntiles ? (int)__ldg(perm + ntile * 128 + r) : 0, np, nm, npv);
     for (int it = 0; tile < ntiles; ++it) {
       TBP_NOW(tp_t0);
       const int buf = it & 1;
-      // ---- prologue: publish the counts; copy the next tile's operands
+      // ---- prologue: publish the counts (and the next tile's pixels, whose records E2 copies);
+      // copy the next tile's e0
       mrow[r] = (uint8_t)m;
+      nprow[r] = npv ? (long long)np : -1ll;
+      ncnt[r] = (uint8_t)nm;
+      if (r == 0) ncnt[128] = ntile < ntiles ? 1 : 0;
       {
         const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
         if (lane == 0) red[warp] = wm;
@@ -450,7 +471,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
         ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
       }
-      if (ntile < ntiles) fill(buf ^ 1, np, nm, npv);   // buffer buf^1 was last read by the previous tile's MMAs
+      if (ntile < ntiles) fill_e0(buf ^ 1, np, npv);   // buffer buf^1's e0 was last read by the previous tile's accB batch
       const int nnpe = nntile < ntiles ? (int)__ldg(perm + nntile * 128 + r) : 0;   // decoded next iteration
       TBP_NOW(tp_t1);
       TBP_ADD(1, tp_t0, tp_t1);
