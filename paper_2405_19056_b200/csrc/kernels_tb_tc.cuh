@@ -319,6 +319,13 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::fence_after_sync();
         tc::fence_proxy_async();
         if (Kt > 0) { layer1(0, buf); tc::mma_commit(done1); }
+        // accB = e0 W_B,e0^T now (E1 read the previous tile's accB before publishing these
+        // counts); the tau part is added after the pool, so the tile's tail holds only it
+        const uint32_t e0b = sE0 + buf * (C0 / 8) * PL;
+#pragma unroll
+        for (int q = 0; q < C0 / 16; ++q)
+          tc::mma_f16_ss(t_accB, tc::smem_desc(e0b + 2 * q * PL, PL, 128),
+                         tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
         for (int t = 0; t < Kt; ++t) {
           tc::mbar_wait(rdyA, aph); aph ^= 1;      // A2 of slot t in TMEM (acc1 read)
           if (t >= 2) { tc::mbar_wait(free2 + (t & 1), f2ph[t & 1]); f2ph[t & 1] ^= 1; }   // acc2[t&1] read
@@ -336,11 +343,6 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::mbar_wait(rdyF, fph); fph ^= 1;        // tau written
         tc::fence_after_sync();
         tc::fence_proxy_async();
-        const uint32_t e0b = sE0 + buf * (C0 / 8) * PL;
-#pragma unroll
-        for (int q = 0; q < C0 / 16; ++q)
-          tc::mma_f16_ss(t_accB, tc::smem_desc(e0b + 2 * q * PL, PL, 128),
-                         tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
         if (Kt > 0) {
 #pragma unroll
           for (int q = 0; q < H / 16; ++q)
