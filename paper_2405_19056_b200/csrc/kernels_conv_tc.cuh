@@ -114,8 +114,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* sBias = reinterpret_cast<float*>(tempty + 4);                        // NS floats
-  uint8_t* sOut = reinterpret_cast<uint8_t*>(sBias) + ((NS * 4 + 127) / 128) * 128;   // OST: [4 warps][2][32][NS] bf16
+  float* sBias = reinterpret_cast<float*>(tempty + 4);                        // NS floats (EPI 1: + 3 x NS of wz)
+  uint8_t* sOut = reinterpret_cast<uint8_t*>(sBias) + ((NS * 4 * (EPI ? 4 : 1) + 127) / 128) * 128;   // OST: [4 warps][2][32][NS] bf16
 
   const int split = blockIdx.x % a.nsplit;
   if (!WS) {  // resident weights of this split
@@ -124,6 +124,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
   }
   for (int i = tid; i < NS; i += blockDim.x) sBias[i] = a.bias[split * NS + i];
+  if (EPI == 1)   // the z projection's weights (EPI 1 runs unsplit: NS = Cout)
+    for (int i = tid; i < 3 * NS; i += blockDim.x) sBias[NS + i] = a.wz[i];
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(tfull + i, 1); tc::mbar_init(tempty + i, 128); }
@@ -272,9 +274,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int o = c * 16 + i;
-              z0 = fmaf(__ldg(a.wz + o), y[i], z0);
-              z1 = fmaf(__ldg(a.wz + NS + o), y[i], z1);
-              z2 = fmaf(__ldg(a.wz + 2 * NS + o), y[i], z2);
+              z0 = fmaf(sBias[NS + o], y[i], z0);
+              z1 = fmaf(sBias[2 * NS + o], y[i], z1);
+              z2 = fmaf(sBias[3 * NS + o], y[i], z2);
             }
           }
         }

@@ -218,11 +218,11 @@ static int make_halo_maps(int S, ConvGeom& G, void* in, int B, int C, int rr) {
   return 0;
 }
 
-static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost = 0, int rr = 1) {
+static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost = 0, int rr = 1, int epi = 0) {
   const size_t tx = S == 1 ? (size_t)(rr + 2) * conv::Halo<1>::ROW : conv::Halo<2>::TX;
   const size_t sb = (tx + 1023) / 1024 * 1024 + (ws ? (size_t)9 * 2 * NS * 16 : 0);
   const size_t w = ws ? 0 : (((size_t)9 * Cin * NS * 2 + 1023) / 1024) * 1024;
-  const size_t bias = ((size_t)NS * 4 + 127) / 128 * 128;
+  const size_t bias = ((size_t)NS * 4 * (epi ? 4 : 1) + 127) / 128 * 128;   // bias (+ the z projection's 3 x NS)
   return w + nstage * sb + (2 * nstage + 4) * 8 + bias + (ost ? (size_t)4 * 2 * 32 * NS * 2 : 0) + 128;
 }
 
@@ -234,11 +234,11 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
   int NS = Cout;
   // full width with resident weights if they fit; else full width with the weights streamed
   // per channel chunk (no N-split: an N-split re-reads the halo and multiplies the MMA count)
-  L.ws = (conv_smem(S, Cin, Cout, 2) > LIMIT && Cout <= 256 && conv_smem(S, Cin, Cout, 2, 1) <= LIMIT && epi == 0 &&
+  L.ws = (conv_smem(S, Cin, Cout, 2, 0, 0, 1, epi) > LIMIT && Cout <= 256 && conv_smem(S, Cin, Cout, 2, 1, 0, 1, epi) <= LIMIT && epi == 0 &&
           !getenv("GN_CONV_NO_STREAM")) ? 1 : 0;
   if (!L.ws)
-    while (NS > 16 && conv_smem(S, Cin, NS, 2) > LIMIT) NS /= 2;
-  if (conv_smem(S, Cin, NS, 2, L.ws) > LIMIT || (epi == 1 && NS != Cout))
+    while (NS > 16 && conv_smem(S, Cin, NS, 2, 0, 0, 1, epi) > LIMIT) NS /= 2;
+  if (conv_smem(S, Cin, NS, 2, L.ws, 0, 1, epi) > LIMIT || (epi == 1 && NS != Cout))
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv %d->%d does not fit shared memory", Cin, Cout);
   L.NS = NS;
   L.nsplit = Cout / NS;
@@ -247,23 +247,23 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
   L.rr = 1;
   if (S == 1)
     for (int rr : {4, 2})
-      if (2 * rr * NS <= 512 && conv_smem(S, Cin, NS, 2, L.ws, 0, rr) <= LIMIT) { L.rr = rr; break; }
+      if (2 * rr * NS <= 512 && conv_smem(S, Cin, NS, 2, L.ws, 0, rr, epi) <= LIMIT) { L.rr = rr; break; }
   if (const char* e = getenv("GN_CONV_RR")) if (S == 1) L.rr = atoi(e);
   L.nstage = 4;
-  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws, 0, L.rr) > LIMIT) --L.nstage;
+  while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws, 0, L.rr, epi) > LIMIT) --L.nstage;
   // staged (bulk-copied) output when it fits without giving up pipeline depth
-  L.ost = (epi == 0 && !L.ws && conv_smem(S, Cin, NS, L.nstage, L.ws, 1, L.rr) <= LIMIT && !getenv("GN_CONV_NO_OST"))
+  L.ost = (epi == 0 && !L.ws && conv_smem(S, Cin, NS, L.nstage, L.ws, 1, L.rr, epi) <= LIMIT && !getenv("GN_CONV_NO_OST"))
               ? 1 : 0;
-  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws, L.ost, L.rr);
+  L.smem = conv_smem(S, Cin, NS, L.nstage, L.ws, L.ost, L.rr, epi);
   const int acc2 = 2 * L.rr * NS;
   const int tcols = acc2 <= 32 ? 32 : acc2 <= 64 ? 64 : acc2 <= 128 ? 128 : acc2 <= 256 ? 256 : 512;
   // a tcgen05.mma issue blocks its thread for about one MMA, so two CTAs per SM (two MMA
   // issuers) beat a deeper pipeline: trade stages for a second CTA when TMEM allows it
   if (2 * tcols <= 512)
     for (int ns = L.nstage; ns >= 2; --ns)
-      if (2 * (conv_smem(S, Cin, NS, ns, L.ws, L.ost, L.rr) + 1024) <= 232448) {
+      if (2 * (conv_smem(S, Cin, NS, ns, L.ws, L.ost, L.rr, epi) + 1024) <= 232448) {
         L.nstage = ns;
-        L.smem = conv_smem(S, Cin, NS, ns, L.ws, L.ost, L.rr);
+        L.smem = conv_smem(S, Cin, NS, ns, L.ws, L.ost, L.rr, epi);
         break;
       }
   L.ctas_per_sm = (int)(232448 / (L.smem + 1024));
