@@ -384,14 +384,15 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         // saturation, and masked slots clamp to exactly 2^23 (0)
         const float hi = (s < m) ? TB_QMAX : TB_QMAGIC;
 #pragma unroll
-        for (int c = 0; c < H / 16; ++c) {
-          uint32_t u[16];
-          tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 16, u);
+        for (int c = 0; c < H / 32; ++c) {   // two 16-column loads in flight per wait
+          uint32_t u[32];
+          tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[16]>(u));
+          tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(u + 16));
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < 32; ++i) {
             const float x = fminf(fmaxf(__uint_as_float(u[i]), TB_QMAGIC), hi);
-            pool[c * 16 + i] += __float_as_uint(x);
+            pool[c * 32 + i] += __float_as_uint(x);
           }
         }
         tc::fence_before_sync();
