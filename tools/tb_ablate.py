@@ -4,9 +4,19 @@ usage: python tools/tb_ablate.py libname.so [libname2.so ...]  (each in its own 
 import os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if len(sys.argv) > 2 or (len(sys.argv) == 2 and not sys.argv[1].startswith("--one=")):
-    for name in sys.argv[1:]:
-        out = subprocess.run([sys.executable, __file__, "--one=" + name], capture_output=True, text=True, timeout=300)
-        print(f"{name:40s} {out.stdout.strip()} {out.stderr.strip()[-300:] if out.returncode else ''}")
+    reps = int(os.environ.get("TB_REPS", "1"))
+    res = {n: [] for n in sys.argv[1:]}
+    for _ in range(reps):   # interleaved, so box drift hits every library alike
+        for name in sys.argv[1:]:
+            out = subprocess.run([sys.executable, __file__, "--one=" + name], capture_output=True, text=True, timeout=300)
+            if out.returncode:
+                print(f"{name:40s} FAILED {out.stderr.strip()[-300:]}")
+                continue
+            res[name].append(float(out.stdout.split()[1]))
+    for name, v in res.items():
+        v = sorted(v)
+        if v:
+            print(f"{name:40s} T_B_psi min {v[0]:.3f} median {v[len(v) // 2]:.3f} ms over {len(v)}")
     sys.exit(0)
 name = sys.argv[1][6:]
 sys.path.insert(0, ROOT)
