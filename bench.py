@@ -328,7 +328,8 @@ def run_ours(args):
                     "mean_valid_fragments": mean_n}
             metric = METRIC
         line = {"metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "ms_per_frame": ms / args.steps / frames_per_step, "higher_is_better": True,
                 "scaling": "strong" if tiles_mode else "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded generator, synth/)",
                 "config": cfgj,
