@@ -96,8 +96,11 @@ int glassnet_forward(glassnet_t net, const void* gbuf, const void* direct, const
                      const uint8_t* tcount, float* out, int32_t batch, glassnet_stream_t stream);
 
 /* Same as glassnet_forward but with HOST buffers (pinned for best speed): copies the
- * inputs host->device on `stream`, runs the forward, copies `out` back and
- * synchronises the stream before returning (the end-to-end user call). */
+ * inputs host->device, runs the forward on `stream`, copies `out` back and synchronises
+ * before returning (the end-to-end user call).  Pipelined in chunks of up to 4 frames:
+ * the copies run on the handle's own two copy streams and overlap the forward of the
+ * neighbouring chunk; the result is bitwise the whole-batch forward's (frames are
+ * independent).  Host buffers must stay valid until the call returns. */
 int glassnet_forward_host(glassnet_t net, const void* gbuf, const void* direct,
                           const void* tbuf, const uint8_t* tcount, float* out, int32_t batch,
                           glassnet_stream_t stream);

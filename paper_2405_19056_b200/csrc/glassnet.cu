@@ -219,6 +219,8 @@ extern "C" void glassnet_destroy(glassnet_t net) {
   void* ptrs[] = {net->w_tb, net->wz, net->x16, net->psi, net->z, net->st_g, net->st_d, net->st_t,
                   net->st_n, net->st_o};
   for (void* q : ptrs) if (q) cudaFree(q);
+  if (net->st_in) cudaStreamDestroy(net->st_in);
+  if (net->st_out) cudaStreamDestroy(net->st_out);
   for (int i = 0; i < 8; ++i) { if (net->convW[i]) cudaFree(net->convW[i]); if (net->convB[i]) cudaFree(net->convB[i]); }
   for (int i = 0; i < 4; ++i) { if (net->e[i]) cudaFree(net->e[i]); if (net->y[i]) cudaFree(net->y[i]); if (net->dd[i]) cudaFree(net->dd[i]); }
   gn::tc_release(net);
@@ -503,16 +505,55 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
     CUDA_TRY(cudaMalloc(&net->st_n, MB * P));
     CUDA_TRY(cudaMalloc((void**)&net->st_o, MB * P * 3 * sizeof(float)));
   }
+  if (!net->st_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&net->st_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&net->st_out, cudaStreamNonBlocking));
+  }
+  // Pipelined in chunks of frames: the copy-in of chunk i+1 (stream st_in) and the copy-out of
+  // chunk i-1 (st_out) overlap the forward of chunk i (the caller's stream); chunks use
+  // disjoint frame ranges of the staging buffers, and frames are independent (R21), so the
+  // result equals one whole-batch forward bit for bit.
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t Bn = (size_t)batch;
-  CUDA_TRY(cudaMemcpyAsync(net->st_g, gbuf, Bn * P * 12 * es, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(net->st_d, direct, Bn * P * 3 * es, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(net->st_t, tbuf, Bn * P * d.k_slots * 11 * es, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(net->st_n, tcount, Bn * P, cudaMemcpyHostToDevice, st));
-  int rc = glassnet_forward(net, net->st_g, net->st_d, net->st_t, (const uint8_t*)net->st_n, net->st_o, batch, stream);
+  const int CF = batch < 4 ? batch : 4;
+  const int nch = (batch + CF - 1) / CF;
+  std::vector<cudaEvent_t> ev_in(nch), ev_c(nch);
+  for (int i = 0; i < nch; ++i) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_c[i], cudaEventDisableTiming));
+  }
+  cudaEvent_t ev0;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ev0, st));               // the copies follow earlier work on the caller's stream
+  CUDA_TRY(cudaStreamWaitEvent(net->st_in, ev0, 0));
+  int rc = GLASSNET_OK;
+  for (int i = 0; i < nch && rc == GLASSNET_OK; ++i) {
+    const size_t f0 = (size_t)i * CF, nf = (size_t)((i + 1) * CF <= batch ? CF : batch - i * CF);
+    const char* hg = (const char*)gbuf + f0 * P * 12 * es;
+    const char* hd = (const char*)direct + f0 * P * 3 * es;
+    const char* ht = (const char*)tbuf + f0 * P * d.k_slots * 11 * es;
+    char* dg = (char*)net->st_g + f0 * P * 12 * es;
+    char* dd = (char*)net->st_d + f0 * P * 3 * es;
+    char* dt = (char*)net->st_t + f0 * P * d.k_slots * 11 * es;
+    uint8_t* dn = (uint8_t*)net->st_n + f0 * P;
+    float* dout = net->st_o + f0 * P * 3;
+    CUDA_TRY(cudaMemcpyAsync(dg, hg, nf * P * 12 * es, cudaMemcpyHostToDevice, net->st_in));
+    CUDA_TRY(cudaMemcpyAsync(dd, hd, nf * P * 3 * es, cudaMemcpyHostToDevice, net->st_in));
+    CUDA_TRY(cudaMemcpyAsync(dt, ht, nf * P * d.k_slots * 11 * es, cudaMemcpyHostToDevice, net->st_in));
+    CUDA_TRY(cudaMemcpyAsync(dn, tcount + f0 * P, nf * P, cudaMemcpyHostToDevice, net->st_in));
+    CUDA_TRY(cudaEventRecord(ev_in[i], net->st_in));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev_in[i], 0));
+    rc = glassnet_forward(net, dg, dd, dt, dn, dout, (int32_t)nf, stream);
+    if (rc) break;
+    CUDA_TRY(cudaEventRecord(ev_c[i], st));
+    CUDA_TRY(cudaStreamWaitEvent(net->st_out, ev_c[i], 0));
+    CUDA_TRY(cudaMemcpyAsync(out + f0 * P * 3, dout, nf * P * 3 * sizeof(float), cudaMemcpyDeviceToHost, net->st_out));
+  }
+  const cudaError_t e1 = cudaStreamSynchronize(net->st_in), e2 = cudaStreamSynchronize(net->st_out),
+                    e3 = cudaStreamSynchronize(st);
+  for (int i = 0; i < nch; ++i) { cudaEventDestroy(ev_in[i]); cudaEventDestroy(ev_c[i]); }
+  cudaEventDestroy(ev0);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(out, net->st_o, Bn * P * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3);
   return GLASSNET_OK;
 }
 

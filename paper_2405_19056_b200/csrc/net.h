@@ -70,6 +70,7 @@ struct glassnet {
   // staging for glassnet_forward_host
   void *st_g = nullptr, *st_d = nullptr, *st_t = nullptr, *st_n = nullptr;
   float* st_o = nullptr;
+  cudaStream_t st_in = nullptr, st_out = nullptr;   // forward_host's copy streams (created on first use)
   // tensor-core state (kernels_tc.cuh)
   void* tc_state = nullptr;
   StageProfiler prof;

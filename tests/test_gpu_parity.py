@@ -136,6 +136,24 @@ def test_empty_and_full_counts(cuda_ok, family):
         assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1], (fill, mx)
 
 
+def test_forward_host_chunked_equals_device(cuda_ok):
+    """glassnet_forward_host pipelines chunks of <= 4 frames over copy streams: bitwise the
+    whole-batch device forward (frames are independent, R21; T's count sort regroups pixels
+    across the chunk boundary, which by construction changes no per-pixel result)."""
+    import torch
+    from synth import device
+    cfg = _cfg("h", 96, 128, 6, 8, "bf16")
+    net = net_for(cfg)
+    g, d, t, n = device.alloc_and_fill(cfg)
+    ref = net.forward(g, d, t, n)
+    torch.cuda.synchronize()
+    hg, hd, ht, hn = (x.cpu().pin_memory() for x in (g, d, t, n))
+    hout = torch.empty(ref.shape, dtype=torch.float32).pin_memory()
+    net.forward_host(hg, hd, ht, hn, hout)
+    assert torch.equal(hout, ref.cpu())
+    net.close()
+
+
 def test_workspace_independent_of_K(cuda_ok):
     """P12 (fig:MemUsage): the library's workspace does not grow with K."""
     sizes = []
