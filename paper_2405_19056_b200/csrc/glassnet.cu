@@ -618,6 +618,25 @@ extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int
   return GLASSNET_OK;
 }
 
+#ifdef GN_MBAR_WATCHDOG
+static unsigned int* gn_wd_host = nullptr;
+// diagnostic: map a host log the mbarrier watchdog writes before it traps (read after a failure)
+extern "C" int glassnet_debug_watchdog(unsigned int* out8, int init) {
+  if (init) {
+    if (!gn_wd_host) {
+      if (cudaHostAlloc((void**)&gn_wd_host, 64, cudaHostAllocMapped) != cudaSuccess) return -1;
+      unsigned int* dptr = nullptr;
+      cudaHostGetDevicePointer((void**)&dptr, gn_wd_host, 0);
+      cudaMemcpyToSymbol(gn::gn_wd_log, &dptr, sizeof dptr);
+    }
+    memset(gn_wd_host, 0, 64);
+    return 0;
+  }
+  for (int i = 0; i < 8; ++i) out8[i] = gn_wd_host ? ((volatile unsigned int*)gn_wd_host)[i] : 0u;
+  return 0;
+}
+#endif
+
 #ifdef GN_PROFILE_TB
 extern "C" int glassnet_debug_tb_prof(unsigned long long* out32, int reset) {
   cudaDeviceSynchronize();

@@ -153,6 +153,29 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+#ifdef GN_MBAR_WATCHDOG
+// diagnostic builds only: a wait that spins ~seconds records (1, block, thread, barrier smem
+// address, phase) into mapped host memory and traps, so a hang becomes a report
+}  // namespace tc
+__device__ unsigned int* gn_wd_log = nullptr;   // (the product library is one translation unit)
+namespace tc {
+__device__ __noinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  for (long long i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+    if (ok) return;
+    if (i == (1ll << 22)) {
+      volatile unsigned int* L = gn_wd_log;
+      if (L && atomicCAS((unsigned int*)L, 0u, 1u) == 0u) {
+        L[1] = blockIdx.x; L[2] = threadIdx.x; L[3] = smem_u32(bar); L[4] = phase;
+        __threadfence_system();
+      }
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -164,6 +187,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
