@@ -174,17 +174,23 @@ struct TbLayout {
   static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B + ONES_B + 2 * BB_B;
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBT = OFF_W2 + W2_B, OFF_WBE = OFF_WBT + WBT_B;
   static constexpr int OFF_ONES = OFF_WBE + WBE_B, OFF_BB1 = OFF_ONES + ONES_B, OFF_BB2 = OFF_BB1 + BB_B;
-  // one chain:
-  static constexpr int CH_A1 = 0;                     // 2 buffers x A1_PL planes
-  static constexpr int CH_E0 = CH_A1 + 2 * A1_PL * PL;          // 2 buffers x C0/8 planes
+  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 12 mbarrier slots; then the tmem ptr
+  static constexpr int OFF_RED = OFF_BAR + 4 * 96 + 16;     // per chain 8 ints: warp max counts, Kt, tile ids
+  static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 127) / 128 * 128;
+  // one chain: the layer-1 operand is double-buffered (the next tile's records copied during
+  // this tile) unless that leaves room for only one chain, where two single-buffered chains
+  // fit instead (K = 16: 352-byte records); single-buffered, E2 copies the next tile's records
+  // right after this tile's last layer-2 batch, overlapping the tile's tail
+  static constexpr int CH_REST = 2 * (C0 / 8) * PL + (H / 8) * PL + 128 + 128 * 8 + 144;
+  static constexpr int AVAIL = 232448 - 1024 - OFF_CH;
+  static constexpr int A1_NB = (AVAIL / (2 * A1_PL * PL + CH_REST) >= 2 || AVAIL / (A1_PL * PL + CH_REST) < 2) ? 2 : 1;
+  static constexpr int CH_A1 = 0;                     // A1_NB buffers x A1_PL planes
+  static constexpr int CH_E0 = CH_A1 + A1_NB * A1_PL * PL;      // 2 buffers x C0/8 planes
   static constexpr int CH_TAU = CH_E0 + 2 * (C0 / 8) * PL;      // H/8 planes (f16)
   static constexpr int CH_MROW = CH_TAU + (H / 8) * PL;         // 128 x u8: the rows' valid counts
   static constexpr int CH_NPIX = CH_MROW + 128;                 // 128 x i64: the NEXT tile's pixels (-1: none)
   static constexpr int CH_NCNT = CH_NPIX + 128 * 8;             // 128 x u8 its counts; [128] = a next tile exists
   static constexpr int CH_B = CH_NCNT + 144;
-  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 12 mbarrier slots; then the tmem ptr
-  static constexpr int OFF_RED = OFF_BAR + 4 * 96 + 16;     // per chain 8 ints: warp max counts, Kt, tile ids
-  static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 127) / 128 * 128;
   static constexpr int TCOLS = (3 * H + C0 + H / 2 + 31) / 32 * 32;   // acc1, acc2 x2, accB, A2 (packed)
   static constexpr int NCH_T = 512 / TCOLS;
   static constexpr int NCH_S = (232448 - 1024 - OFF_CH) / CH_B;
@@ -231,8 +237,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   TBP_INIT();
   for (int i = threadIdx.x; i < S::WIMG_B / 16; i += blockDim.x)
     reinterpret_cast<int4*>(smem)[i] = reinterpret_cast<const int4*>(wimg)[i];
-  for (int c = 0; c < NCH; ++c)   // the zero pad planes of both A1 buffers
-    for (int i = threadIdx.x; i < 2 * 2 * (int)PL / 16; i += blockDim.x) {
+  for (int c = 0; c < NCH; ++c)   // the zero pad planes of the A1 buffers
+    for (int i = threadIdx.x; i < S::A1_NB * 2 * (int)PL / 16; i += blockDim.x) {
       const int b = i / (2 * PL / 16), o = i % (2 * PL / 16);
       reinterpret_cast<int4*>(smem + S::OFF_CH + c * S::CH_B + S::CH_A1 + (b * S::A1_PL + S::NPL) * PL)[o] =
           make_int4(0, 0, 0, 0);
@@ -304,7 +310,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       const uint64_t dBB2 = tc::smem_desc(tc::smem_u32(smem + S::OFF_BB2), H * 16, 128);
       auto layer1 = [&](int k, int buf) {
         const int j = (11 * k) >> 3, o = (11 * k) & 7;
-        const uint32_t a = sA1 + (buf * S::A1_PL + j) * PL, w = sW1 + o * 4 * H * 16;
+        const uint32_t a = sA1 + ((S::A1_NB == 2 ? buf : 0) * S::A1_PL + j) * PL, w = sW1 + o * 4 * H * 16;
         tc::mma_f16_ss(t_acc1, tc::smem_desc(a, PL, 128), tc::smem_desc(w, H * 16, 128), ID_T, 0);
         if (o > 5)
           tc::mma_f16_ss(t_acc1, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
@@ -364,13 +370,19 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       const int Kt = red[4];
       if (Kt < 0) break;
       const int m = mrow[r];
-      if (ncnt[128]) {   // the next tile's records into the other operand buffer (its last
-                         // reader, the tile before this one, has completed: E2 saw its last batch)
-        const long np = (long)nprow[r];
-        fill_rec(r, nbuf, np, ncnt[r], np >= 0);
-        cp_async_arrive(loaded + nbuf);
-      }
-      nbuf ^= 1;
+      // the next tile's records: double-buffered, now into the other operand buffer (its last
+      // reader, the tile before this one, has completed: E2 saw its last batch); single-
+      // buffered, after this tile's last layer-2 batch (all its layer-1 MMAs have completed)
+      const bool has_next = ncnt[128] != 0;
+      const long np_next = has_next ? (long)nprow[r] : -1;
+      const int nm_next = has_next ? (int)ncnt[r] : 0;
+      auto fill_next = [&]() {
+        if (has_next) {
+          fill_rec(r, S::A1_NB == 2 ? nbuf : 0, np_next, nm_next, np_next >= 0);
+          cp_async_arrive(loaded + nbuf);
+        }
+      };
+      if (S::A1_NB == 2) fill_next();
       uint32_t pool[H];
 #pragma unroll
       for (int j = 0; j < H; ++j) pool[j] = 0;
@@ -398,6 +410,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::fence_before_sync();
         tc::mbar_arrive(free2 + b);
       }
+      if (S::A1_NB == 1) fill_next();
+      nbuf ^= 1;
       if (Kt > 0) {   // tau = pool (f16) -> its operand
         const uint32_t off = (uint32_t)Kt * TB_QBITS;
         const float sc = (POOL == 1 && m > 0) ? (1.f / TB_QSCALE) / (float)m : 1.f / TB_QSCALE;
