@@ -96,14 +96,15 @@ def test_mean_pool_and_c0_net_bf16(cuda_ok, family):
 
 
 @pytest.mark.parametrize("family", FAMILIES)
-@pytest.mark.parametrize("prec", ["bf16", "fp32"])
-def test_permutation_garbage_bitwise(cuda_ok, family, prec):
+@pytest.mark.parametrize("prec,K", [("bf16", 8), ("bf16", 16), ("fp32", 8)])
+def test_permutation_garbage_bitwise(cuda_ok, family, prec, K):
     """P3/P4 on the GPU: permuting the valid slots and filling masked slots with NaN/Inf
-    bit patterns gives a bitwise-identical output (table:OrderLoss P:666-679; R4, R5)."""
+    bit patterns gives a bitwise-identical output (table:OrderLoss P:666-679; R4, R5).
+    K = 16 runs the T kernel's single-buffered layer-1 operand."""
     if prec == "fp32" and family == "tc":
         pytest.skip("fp32 check mode has only the FFMA family")
     rng = np.random.default_rng(5)
-    cfg = _cfg("p", 32, 48, 1, 8, prec)
+    cfg = _cfg("p", 32, 48, 1, K, prec)
     fr = synth.gen_frames(cfg)
     out, net = _run(cfg, fr, family)
     tb = fr.tbuf.copy()
@@ -114,7 +115,7 @@ def test_permutation_garbage_bitwise(cuda_ok, family, prec):
         for x in range(48):
             m = int(n[y, x])
             tb[0, y, x, :m] = fr.tbuf[0, y, x, rng.permutation(m)]
-            tb[0, y, x, m:] = rng.choice(garbage, size=(8 - m, 11))
+            tb[0, y, x, m:] = rng.choice(garbage, size=(K - m, 11))
     fr2 = synth.Frames(fr.gbuf, fr.direct, tb, fr.tcount, prec)
     out2, _ = _run(cfg, fr2, family, net)
     assert np.array_equal(out.view(np.uint32), out2.view(np.uint32))
