@@ -245,7 +245,8 @@ def run_ours(args):
     value = frames_per_step * args.steps / (ms / 1000.0)
 
     # per-stage times (events after every launch, same stream; a second pass of K steps)
-    launches = net.launches_per_forward(B)
+    # (a row tile also builds x16 for its halo exchange: one more launch than the full frame)
+    launches = net.launches_per_forward(B) + (1 if tiles_mode and args.family == "tc" else 0)
     net.profile_begin(launches * args.steps + 2)
     for _ in range(args.steps):
         run()

@@ -109,7 +109,8 @@ int glassnet_forward_host(glassnet_t net, const void* gbuf, const void* direct,
 size_t glassnet_workspace_bytes(glassnet_t net);
 size_t glassnet_weight_bytes(glassnet_t net);
 
-/* Number of kernel launches one glassnet_forward of `batch` frames enqueues. */
+/* Number of kernel launches one glassnet_forward of `batch` frames enqueues
+ * (glassnet_forward_sharded's row tile adds one: the x16 input stage for its halo exchange). */
 int glassnet_launches_per_forward(glassnet_t net, int32_t batch);
 
 /* Select the kernel family for bf16 mode: 1 = tcgen05 tensor-core kernels (default

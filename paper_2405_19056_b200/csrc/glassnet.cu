@@ -246,9 +246,9 @@ extern "C" int glassnet_launches_per_forward(glassnet_t net, int32_t batch) {
   if (!net) return 0;
   const int L = net->d.levels;
   (void)batch;
-  // prep, F_0..F_{L-1}, T (+ its count-sort pre-pass on the tensor-core family), R_{L-1}..R_1,
-  // up2add at levels L-2..1, output
-  return 1 + L + (net->tc ? 2 : 1) + (L - 1) + (L - 2) + 1;
+  // prep (SIMT family only), F_0..F_{L-1}, T (+ its count-sort pre-pass on the tensor-core
+  // family), R_{L-1}..R_1, up2add at levels L-2..1, output
+  return (net->tc ? 0 : 1) + L + (net->tc ? 2 : 1) + (L - 1) + (L - 2) + 1;   // (tc: F0 reads the G-buffer)
 }
 
 // ------------------------------------------------------------------------ forward (SIMT family)
@@ -402,15 +402,18 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
   typedef __nv_bfloat16 bf;
   switch (sp.kind) {
     case ST_PREP: {
+      // the full frame's F0 reads the G-buffer itself (k_conv_tc<..., GB = 1>); a row tile
+      // builds x16 (with its halo rows exchanged) -- unnormalised: F0's weights carry R9
+      if (!tile) return 0;
       bf* x = (bf*)G.x16 + (size_t)h * G.W[0] * 16;
       const dim3 grid((unsigned)((G.W[0] + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
-      ew::k_prep_x<<<grid, 256, 0, st>>>((const bf*)gbuf, (const bf*)direct, x, G.W[0], G.rows[0],
-                                         (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
+      ew::k_prep_x<<<grid, 256, 0, st>>>((const bf*)gbuf, (const bf*)direct, x, G.W[0], G.rows[0], 0);
       net->prof.mark("prep_x", st);
       return 0;
     }
     case ST_CONV: {
-      int rc = launch_conv(net, s->conv[sp.idx], G.cg[sp.idx], B, st);
+      int rc = (!tile && sp.idx == 0) ? launch_conv(net, s->conv[0], G.cg[0], B, st, gbuf, direct)
+                                      : launch_conv(net, s->conv[sp.idx], G.cg[sp.idx], B, st);
       net->prof.mark(kConvNames[sp.idx], st);
       return rc;
     }

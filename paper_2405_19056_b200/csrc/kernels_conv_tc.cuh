@@ -75,6 +75,9 @@ struct ConvArgs {
   int in_rows_buf;       // input buffer rows per frame (stride-2 view stacks frames along rows)
   int out_row_off;       // output buffer row of output row 0
   int out_rows_buf;      // output buffer rows per frame
+  const uint16_t* gbuf;  // GB = 1 (F0 on the full frame): [B][H][W][12] bf16, read directly
+  const uint16_t* direct;   //                                  [B][H][W][3]
+  int Wi;                // input width (GB = 1)
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
@@ -90,8 +93,12 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 // 16-byte per-thread stores that touch every sector twice.
 // RR: output rows per tile (stride 1 only): the RR rows share RR + 2 halo rows (each input
 // row is read from L2 (RR + 2) / RR times instead of 3 times); RR accumulators of NS columns.
-template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1>
-__global__ void __launch_bounds__(192, 1)
+// GB = 1 (F0 only, full frame): the producer warp builds the halo itself from the G-buffer
+// and L_d (one pixel row = [G(12), L_d(3), 0], the input normalisation folded into F0's
+// weights, exactly) in the same SWIZZLE_32B layout TMA writes, so x16 is never stored.
+constexpr int GB_PRODUCERS = 5;   // GB = 1: warps 0 and 6..9 build the halo
+template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1, int GB = 0>
+__global__ void __launch_bounds__(GB ? 320 : 192, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
   static_assert(S == 1 || RR == 1, "multi-row tiles are stride-1 only");
@@ -127,7 +134,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (EPI == 1)   // the z projection's weights (EPI 1 runs unsplit: NS = Cout)
     for (int i = tid; i < 3 * NS; i += blockDim.x) sBias[NS + i] = a.wz[i];
   if (tid == 0) {
-    for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
+    for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, GB ? GB_PRODUCERS : 1); tc::mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(tfull + i, 1); tc::mbar_init(tempty + i, 128); }
     tc::fence_mbar_init();
   }
@@ -144,7 +151,55 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const int cta = blockIdx.x / a.nsplit, ncta = gridDim.x / a.nsplit;
   const int nchunk = Cin / 16;
 
-  if (warp == 0) {
+  if (GB && (warp == 0 || warp >= 6)) {   // ---------------- G-buffer producers (5 warps), one 16-channel chunk
+    const int pw = warp == 0 ? 0 : warp - 5;
+    static_assert(!GB || (S == 1 && WS == 0), "GB: the stride-1 first layer");
+    int stage = 0;
+    uint32_t ph = 0;
+    for (long t = cta; t < ntiles; t += ncta) {
+      const int xt = (int)(t % ntx);
+      const long r = t / ntx;
+      const int oy = (int)(r % nry) * RR;
+      const int b = (int)(r / nry);
+      const int x0 = xt * TILE_M;
+      if (lane == 0) tc::mbar_wait(empty + stage, ph ^ 1);
+      __syncwarp();
+      const uint32_t base = tc::smem_u32(sA + stage * SB);
+      // all of this thread's pixels' loads first (up to NPT in flight), then the stores
+      constexpr int NSLOT = (RR + 2) * Halo<1>::SLOTS, NPT = (NSLOT + 32 * GB_PRODUCERS - 1) / (32 * GB_PRODUCERS);
+      uint32_t w[NPT][8];
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) {
+        const int slot = pw * 32 + lane + k * 32 * GB_PRODUCERS;
+        const int y = slot / Halo<1>::SLOTS, sx = slot - y * Halo<1>::SLOTS;
+        const int gy = oy - 1 + y, gx = x0 - 1 + sx;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[k][i] = 0;
+        if (slot < NSLOT && gy >= 0 && gy < a.in_rows_buf && gx >= 0 && gx < a.Wi) {
+          const long p = ((long)b * a.in_rows_buf + gy) * a.Wi + gx;
+          const uint2* g = reinterpret_cast<const uint2*>(a.gbuf + p * 12);
+          const uint2 g0 = __ldg(g), g1 = __ldg(g + 1), g2 = __ldg(g + 2);
+          const uint16_t* dl = a.direct + p * 3;
+          w[k][0] = g0.x; w[k][1] = g0.y; w[k][2] = g1.x; w[k][3] = g1.y; w[k][4] = g2.x; w[k][5] = g2.y;
+          w[k][6] = (uint32_t)__ldg(dl) | ((uint32_t)__ldg(dl + 1) << 16);
+          w[k][7] = (uint32_t)__ldg(dl + 2);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) {
+        const int slot = pw * 32 + lane + k * 32 * GB_PRODUCERS;
+        if (slot < NSLOT) {
+          const uint32_t row = base + (uint32_t)slot * 32, sw = (row >> 7) & 1u;   // SWIZZLE_32B
+          tc::sts128(row + (sw << 4), w[k][0], w[k][1], w[k][2], w[k][3]);
+          tc::sts128(row + ((sw ^ 1u) << 4), w[k][4], w[k][5], w[k][6], w[k][7]);
+        }
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(full + stage);
+      if (++stage == NST) { stage = 0; ph ^= 1; }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t ph = 0;

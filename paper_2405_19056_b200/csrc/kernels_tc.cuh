@@ -228,7 +228,7 @@ static size_t conv_smem(int S, int Cin, int NS, int nstage, int ws = 0, int ost 
 
 // One conv layer: choose the N split so the split's weights stay resident, pack them.
 static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const float* bias, int cin_real, int Cin,
-                      int Cout, int epi) {
+                      int Cout, int epi, const float* in_scale = nullptr) {
   constexpr size_t LIMIT = 232448 - 1024;
   L.used = true; L.S = S; L.Cin = Cin; L.Cout = Cout; L.epi = epi;
   int NS = Cout;
@@ -279,7 +279,8 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
         for (int n = 0; n < NS; ++n)
           for (int kk = 0; kk < 8; ++kk) {
             const int co = sp * NS + n, ci = 8 * j + kk;
-            const float v = ci < cin_real ? W[((size_t)co * 9 + t) * cin_real + ci] : 0.f;
+            const float v = ci < cin_real ? W[((size_t)co * 9 + t) * cin_real + ci] * (in_scale ? in_scale[ci] : 1.f)
+                                          : 0.f;
             const size_t idx = L.ws ? (((((size_t)(j / 2) * 9 + t) * 2 + (j % 2)) * NS + n) * 8 + kk)
                                     : (((((size_t)sp * 9 + t) * (Cin / 8) + j) * NS + n) * 8 + kk);
             img[idx] = h_bf16(v);
@@ -297,7 +298,14 @@ inline int tc_setup_convs(glassnet* net, const std::vector<const float*>& FW, co
   const glassnet_dims& d = net->d;
   const int L = d.levels;
   const int* c = d.widths;
-  int rc = setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], 0);
+  // F0's weights carry the input normalisation (reading R9: position x 2^-3, depth x 2^-7 --
+  // powers of two, so bf16(W) x scale is exact and each MMA product equals the one on the
+  // normalised input bit for bit): F0 then reads the raw G-buffer (full frame: directly, no
+  // x16; row tiles: x16 built without normalisation)
+  float sc0[16];
+  for (int i = 0; i < 16; ++i) sc0[i] = 1.f;
+  if (d.flags & GLASSNET_FLAG_INPUT_NORM) { sc0[0] = sc0[1] = sc0[2] = 0.125f; sc0[11] = 0.0078125f; }
+  int rc = setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], 0, sc0);
   for (int l = 1; l < L && !rc; ++l) rc = setup_conv(net, s->conv[l], 2, FW[l], net->convB[l], c[l - 1], c[l - 1], c[l], 0);
   for (int l = L - 1; l >= 1 && !rc; --l)
     rc = setup_conv(net, s->conv[4 + l], 1, RW[l], net->convB[4 + l], c[l], c[l], c[l - 1], l == 1 ? 1 : 0);
@@ -382,23 +390,37 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
   return 0;
 }
 
-template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1>
-static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
-  auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST, RR>;
+template <int S, int NS, int EPI, int WS, int OST, int RR, int GB = 0>
+static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
+                          const void* gbuf = nullptr, const void* direct = nullptr) {
+  auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST, RR, GB>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   conv::ConvArgs a;
   a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
   a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
   a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
   a.in_rows_buf = G.Hi_buf;
+  a.gbuf = reinterpret_cast<const uint16_t*>(gbuf); a.direct = reinterpret_cast<const uint16_t*>(direct); a.Wi = G.Wi;
   const long ntiles = (long)B * ((G.Ho + RR - 1) / RR) * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
   long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
   if (per_split > ntiles) per_split = ntiles;
   if (per_split < 1) per_split = 1;
-  kfn<<<(unsigned)(per_split * L.nsplit), 192, L.smem, st>>>(G.mA, G.mO, a);
+  kfn<<<(unsigned)(per_split * L.nsplit), GB ? 320 : 192, L.smem, st>>>(G.mA, G.mO, a);
 }
 
-static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st) {
+static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
+                       const void* gbuf = nullptr, const void* direct = nullptr) {
+  if (gbuf) {   // F0 straight from the G-buffer (full frame)
+#define CONV_GB(NS_, OST_, RR_)                                                                          \
+    if (L.S == 1 && L.NS == NS_ && L.epi == 0 && L.ws == 0 && L.ost == OST_ && L.rr == RR_) {           \
+      launch_conv_k<1, NS_, 0, 0, OST_, RR_, 1>(net, L, G, B, st, gbuf, direct);                       \
+      return 0;                                                                                         \
+    }
+    CONV_GB(16, 0, 4) CONV_GB(16, 1, 4) CONV_GB(32, 0, 4) CONV_GB(32, 1, 4)
+    CONV_GB(16, 0, 2) CONV_GB(16, 1, 2) CONV_GB(32, 0, 2) CONV_GB(32, 1, 2)
+#undef CONV_GB
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "F0 from the G-buffer: NS=%d ost=%d rr=%d", L.NS, L.ost, L.rr);
+  }
 #define CONV_K(S_, NS_, E_, WS_, OST_, RR_)                                                              \
   if (L.S == S_ && L.NS == NS_ && L.epi == E_ && L.ws == WS_ && L.ost == OST_ && L.rr == RR_) {         \
     launch_conv_k<S_, NS_, E_, WS_, OST_, RR_>(net, L, G, B, st);                                       \
