@@ -96,9 +96,9 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 // GB = 1 (F0 only, full frame): the producer warp builds the halo itself from the G-buffer
 // and L_d (one pixel row = [G(12), L_d(3), 0], the input normalisation folded into F0's
 // weights, exactly) in the same SWIZZLE_32B layout TMA writes, so x16 is never stored.
-constexpr int GB_PRODUCERS = 5;   // GB = 1: warps 0 and 6..9 build the halo
+constexpr int GB_PRODUCERS = 7;   // GB = 1: warps 0 and 6..11 build the halo
 template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1, int GB = 0>
-__global__ void __launch_bounds__(GB ? 320 : 192, 1)
+__global__ void __launch_bounds__(GB ? 32 * (5 + GB_PRODUCERS) : 192, GB ? 2 : 1)
 k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, const ConvArgs a) {
   using HL = Halo<S>;
   static_assert(S == 1 || RR == 1, "multi-row tiles are stride-1 only");
@@ -151,7 +151,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const int cta = blockIdx.x / a.nsplit, ncta = gridDim.x / a.nsplit;
   const int nchunk = Cin / 16;
 
-  if (GB && (warp == 0 || warp >= 6)) {   // ---------------- G-buffer producers (5 warps), one 16-channel chunk
+  if (GB && (warp == 0 || warp >= 6)) {   // ---------------- G-buffer producers, one 16-channel chunk
     const int pw = warp == 0 ? 0 : warp - 5;
     static_assert(!GB || (S == 1 && WS == 0), "GB: the stride-1 first layer");
     int stage = 0;

@@ -405,7 +405,7 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
   long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
   if (per_split > ntiles) per_split = ntiles;
   if (per_split < 1) per_split = 1;
-  kfn<<<(unsigned)(per_split * L.nsplit), GB ? 320 : 192, L.smem, st>>>(G.mA, G.mO, a);
+  kfn<<<(unsigned)(per_split * L.nsplit), GB ? 32 * (5 + conv::GB_PRODUCERS) : 192, L.smem, st>>>(G.mA, G.mO, a);
 }
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
