@@ -9,7 +9,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tb
 ncu -i /tmp/tb.ncu-rep --page raw --csv > gpurun_out/tb_raw_${SUF:-r1d}.csv 2>/dev/null
 timeout 900 ncu --set full --clock-control none -k regex:k_conv_tc -s 7 -c 7 -o /tmp/conv $B > /dev/null 2>&1
 ncu -i /tmp/conv.ncu-rep --page raw --csv > gpurun_out/conv_raw_${SUF:-r1d}.csv 2>/dev/null
-timeout 600 ncu --set full --clock-control none -k regex:"k_up2add|k_prep_x|k_output|k_tb_sort" -s 5 -c 5 -o /tmp/ew $B > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:"k_up2add|k_prep_x|k_output|k_tb_sort" -s 4 -c 4 -o /tmp/ew $B > /dev/null 2>&1
 ncu -i /tmp/ew.ncu-rep --page raw --csv > gpurun_out/ew_raw_${SUF:-r1d}.csv 2>/dev/null
 rm -f /tmp/*.ncu-rep
 ls -la gpurun_out/
