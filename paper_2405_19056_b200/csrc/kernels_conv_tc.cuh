@@ -16,7 +16,8 @@
 // halo: each pipeline stage then carries the 16-channel chunk's 9 x 16 x Cout weights too
 // (one bulk copy), so N = Cout in one pass instead of re-reading the halo per N-split.
 // Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner),
-// 2..5 = epilogue (TMEM -> bias/ReLU -> bf16 NHWC store, or the z projection of R_1).
+// 2..5 = epilogue (TMEM -> bias/ReLU -> bf16 NHWC store, or the z projection of R_1);
+// GB = 1 (F0 on the full frame): warps 0 and 6.. build the halo from the G-buffer instead.
 // Accumulators are double-buffered in TMEM so the epilogue overlaps the next tile.
 #pragma once
 #include <cuda.h>
