@@ -33,8 +33,8 @@
 //                 tau = pool (f16)                   -> MMA: accB = e0 W_B,e0^T + tau W_B,tau^T
 //   MMA (1 warp)  one thread issues every tcgen05.mma of the chain, and executes the
 //                 generic -> async proxy fence for the operands the others wrote.
-// Hand-offs are mbarriers: loaded[b] (cp.async completion of operand buffer b), rdyA
-// (E1 -> MMA: counts published / A2 written), tstart (E1 -> E2), free2[b] (E2 -> MMA: acc2
+// Hand-offs are mbarriers: loaded[b] (cp.async completion of operand buffer b), rdyC (E1 ->
+// MMA: counts published), rdyA (E1 -> MMA: A2 written), tstart (E1 -> E2), free2[b] (E2 -> MMA: acc2
 // buffer b read), rdyF (E2 -> MMA: tau written), done1 (commit -> E1, batches holding a
 // layer-1 MMA), done2[b] (commit -> E2, layer-2 batches into buffer b) and doneF (commit ->
 // E1, the accB batch).  Each waiter can be at most one
@@ -231,6 +231,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   uint64_t* done2 = bars + 7;      // [2]
   uint64_t* tstart = bars + 9;
   uint64_t* doneF = bars + 10;
+  uint64_t* rdyC = bars + 11;      // E1 -> MMA: a tile's counts published (separate from rdyA: E1's
+                                   // round 0 may follow at once when layer 1 was issued early)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 4 * 96);
   volatile int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 8 * g;   // [0..3] warp max, [4] Kt, [5..7] tile ids
 
@@ -252,6 +254,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       tc::mbar_init(b + 6, 1); tc::mbar_init(b + 7, 1); tc::mbar_init(b + 8, 1);   // done1, done2[2]
       tc::mbar_init(b + 9, 128);                              // tstart
       tc::mbar_init(b + 10, 1);                               // doneF
+      tc::mbar_init(b + 11, 128);                             // rdyC
     }
     tc::fence_mbar_init();
   }
@@ -316,15 +319,22 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           tc::mma_f16_ss(t_acc1, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
         tc::mma_f16_ss(t_acc1, dONES, dBB1, ID_T, 1);   // + b1
       };
-      uint32_t aph = 0, fph = 0, lph[2] = {0, 0}, f2ph[2] = {0, 0};
+      uint32_t aph = 0, cph = 0, fph = 0, lph[2] = {0, 0}, f2ph[2] = {0, 0};
+      bool have_l1 = false;   // this tile's first layer-1 batch was issued after the previous tile
       for (int buf = 0;; buf ^= 1) {
-        tc::mbar_wait(rdyA, aph); aph ^= 1;        // the tile's counts
+        tc::mbar_wait(rdyC, cph); cph ^= 1;        // the tile's counts
         const int Kt = red[4];
         if (Kt < 0) break;
-        tc::mbar_wait(loaded + buf, lph[buf]); lph[buf] ^= 1;   // its records and e0 (cp.async)
-        tc::fence_after_sync();
-        tc::fence_proxy_async();
-        if (Kt > 0) { layer1(0, buf); tc::mma_commit(done1); }
+        const bool next_exists = ncnt[128] != 0;   // written with these counts
+        if (!have_l1) {   // (always issued, also for Kt = 0: E1 consumes one layer-1 commit per tile)
+          tc::mbar_wait(loaded + buf, lph[buf]); lph[buf] ^= 1;   // its records and e0 (cp.async)
+          tc::fence_after_sync();
+          tc::fence_proxy_async();
+          layer1(0, buf);
+          tc::mma_commit(done1);
+        } else {
+          tc::fence_after_sync();
+        }
         // accB = e0 W_B,e0^T now (E1 read the previous tile's accB before publishing these
         // counts); the tau part is added after the pool, so the tile's tail holds only it
         const uint32_t e0b = sE0 + buf * (C0 / 8) * PL;
@@ -356,6 +366,19 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
                            tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
         }
         tc::mma_commit(doneF);
+        // the next tile's first layer-1 batch now: acc1 is free (E1 read this tile's last slot
+        // before the tail), so E1's round 0 of the next tile does not wait for it.  Only after a
+        // tile with slot rounds: E1's rdyA arrivals then prove it has consumed every earlier
+        // layer-1 commit (after a Kt = 0 tile nothing would stop this commit from landing two
+        // phases ahead of E1's wait -- the parity would alias)
+        have_l1 = next_exists && Kt > 0;
+        if (have_l1) {
+          tc::mbar_wait(loaded + (buf ^ 1), lph[buf ^ 1]); lph[buf ^ 1] ^= 1;
+          tc::fence_after_sync();
+          tc::fence_proxy_async();
+          layer1(0, buf ^ 1);
+          tc::mma_commit(done1);
+        }
       }
     }
   } else if (role == 1) {
@@ -480,7 +503,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       const int Kt = max(max(red[0], red[1]), max(red[2], red[3]));
       const long nntile = red[5 + (it + 2) % 3];
       if (r == 0) red[4] = Kt;
-      tc::mbar_arrive(rdyA);
+      tc::mbar_arrive(rdyC);
       tc::mbar_arrive(tstart);
       float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;   // consumed after the slot rounds (latency hidden)
       if (pv) {
@@ -494,6 +517,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       TBP_ADD(1, tp_t0, tp_t1);
       TBP_ADD(10, 0, Kt + 1);
       TBP_ADD(11, 0, 1);
+      if (Kt == 0) { tc::mbar_wait(done1, d1ph); d1ph ^= 1; }   // the tile's (unused) first layer-1 batch
       // ---- slot rounds: A2 of slot t -> TMEM
 #pragma unroll 1
       for (int t = 0; t < Kt; ++t) {
@@ -559,7 +583,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     tc::bar_sync(bar_id, 128);
     if (r == 0) red[4] = -1;
     tc::bar_sync(bar_id, 128);
-    tc::mbar_arrive(rdyA);
+    tc::mbar_arrive(rdyC);
     tc::mbar_arrive(tstart);
   }
   tc::fence_before_sync();
