@@ -215,3 +215,18 @@ def test_full_size_c3_bench_config(cuda_ok):
 
 def test_full_size_c4(cuda_ok):
     _full_size("c4", [0], [(0, 0), (1080, 1920), (2144, 3808)])
+
+
+def test_repeated_forwards_bitwise(cuda_ok):
+    """Many back-to-back forwards (the T kernel's mbarrier pipeline across tiles, K = 8 double-
+    and K = 16 single-buffered): every output bitwise equal to the first (S:572 run-to-run)."""
+    import torch
+    from synth import device
+    for cfg, reps in ((_cfg("r8", 96, 272, 3, 8, "bf16"), 60), (_cfg("r16", 64, 136, 2, 16, "bf16"), 60)):
+        net = net_for(cfg)
+        g, d, t, n = device.alloc_and_fill(cfg)
+        first = net.forward(g, d, t, n).clone()
+        for _ in range(reps):
+            out = net.forward(g, d, t, n)
+            assert torch.equal(out, first)
+        net.close()
