@@ -402,6 +402,10 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
   typedef __nv_bfloat16 bf;
   switch (sp.kind) {
     case ST_PREP: {
+      {   // T's count sort, on its own stream beside the encoder (kernels_tc.cuh)
+        const int rc = tc_launch_sort(net, tcount, P0, st);
+        if (rc) return rc;
+      }
       // the full frame's F0 reads the G-buffer itself (k_conv_tc<..., GB = 1>); a row tile
       // builds x16 (with its halo rows exchanged) -- unnormalised: F0's weights carry R9
       if (!tile) return 0;

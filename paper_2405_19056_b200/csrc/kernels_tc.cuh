@@ -51,6 +51,8 @@ struct Geom {
 
 struct TcState {
   uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
+  cudaStream_t sort_st = nullptr;   // the count sort runs here, beside the F encoder
+  cudaEvent_t ev_fwd = nullptr, ev_sorted = nullptr;
   TbParams tb_prm;              // bB, wBn, WO (c0+3 wide), bO (kernel parameters)
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
@@ -454,6 +456,9 @@ inline void tc_release(glassnet* net) {
   if (s->tile) { for (void* q : s->tile->owned) cudaFree(q); delete s->tile; }
   if (s->sched) cudaFree(s->sched);
   if (s->perm) cudaFree(s->perm);
+  if (s->sort_st) cudaStreamDestroy(s->sort_st);
+  if (s->ev_fwd) cudaEventDestroy(s->ev_fwd);
+  if (s->ev_sorted) cudaEventDestroy(s->ev_sorted);
   delete s;
   net->tc_state = nullptr;
 }
@@ -465,7 +470,8 @@ static int launch_tb_tc_kp(glassnet* net, const __nv_bfloat16* tbuf, const uint8
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
   const long nsb = (P + TB_SBP - 1) / TB_SBP;
   if (nsb * TB_SBP > s->perm_cap) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "T kernel: %ld pixels exceed the workspace", P);
-  k_tb_sort<K><<<(unsigned)nsb, 256, 0, st>>>(tcount, s->perm, P);
+  (void)tcount;
+  cudaStreamWaitEvent(st, s->ev_sorted, 0);   // k_tb_sort (tc_launch_sort) ran beside the encoder
   auto kfn = k_tb_tc<K, H, C0, POOL>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   const long ntiles = nsb * TB_SBT;
@@ -501,6 +507,37 @@ static int launch_tb_tc_h(glassnet* net, const __nv_bfloat16* tbuf, const uint8_
 #undef KCASE
   }
   return gn_fail(GLASSNET_ERR_UNSUPPORTED, "k_slots");
+}
+
+// The T kernel's count-sort pre-pass reads only the input counts, so it runs on its own stream
+// at the start of the forward, overlapping the F encoder; the T launch waits for it.
+inline int tc_launch_sort(glassnet* net, const uint8_t* tcount, long P, cudaStream_t st) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  if (!s->sort_st) {
+    if (cudaStreamCreateWithFlags(&s->sort_st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_fwd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_sorted, cudaEventDisableTiming) != cudaSuccess)
+      return gn_fail(GLASSNET_ERR_CUDA, "sort stream / events");
+  }
+  const long nsb = (P + TB_SBP - 1) / TB_SBP;
+  if (nsb * TB_SBP > s->perm_cap) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "T kernel: %ld pixels exceed the workspace", P);
+  cudaEventRecord(s->ev_fwd, st);               // after the previous forward's T kernel read perm
+  cudaStreamWaitEvent(s->sort_st, s->ev_fwd, 0);
+  switch (net->d.k_slots) {
+#define KCASE(k) case k: k_tb_sort<k><<<(unsigned)nsb, 256, 0, s->sort_st>>>(tcount, s->perm, P); break;
+#ifdef GN_DIAG_K8_ONLY
+    KCASE(8)
+#else
+    KCASE(1) KCASE(2) KCASE(3) KCASE(4) KCASE(5) KCASE(6) KCASE(7) KCASE(8)
+    KCASE(9) KCASE(10) KCASE(11) KCASE(12) KCASE(13) KCASE(14) KCASE(15) KCASE(16)
+#endif
+#undef KCASE
+    default: return gn_fail(GLASSNET_ERR_UNSUPPORTED, "k_slots");
+  }
+  cudaEventRecord(s->ev_sorted, s->sort_st);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "count sort launch: %s", cudaGetErrorString(e));
+  return 0;
 }
 
 inline int tc_launch_tb(glassnet* net, const __nv_bfloat16* tbuf, const uint8_t* tcount, const __nv_bfloat16* e0,
