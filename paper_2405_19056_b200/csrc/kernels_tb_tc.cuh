@@ -70,7 +70,7 @@ constexpr float TB_QSCALE = 4096.0f;            // pool fixed point: 2^12 per un
 constexpr float TB_QMAGIC = 8388608.0f;         // 2^23
 constexpr float TB_QMAX = 16777215.0f;          // 2^24 - 1 (saturation at 2048 - 2^-12)
 constexpr uint32_t TB_QBITS = 0x4B000000u;      // bits of 2^23
-constexpr int TB_SBT = 16;                      // tiles per superblock (the count sort's window)
+constexpr int TB_SBT = 32;                      // tiles per superblock (the count sort's window)
 constexpr int TB_SBP = TB_SBT * 128;
 
 // Small per-network constants, passed by value so the epilogues read them from the
@@ -84,19 +84,20 @@ struct TbParams {
 
 // ---------------------------------------------------------------------------------------
 // Pre-pass: per superblock of TB_SBP pixels, a counting sort by min(n, K) (absent pixels,
-// beyond P, last).  perm[sb*SBP + i] = (pixel offset in the superblock) | (count << 11).
-// 256 threads x 8 consecutive pixels (one 8-byte load); the per-thread bin counts are packed
+// beyond P, last).  perm[sb*SBP + i] = (pixel offset in the superblock) | (count << 16).
+// TB_SBP/8 threads x 8 consecutive pixels (one 8-byte load); the per-thread bin counts are packed
 // two 16-bit fields per word and prefix-summed across the block in one pass; the sorted
 // superblock is staged in shared memory and written with 16-byte stores.  The order inside
 // a bin is deterministic but irrelevant (every MMA row is independent).
 template <int K>
-__global__ void __launch_bounds__(256) k_tb_sort(const uint8_t* __restrict__ tcount, uint16_t* __restrict__ perm,
-                                                 long P) {
-  static_assert(TB_SBP == 2048, "256 threads x 8 pixels");
+__global__ void __launch_bounds__(TB_SBP / 8) k_tb_sort(const uint8_t* __restrict__ tcount, uint32_t* __restrict__ perm,
+                                                        long P) {
+  constexpr int NT = TB_SBP / 8, NW = NT / 32;   // threads x 8 pixels; per-bin totals <= TB_SBP < 2^16
+  static_assert(NT % 32 == 0 && TB_SBP < 65536, "sort block");
   constexpr int NB = K + 2, NV = (NB + 1) / 2;
-  __shared__ uint32_t wtot[8][NV];
-  __shared__ uint16_t soff[256][NB + 1];
-  __shared__ __align__(16) uint16_t sperm[TB_SBP];
+  __shared__ uint32_t wtot[NW][NV];
+  __shared__ uint16_t soff[NT][NB + 1];
+  __shared__ __align__(16) uint32_t sperm[TB_SBP];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const long q0 = (long)blockIdx.x * TB_SBP + 8 * t;
   int bin[8];
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(256) k_tb_sort(const uint8_t* __restrict__ tco
   for (int i = 0; i < NV; ++i) {
     uint32_t pre = 0, all = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const uint32_t x = wtot[w][i];
       pre += w < warp ? x : 0u;
       all += x;
@@ -152,10 +153,12 @@ __global__ void __launch_bounds__(256) k_tb_sort(const uint8_t* __restrict__ tco
     int r = 0;
 #pragma unroll
     for (int i = 0; i < j; ++i) r += bin[i] == bin[j] ? 1 : 0;
-    sperm[soff[t][bin[j]] + r] = (uint16_t)((8 * t + j) | (bin[j] << 11));
+    sperm[soff[t][bin[j]] + r] = (uint32_t)(8 * t + j) | ((uint32_t)bin[j] << 16);
   }
   __syncthreads();
-  reinterpret_cast<uint4*>(perm + (long)blockIdx.x * TB_SBP)[t] = reinterpret_cast<const uint4*>(sperm)[t];
+  uint4* dst = reinterpret_cast<uint4*>(perm + (long)blockIdx.x * TB_SBP);
+  dst[2 * t] = reinterpret_cast<const uint4*>(sperm)[2 * t];
+  dst[2 * t + 1] = reinterpret_cast<const uint4*>(sperm)[2 * t + 1];
 }
 
 template <int K, int H, int C0>
@@ -211,7 +214,7 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 template <int K, int H, int C0, int POOL>
 __global__ void __launch_bounds__(TbLayout<K, H, C0>::THREADS, 1)
 k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, const uint16_t* __restrict__ direct,
-        const uint8_t* __restrict__ wimg, const __grid_constant__ TbParams prm, const uint16_t* __restrict__ perm,
+        const uint8_t* __restrict__ wimg, const __grid_constant__ TbParams prm, const uint32_t* __restrict__ perm,
         float* __restrict__ psi, long P, int* __restrict__ sched) {
   using S = TbLayout<K, H, C0>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -459,9 +462,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     uint32_t d1ph = 0, dfph = 0;
     auto decode = [&](long tl, int pe, long& pp, int& mm, bool& ok) {   // this thread's pixel of tile tl
-      pp = tl / TB_SBT * TB_SBP + (pe & 2047);
+      pp = tl / TB_SBT * TB_SBP + (pe & 0xFFFF);
       ok = tl < ntiles && pp < P;
-      mm = ok ? (pe >> 11) : 0;
+      mm = ok ? (pe >> 16) : 0;
     };
     // copy row r's e0 of a tile into operand buffer `buf` (its records: fill_rec, by E2)
     auto fill_e0 = [&](int buf, long pp, bool ok) {

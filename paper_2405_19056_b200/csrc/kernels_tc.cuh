@@ -58,7 +58,7 @@ struct TcState {
   Geom full;                    // the handle's own workspace
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
   int* sched = nullptr;         // T kernel's dynamic tile counter
-  uint16_t* perm = nullptr;     // T kernel's count-sorted pixel order (k_tb_sort), one entry per pixel
+  uint32_t* perm = nullptr;     // T kernel's count-sorted pixel order (k_tb_sort), one entry per pixel
   long perm_cap = 0;
   int tile_nranks = 0, tile_rank = -1;
 };
@@ -167,7 +167,7 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   for (int j = 0; j < 3; ++j) prm.bO[j] = Ob[j];
   s->perm_cap = ((long)d.max_batch * d.height * d.width + TB_SBP - 1) / TB_SBP * TB_SBP;
   if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess || cudaMalloc(&s->sched, sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&s->perm, s->perm_cap * sizeof(uint16_t)) != cudaSuccess)
+      cudaMalloc(&s->perm, s->perm_cap * sizeof(uint32_t)) != cudaSuccess)
     return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "tc weight alloc");
   cudaMemcpy(s->tb_wimg, img.data(), img.size(), cudaMemcpyHostToDevice);
   net->w_bytes += img.size() + sizeof(TbParams);
@@ -524,7 +524,7 @@ inline int tc_launch_sort(glassnet* net, const uint8_t* tcount, long P, cudaStre
   cudaEventRecord(s->ev_fwd, st);               // after the previous forward's T kernel read perm
   cudaStreamWaitEvent(s->sort_st, s->ev_fwd, 0);
   switch (net->d.k_slots) {
-#define KCASE(k) case k: k_tb_sort<k><<<(unsigned)nsb, 256, 0, s->sort_st>>>(tcount, s->perm, P); break;
+#define KCASE(k) case k: k_tb_sort<k><<<(unsigned)nsb, TB_SBP / 8, 0, s->sort_st>>>(tcount, s->perm, P); break;
 #ifdef GN_DIAG_K8_ONLY
     KCASE(8)
 #else
