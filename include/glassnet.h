@@ -126,6 +126,13 @@ int glassnet_profile_begin(glassnet_t net, int32_t max_launches);
 int glassnet_profile_end(glassnet_t net, int32_t max_stages, char* names, double* total_ms,
                          int32_t* launches, int32_t* n_stages);
 
+/* Test / diagnostic: copy (device to device, on `stream`) the psi intermediate of the last
+ * glassnet_forward -- psi = W_O,d0 phi + W_O,L L_d + b_O, [batch][H][W][3] fp32 (reading
+ * R15), the only place the transparency latent tau reaches memory -- into the caller's
+ * device buffer `dst`.  Bitwise checks of T (slot permutation invariance, Eq.
+ * eq:SymmetricNN P:303-318, table:OrderLoss P:666-679) compare it across forwards. */
+int glassnet_debug_psi(glassnet_t net, float* dst, int32_t batch, glassnet_stream_t stream);
+
 /* ---- row-tile sharding (one process per GPU, NCCL point-to-point halos) ---- */
 
 /* ncclGetUniqueId into id[128] (rank 0 calls it and broadcasts the bytes). */

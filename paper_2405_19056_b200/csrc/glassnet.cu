@@ -564,6 +564,16 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
   return GLASSNET_OK;
 }
 
+extern "C" int glassnet_debug_psi(glassnet_t net, float* dst, int32_t batch, glassnet_stream_t stream) {
+  if (!net || !dst) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net or dst is NULL");
+  if (batch < 1 || batch > net->d.max_batch)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "batch=%d outside [1, max_batch=%d]", batch, net->d.max_batch);
+  CUDA_TRY(cudaSetDevice(net->dev));
+  CUDA_TRY(cudaMemcpyAsync(dst, net->psi, (size_t)batch * net->d.height * net->d.width * 3 * sizeof(float),
+                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return GLASSNET_OK;
+}
+
 // ------------------------------------------------------------------------ profiling
 extern "C" int glassnet_profile_begin(glassnet_t net, int32_t max_launches) {
   if (!net || max_launches < 2) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "bad profile_begin args");
@@ -644,14 +654,3 @@ extern "C" int glassnet_debug_watchdog(unsigned int* out8, int init) {
 }
 #endif
 
-#ifdef GN_PROFILE_TB
-extern "C" int glassnet_debug_tb_prof(unsigned long long* out32, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out32, gn::gn_tb_prof, 32 * sizeof(unsigned long long));
-  if (reset) {
-    unsigned long long z[32] = {};
-    cudaMemcpyToSymbol(gn::gn_tb_prof, z, sizeof z);
-  }
-  return 0;
-}
-#endif

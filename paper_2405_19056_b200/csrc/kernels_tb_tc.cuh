@@ -3,42 +3,40 @@
 // PAPER.md Eq. eq:SymmetricNN: tau = sum_i h(b_i), h shared; B;
 // the psi projection is reading R15.
 //
-// Work unit: a tile of 128 pixels.  Pixels are grouped in superblocks of TB_SBT tiles and a
-// pre-pass (k_tb_sort) orders each superblock's pixels by their valid count n, so a tile
-// runs only as many slot rounds as its own largest count.  Per-pixel results do not depend
-// on the row a pixel lands in (every MMA row is an independent dot product), so the
-// ordering is a pure schedule.
+// Work unit: a tile of 128 pixels (MMA row / TMEM lane r = pixel r).  Pixels are grouped in
+// superblocks of TB_SBT tiles and a pre-pass (k_tb_sort) orders each superblock's pixels by
+// their valid count n, so a tile runs only as many slot "items" as its largest count.
 //
-// Operands.  A tile row's K records (K*22 contiguous bytes) are copied by cp.async, with
-// zero fill beyond the n valid records, straight into the layer-1 operand as 16-byte K-planes
-// (plane i = bytes 16i..16i+15 of every row): record k is the K-window of halfwords
-// [11k, 11k+11) and its layer-1 MMA reads planes j = floor(11k/8).. with a copy of W1
-// placed at column offset 11k - 8j (8 offset copies; two MMAs when the window crosses a
-// third plane).  Masked slots therefore never reach shared memory (reading R4: they may
-// hold any bits, NaN/Inf included) and the window's neighbouring columns are zeros or
-// finite valid records times zero weights.  The biases enter the accumulators through one
-// more MMA per layer (ONES x bias block; for layer 2 also the pool's magic 2^23); A2 is
-// written to TMEM (tcgen05.st) and layer 2 reads its A operand from TMEM.
+// Slot independence BY CONSTRUCTION (reading R5).  Every record is repacked into its own
+// K=16 window: slot s of a row = K-columns [16s, 16s+16) = [11 features, 1, 1, 1, 0, 0], and
+// W1's window = [W1 (depth column x 2^-7), b1 as three exact bf16 pieces, 0, 0].  So layer 1
+// of EVERY slot is the same single MMA instruction shape over a window at the same column
+// offsets (the bias summed inside it), layer 2 the same four TMEM-A MMAs, and the pool an
+// exact integer sum: a fragment's contribution does not depend on the slot it arrived in
+// (measured in tools/ubench_t2.cu: one K=16 MMA sums its products position-independently;
+// round 1's split windows did not).  Masked slots (k >= n) are zero windows written by the
+// loader, so their bits (NaN/Inf allowed, reading R4) never reach shared memory.
 //
-// Warp specialisation.  A CTA runs NCH independent "chains"; a chain has three roles, all
-// indexed by tile row r = TMEM lane r:
-//   E1 (4 warps)  per tile: publish the rows' counts; issue the cp.asyncs of the NEXT
-//                 tile's records and e0 (double-buffered operands; completion tracked by
-//                 the `loaded` mbarrier, so E1 never waits for global memory);
-//                 round t: A2 = ReLU(acc1 + b1) -> bf16 -> TMEM
-//                                                    -> MMA: acc2[t&1] = A2 W2^T, acc1 = layer 1 of slot t+1
-//                 final: phi = ReLU(accB + b_B + w_Bn n), psi = W_O,d0 phi + W_O,L L_d + b_O -> HBM
-//   E2 (4 warps)  pool += Q(acc2[s&1] + b2) for every slot s as its batch completes (acc2
-//                 is double-buffered, so this runs beside E1's next slot); then
-//                 tau = pool (f16)                   -> MMA: accB = e0 W_B,e0^T + tau W_B,tau^T
-//   MMA (1 warp)  one thread issues every tcgen05.mma of the chain, and executes the
-//                 generic -> async proxy fence for the operands the others wrote.
-// Hand-offs are mbarriers: loaded[b] (cp.async completion of operand buffer b), rdyC (E1 ->
-// MMA: counts published), rdyA (E1 -> MMA: A2 written), tstart (E1 -> E2), free2[b] (E2 -> MMA: acc2
-// buffer b read), rdyF (E2 -> MMA: tau written), done1 (commit -> E1, batches holding a
-// layer-1 MMA), done2[b] (commit -> E2, layer-2 batches into buffer b) and doneF (commit ->
-// E1, the accB batch).  Each waiter can be at most one
-// phase behind its barrier by construction.
+// Pool (R5): a2 = ReLU(W2 a1 + b2) enters as Q = round(a2 * 2^12) via
+//   v = sat(acc2 + b2 2^-11)        (W2 pre-scaled by 2^-11: one FFMA.SAT = bias, ReLU and the
+//                                    saturation at a2 = 2048)
+//   pool += bits(1 + v) - bits(1)   (v + 1 has ulp 2^-23, i.e. 2^-12 in a2 units)
+// -- integer adds, so any order of the valid slots gives the same bits.
+//
+// Warp roles (one CTA per SM, 17 warps):
+//   w0       MMA: one thread issues every tcgen05.mma / commit
+//   w1..w4   loader: claims tiles, reads the count-sorted perm, the valid records (16-byte
+//            loads of the valid prefix only), e0 and L_d; repacks the records into the K=16
+//            slot windows (A1, 2 buffers), e0 into its operand (E0, 3 buffers), per-tile meta
+//   w5..w8   E1: A2 = bf16(ReLU(acc1)) written back INTO acc1's first H/2 columns (layer 2
+//            reads its A operand from TMEM); per tile, one tile late: phi, psi -> HBM
+//   w9..w16  E2: two warps per TMEM lane quadrant, H/2 channels each: the fixed-point pool;
+//            per tile tau -> f16 -> TMEM (the B MMA's A operand)
+// Software pipeline: acc1 and acc2 are 2-deep rings, so layer 1 of item i+1 and E1 of item
+// i+1 overlap layer 2 of item i, and E2 of item i overlaps both.  B of tile t (e0 part + tau
+// part) is issued after layer 2 of tile t+1's item min(1, Kt-1), E1's phi/psi of tile t right
+// after that item's epilogue (the pool of tile t has then had a full item to finish).
+// Hand-offs are mbarriers; each waiter is provably at most one phase behind.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -48,28 +46,9 @@
 
 namespace gn {
 
-#ifdef GN_PROFILE_TB
-// clock64 breakdown of chain 0 of CTA 0 (diagnostic build only): counters 0-15 are kept by
-// E1's thread 0 (16-31 are reserved for the other roles); accumulated in shared memory (a
-// global read-modify-write would itself stall the chain) and flushed at exit
-__device__ unsigned long long gn_tb_prof[32];
-__shared__ unsigned long long gn_tb_sprof[32];
-#define TBP_NOW(v) const long long v = clock64()
-#define TBP_ADD(i, a, b) \
-  if (threadIdx.x == 0) gn_tb_sprof[i] += (unsigned long long)((b) - (a))
-#define TBP_INIT() if (threadIdx.x < 32) gn_tb_sprof[threadIdx.x] = 0
-#define TBP_FLUSH() if (blockIdx.x == 0 && threadIdx.x < 32) gn_tb_prof[threadIdx.x] += gn_tb_sprof[threadIdx.x]
-#else
-#define TBP_INIT()
-#define TBP_FLUSH()
-#define TBP_NOW(v)
-#define TBP_ADD(i, a, b)
-#endif
-
-constexpr float TB_QSCALE = 4096.0f;            // pool fixed point: 2^12 per unit
-constexpr float TB_QMAGIC = 8388608.0f;         // 2^23
-constexpr float TB_QMAX = 16777215.0f;          // 2^24 - 1 (saturation at 2048 - 2^-12)
-constexpr uint32_t TB_QBITS = 0x4B000000u;      // bits of 2^23
+constexpr uint32_t TB_ONE_BITS = 0x3F800000u;   // bits of 1.0f (the pool's per-fragment offset)
+constexpr float TB_VSCALE = 1.0f / 2048.0f;     // a2 -> v = a2 2^-11 (saturation at a2 = 2048)
+constexpr float TB_QUNIT = 1.0f / 4096.0f;      // one pool unit = 2^-12
 constexpr int TB_SBT = 32;                      // tiles per superblock (the count sort's window)
 constexpr int TB_SBP = TB_SBT * 128;
 
@@ -80,6 +59,7 @@ struct TbParams {
   float wBn[32];         // B weight of the count channel n
   float WO[3 * 35];      // [3][C0+3]: output 1x1 over [d0 ; L_d] (L_d part zero if R does not take it)
   float bO[4];
+  float b2s[64];         // b2 2^-11 (the pool's FFMA.SAT addend)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -161,55 +141,96 @@ __global__ void __launch_bounds__(TB_SBP / 8) k_tb_sort(const uint8_t* __restric
   dst[2 * t + 1] = reinterpret_cast<const uint4*>(sperm)[2 * t + 1];
 }
 
+// ---------------------------------------------------------------------------------------
 template <int K, int H, int C0>
 struct TbLayout {
   static constexpr int PL = 128 * 16;                 // one 8-column K-plane of a 128-row operand
-  static constexpr int REC_B = K * 22;                // bytes of one pixel's records
-  static constexpr bool ASYNC = REC_B % 16 == 0;      // records copied by 16-byte cp.async
-  static constexpr int NPL = (REC_B + 15) / 16;       // record planes per row
-  static constexpr int A1_PL = NPL + 2;               // + 2 zero planes (a window may reach past the last record)
-  static constexpr int W1_B = 8 * 4 * H * 16;         // 8 offset copies x 4 planes x H rows
+  static constexpr int A1_B = K * 2 * PL;             // a tile's layer-1 operand: slot s = planes 2s, 2s+1
+  static constexpr int E0_B = (C0 / 8) * PL;          // a tile's e0 operand
+  static constexpr int W1_B = 2 * H * 16;             // [2 planes][H][8]: W1 | b1 pieces | 0
   static constexpr int W2_B = H * H * 2;
-  static constexpr int WBT_B = C0 * H * 2;
   static constexpr int WBE_B = C0 * C0 * 2;
-  static constexpr int ONES_B = 128 * 16 * 2;         // bias MMAs: A = ONES (columns 0..3 = 1)
-  static constexpr int BB_B = H * 16 * 2;              //            B = [b1 pieces] / [2^23, b2 2^12 pieces]
-  static constexpr int WIMG_B = W1_B + W2_B + WBT_B + WBE_B + ONES_B + 2 * BB_B;
-  static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBT = OFF_W2 + W2_B, OFF_WBE = OFF_WBT + WBT_B;
-  static constexpr int OFF_ONES = OFF_WBE + WBE_B, OFF_BB1 = OFF_ONES + ONES_B, OFF_BB2 = OFF_BB1 + BB_B;
-  static constexpr int OFF_BAR = (WIMG_B + 15) / 16 * 16;   // per chain 12 mbarrier slots; then the tmem ptr
-  static constexpr int OFF_RED = OFF_BAR + 4 * 96 + 16;     // per chain 8 ints: warp max counts, Kt, tile ids
-  static constexpr int OFF_CH = (OFF_RED + 4 * 32 + 127) / 128 * 128;
-  // one chain: the layer-1 operand is double-buffered (the next tile's records copied during
-  // this tile) unless that leaves room for only one chain, where two single-buffered chains
-  // fit instead (K = 16: 352-byte records); single-buffered, E2 copies the next tile's records
-  // right after this tile's last layer-2 batch, overlapping the tile's tail
-  static constexpr int CH_REST = 2 * (C0 / 8) * PL + (H / 8) * PL + 128 + 128 * 8 + 144;
-  static constexpr int AVAIL = 232448 - 1024 - OFF_CH;
-  static constexpr int A1_NB = (AVAIL / (2 * A1_PL * PL + CH_REST) >= 2 || AVAIL / (A1_PL * PL + CH_REST) < 2) ? 2 : 1;
-  static constexpr int CH_A1 = 0;                     // A1_NB buffers x A1_PL planes
-  static constexpr int CH_E0 = CH_A1 + A1_NB * A1_PL * PL;      // 2 buffers x C0/8 planes
-  static constexpr int CH_TAU = CH_E0 + 2 * (C0 / 8) * PL;      // H/8 planes (f16)
-  static constexpr int CH_MROW = CH_TAU + (H / 8) * PL;         // 128 x u8: the rows' valid counts
-  static constexpr int CH_NPIX = CH_MROW + 128;                 // 128 x i64: the NEXT tile's pixels (-1: none)
-  static constexpr int CH_NCNT = CH_NPIX + 128 * 8;             // 128 x u8 its counts; [128] = a next tile exists
-  static constexpr int CH_B = CH_NCNT + 144;
-  static constexpr int TCOLS = (3 * H + C0 + H / 2 + 31) / 32 * 32;   // acc1, acc2 x2, accB, A2 (packed)
-  static constexpr int NCH_T = 512 / TCOLS;
-  static constexpr int NCH_S = (232448 - 1024 - OFF_CH) / CH_B;
-  static constexpr int NCH = NCH_T < NCH_S ? (NCH_T < 3 ? NCH_T : 3) : (NCH_S < 3 ? NCH_S : 3);
-  static constexpr int SMEM = OFF_CH + NCH * CH_B;
-  static constexpr int THREADS = NCH * 288;           // warps: E1 (4/chain), E2 (4/chain), MMA (1/chain)
+  static constexpr int WBT_B = C0 * H * 2;            // f16
+  static constexpr int WIMG_B = W1_B + W2_B + WBE_B + WBT_B;
+  static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBE = OFF_W2 + W2_B, OFF_WBT = OFF_WBE + WBE_B;
+  static constexpr int NA = 2, NE = 3;                // A1 ring, E0 / meta ring
+  static constexpr int OFF_A1 = (WIMG_B + 1023) / 1024 * 1024;
+  static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
+  // per-tile meta: pixel ids, counts, L_d (E1's psi needs them one tile late), Kt, tile id
+  static constexpr int M_PIX = 0, M_LD = 128 * 8, M_CNT = M_LD + 128 * 12, M_KT = M_CNT + 128, META_B = M_KT + 16;
+  static constexpr int OFF_META = OFF_E0 + NE * E0_B;
+  static constexpr int NBAR = 24;
+  static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
+  static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch
+  static constexpr int SMEM = OFF_MISC + 64;
+  static constexpr int NWARP = 17, THREADS = 32 * NWARP;
+  static constexpr int T_ACC1 = 0, T_ACC2 = 2 * H, T_ACCB = 4 * H, T_TAU = 4 * H + 2 * C0;   // TMEM columns
+  static_assert(T_TAU + H <= 512, "TMEM");
+  static_assert(SMEM <= 232448 - 1024, "shared memory");
 };
 
-// 16-byte cp.async with zero fill: copies `bytes` (0..16) from src, zeros the rest
-__device__ __forceinline__ void cp_async16z(uint32_t dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+// layer-1 window repack of one record (8 words) from the row's words W starting at halfword 11s
+template <int S>
+__device__ __forceinline__ void tb_window(const uint32_t* W, bool valid, uint32_t (&o)[8]) {
+  constexpr uint32_t ONE = 0x3F80u;   // bf16 1.0
+  if ((S & 1) == 0) {
+    constexpr int a = 11 * S / 2;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o[k] = W[a + k];
+    o[5] = (W[a + 5] & 0xFFFFu) | (ONE << 16);
+  } else {
+    constexpr int a = (11 * S - 1) / 2;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o[k] = __byte_perm(W[a + k], W[a + k + 1], 0x5432);
+    o[5] = (W[a + 5] >> 16) | (ONE << 16);
+  }
+  o[6] = ONE | (ONE << 16);
+  o[7] = 0;
+  if (!valid)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = 0;
 }
-// arrive on `bar` when all of this thread's prior cp.asyncs have completed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+
+template <int S, int NS>
+struct TbWindows {   // slots S..S+NS-1 of a pass whose words start at the pass's first record
+  __device__ __forceinline__ static void run(const uint32_t* W, int m_rel, uint32_t a1, int slot0, int r) {
+    if constexpr (NS > 0) {
+      uint32_t o[8];
+      tb_window<S>(W, S < m_rel, o);
+      const uint32_t dst = a1 + (uint32_t)(2 * (slot0 + S)) * (128 * 16) + r * 16;
+      tc::sts128(dst, o[0], o[1], o[2], o[3]);
+      tc::sts128(dst + 128 * 16, o[4], o[5], o[6], o[7]);
+      TbWindows<S + 1, NS - 1>::run(W, m_rel, a1, slot0, r);
+    }
+  }
+};
+
+__device__ __forceinline__ uint32_t tb_ld_nc(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
 }
+__device__ __forceinline__ uint4 tb_ld_nc4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ffma_sat(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// mbarrier phase bits of a small ring, kept in one register (runtime indices would put an
+// array in local memory)
+template <int V> struct TbInt { static constexpr int value = V; };
+
+struct TbPh {
+  uint32_t v = 0;
+  __device__ __forceinline__ uint32_t operator[](int i) const { return (v >> i) & 1u; }
+  __device__ __forceinline__ void flip(int i) { v ^= 1u << i; }
+};
 
 template <int K, int H, int C0, int POOL>
 __global__ void __launch_bounds__(TbLayout<K, H, C0>::THREADS, 1)
@@ -217,382 +238,370 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         const uint8_t* __restrict__ wimg, const __grid_constant__ TbParams prm, const uint32_t* __restrict__ perm,
         float* __restrict__ psi, long P, int* __restrict__ sched) {
   using S = TbLayout<K, H, C0>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int NCH = S::NCH;
+  extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t PL = S::PL;
   constexpr int NO = C0 + 3;
-  static_assert(C0 <= 32 && H <= 64 && H % 32 == 0, "TbParams sizes / epilogue chunks");
-  const int wg = threadIdx.x >> 5;
-  const int role = wg < 4 * NCH ? 0 : wg < 8 * NCH ? 1 : 2;   // E1, E2, MMA
-  const int g = role == 2 ? wg - 8 * NCH : (wg >> 2) % NCH;    // chain
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * g;
-  uint64_t* loaded = bars + 0;     // [2]
-  uint64_t* rdyA = bars + 2;
-  uint64_t* rdyF = bars + 3;
-  uint64_t* free2 = bars + 4;      // [2]
-  uint64_t* done1 = bars + 6;
-  uint64_t* done2 = bars + 7;      // [2]
-  uint64_t* tstart = bars + 9;
-  uint64_t* doneF = bars + 10;
-  uint64_t* rdyC = bars + 11;      // E1 -> MMA: a tile's counts published (separate from rdyA: E1's
-                                   // round 0 may follow at once when layer 1 was issued early)
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_BAR + 4 * 96);
-  volatile int* red = reinterpret_cast<int*>(smem + S::OFF_RED) + 8 * g;   // [0..3] warp max, [4] Kt, [5..7] tile ids
+  constexpr int LAG = 1;   // B / psi of tile t follow item min(LAG, Kt-1) of tile t+1
+  static_assert(C0 <= 32 && (H == 32 || H == 64), "TbParams sizes / epilogue chunks");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
+  uint64_t* tileReady = bars + 0;   // [3] loader -> all (4 warp arrivals)
+  uint64_t* metaFree = bars + 3;    // [3] MMA commit (B) + E1 (4) + E2 (8) -> loader
+  uint64_t* a1Free = bars + 6;      // [2] MMA commit after the tile's last layer-1 MMA -> loader
+  uint64_t* done1 = bars + 8;       // [2] commit -> E1 (acc1 ring)
+  uint64_t* rdyA = bars + 10;       // [2] E1 (4) -> MMA: A2 in acc1
+  uint64_t* done2 = bars + 12;      // [2] commit -> E2 (acc2 ring)
+  uint64_t* free2 = bars + 14;      // [2] E2 (8) -> MMA: acc2 read
+  uint64_t* tauRdy = bars + 16;     // [2] E2 (8) -> MMA: tau of the tile in TMEM
+  uint64_t* doneB = bars + 18;      // [2] commit -> E1 (psi) and E2 (tau buffer reuse)
+  uint64_t* accBfree = bars + 20;   // [2] E1 (4) -> MMA: accB read
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_MISC);
+  volatile int* lred = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 16);   // [2][4] warp max counts
+  volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 48);    // [4] claimed tile ids
+  auto meta = [&](int e) -> uint8_t* { return smem + S::OFF_META + e * S::META_B; };
 
-  TBP_INIT();
   for (int i = threadIdx.x; i < S::WIMG_B / 16; i += blockDim.x)
     reinterpret_cast<int4*>(smem)[i] = reinterpret_cast<const int4*>(wimg)[i];
-  for (int c = 0; c < NCH; ++c)   // the zero pad planes of the A1 buffers
-    for (int i = threadIdx.x; i < S::A1_NB * 2 * (int)PL / 16; i += blockDim.x) {
-      const int b = i / (2 * PL / 16), o = i % (2 * PL / 16);
-      reinterpret_cast<int4*>(smem + S::OFF_CH + c * S::CH_B + S::CH_A1 + (b * S::A1_PL + S::NPL) * PL)[o] =
-          make_int4(0, 0, 0, 0);
-    }
   if (threadIdx.x == 0) {
-    for (int c = 0; c < NCH; ++c) {
-      uint64_t* b = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR) + 12 * c;
-      tc::mbar_init(b + 0, 256); tc::mbar_init(b + 1, 256);   // loaded[2]: E2 (records) + E1 (e0)
-      tc::mbar_init(b + 2, 128); tc::mbar_init(b + 3, 128);   // rdyA, rdyF
-      tc::mbar_init(b + 4, 128); tc::mbar_init(b + 5, 128);   // free2[2]
-      tc::mbar_init(b + 6, 1); tc::mbar_init(b + 7, 1); tc::mbar_init(b + 8, 1);   // done1, done2[2]
-      tc::mbar_init(b + 9, 128);                              // tstart
-      tc::mbar_init(b + 10, 1);                               // doneF
-      tc::mbar_init(b + 11, 128);                             // rdyC
+    for (int i = 0; i < 3; ++i) { tc::mbar_init(tileReady + i, 4); tc::mbar_init(metaFree + i, 13); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(a1Free + i, 1); tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 4);
+      tc::mbar_init(done2 + i, 1); tc::mbar_init(free2 + i, 8); tc::mbar_init(tauRdy + i, 8);
+      tc::mbar_init(doneB + i, 1); tc::mbar_init(accBfree + i, 4);
     }
     tc::fence_mbar_init();
   }
-  if (threadIdx.x < 32) tc::tmem_alloc<512>(tptr);
+  if (warp == 0) tc::tmem_alloc<512>(tptr);
   tc::fence_proxy_async();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tmem = *tptr + g * S::TCOLS;
-  const uint32_t t_acc1 = tmem, t_acc2 = tmem + H, t_accB = tmem + 3 * H, t_a2 = tmem + 3 * H + C0;
-  uint8_t* chs = smem + S::OFF_CH + g * S::CH_B;
-  volatile uint8_t* mrow = chs + S::CH_MROW;
-  volatile long long* nprow = reinterpret_cast<volatile long long*>(chs + S::CH_NPIX);
-  volatile uint8_t* ncnt = chs + S::CH_NCNT;
-  const uint32_t sA1 = tc::smem_u32(chs + S::CH_A1), sE0 = tc::smem_u32(chs + S::CH_E0);
-  const uint32_t sTAU = tc::smem_u32(chs + S::CH_TAU);
-  // copy row r's records of a tile (pixel pp, mm valid records) into operand buffer `buf`, zero
-  // fill beyond the valid bytes (E2 issues these for the next tile; E1 for the first)
-  auto fill_rec = [&](int r, int buf, long pp, int mm, bool ok) {
-    const uint32_t a = sA1 + buf * S::A1_PL * PL + r * 16;
-    const int vb = ok ? mm * 22 : 0;            // valid bytes of the row
-    if (S::ASYNC) {
-      const char* src = ok ? reinterpret_cast<const char*>(tbuf + pp * (K * 11)) : reinterpret_cast<const char*>(tbuf);
-#pragma unroll
-      for (int i = 0; i < S::NPL; ++i)
-        cp_async16z(a + i * PL, src + 16 * i, (uint32_t)min(max(vb - 16 * i, 0), 16));
-    } else {   // rows not 16-byte aligned in global memory: through registers
-      const uint16_t* src = tbuf + pp * (K * 11);
-#pragma unroll
-      for (int i = 0; i < S::NPL; ++i) {
-        uint32_t w[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int e = 8 * i + 2 * h;
-          const uint32_t lo = 2 * e < vb ? __ldg(src + e) : 0u, hi = 2 * e + 2 < vb ? __ldg(src + e + 1) : 0u;
-          w[h] = lo | (hi << 16);
-        }
-        tc::sts128(a + i * PL, w[0], w[1], w[2], w[3]);
-      }
-    }
-  };
+  const uint32_t tmem = *tptr;
   const long ntiles = (P + TB_SBP - 1) / TB_SBP * TB_SBT;
 
-  if (role == 2) {
-    // ------------------------------------------------------------------ MMA warp of chain g
-    if ((threadIdx.x & 31) == 0) {
+  if (warp == 0) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
       const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
-      const uint32_t sWBT = tc::smem_u32(smem + S::OFF_WBT), sWBE = tc::smem_u32(smem + S::OFF_WBE);
+      const uint32_t sWBE = tc::smem_u32(smem + S::OFF_WBE), sWBT = tc::smem_u32(smem + S::OFF_WBT);
+      const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
       constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
       constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
       constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
-      // layer 1 of slot k from operand buffer `buf`: the record's K-window starts in plane
-      // j = 11k/8 at column offset o = 11k mod 8 (W1 copy o); a third plane needs a 2nd MMA
-      const uint64_t dONES = tc::smem_desc(tc::smem_u32(smem + S::OFF_ONES), PL, 128);
-      const uint64_t dBB1 = tc::smem_desc(tc::smem_u32(smem + S::OFF_BB1), H * 16, 128);
-      const uint64_t dBB2 = tc::smem_desc(tc::smem_u32(smem + S::OFF_BB2), H * 16, 128);
-      auto layer1 = [&](int k, int buf) {
-        const int j = (11 * k) >> 3, o = (11 * k) & 7;
-        const uint32_t a = sA1 + ((S::A1_NB == 2 ? buf : 0) * S::A1_PL + j) * PL, w = sW1 + o * 4 * H * 16;
-        tc::mma_f16_ss(t_acc1, tc::smem_desc(a, PL, 128), tc::smem_desc(w, H * 16, 128), ID_T, 0);
-        if (o > 5)
-          tc::mma_f16_ss(t_acc1, tc::smem_desc(a + 2 * PL, PL, 128), tc::smem_desc(w + 2 * H * 16, H * 16, 128), ID_T, 1);
-        tc::mma_f16_ss(t_acc1, dONES, dBB1, ID_T, 1);   // + b1
+      const uint64_t dW1 = tc::smem_desc(sW1, H * 16, 128);
+      TbPh trph, aph, f2ph, tph, bfph;
+      int i1 = 0, i2 = 0;
+      auto layer1 = [&](int t, int s) {   // tile t's slot s -> acc1[i1 & 1]
+        const uint32_t a = sA1 + (uint32_t)(t & 1) * S::A1_B + (uint32_t)(2 * s) * PL;
+        tc::mma_f16_ss(tmem + S::T_ACC1 + (i1 & 1) * H, tc::smem_desc(a, PL, 128), dW1, ID_T, 0);
+        tc::mma_commit(done1 + (i1 & 1));
+        ++i1;
       };
-      uint32_t aph = 0, cph = 0, fph = 0, lph[2] = {0, 0}, f2ph[2] = {0, 0};
-      bool have_l1 = false;   // this tile's first layer-1 batch was issued after the previous tile
-      for (int buf = 0;; buf ^= 1) {
-        tc::mbar_wait(rdyC, cph); cph ^= 1;        // the tile's counts
-        const int Kt = red[4];
-        if (Kt < 0) break;
-        const bool next_exists = ncnt[128] != 0;   // written with these counts
-        if (!have_l1) {   // (always issued, also for Kt = 0: E1 consumes one layer-1 commit per tile)
-          tc::mbar_wait(loaded + buf, lph[buf]); lph[buf] ^= 1;   // its records and e0 (cp.async)
-          tc::fence_after_sync();
-          tc::fence_proxy_async();
-          layer1(0, buf);
-          tc::mma_commit(done1);
-        } else {
-          tc::fence_after_sync();
-        }
-        // accB = e0 W_B,e0^T now (E1 read the previous tile's accB before publishing these
-        // counts); the tau part is added after the pool, so the tile's tail holds only it
-        const uint32_t e0b = sE0 + buf * (C0 / 8) * PL;
+      auto blend = [&](int u, int Ku) {   // B of tile u: accB = e0 W_B,e0^T + tau W_B,tau^T
+        const int ab = u & 1, e = u % 3;
+        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);   // E1 read tile u-2's accB
+        tc::mbar_wait(tauRdy + ab, tph[ab]); tph.flip(ab);           // E2 wrote tau(u) (even Ku = 0)
+        tc::fence_after_sync();
+        const uint32_t dB = tmem + S::T_ACCB + ab * C0;
 #pragma unroll
         for (int q = 0; q < C0 / 16; ++q)
-          tc::mma_f16_ss(t_accB, tc::smem_desc(e0b + 2 * q * PL, PL, 128),
+          tc::mma_f16_ss(dB, tc::smem_desc(sE0 + (uint32_t)e * S::E0_B + 2 * q * PL, PL, 128),
                          tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-        for (int t = 0; t < Kt; ++t) {
-          tc::mbar_wait(rdyA, aph); aph ^= 1;      // A2 of slot t in TMEM (acc1 read)
-          if (t >= 2) { tc::mbar_wait(free2 + (t & 1), f2ph[t & 1]); f2ph[t & 1] ^= 1; }   // acc2[t&1] read
-          tc::fence_after_sync();
+        if (Ku > 0)
 #pragma unroll
           for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ts(t_acc2 + (t & 1) * H, t_a2 + q * 8, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T,
-                           q > 0);
-          tc::mma_f16_ss(t_acc2 + (t & 1) * H, dONES, dBB2, ID_T, 1);   // + 2^23 + b2 2^12
-          if (t + 1 < Kt) { layer1(t + 1, buf); tc::mma_commit(done1); }
-          tc::mma_commit(done2 + (t & 1));
-        }
-        if (Kt >= 2) { tc::mbar_wait(free2 + ((Kt - 2) & 1), f2ph[(Kt - 2) & 1]); f2ph[(Kt - 2) & 1] ^= 1; }
-        if (Kt >= 1) { tc::mbar_wait(free2 + ((Kt - 1) & 1), f2ph[(Kt - 1) & 1]); f2ph[(Kt - 1) & 1] ^= 1; }
-        tc::mbar_wait(rdyF, fph); fph ^= 1;        // tau written
-        tc::fence_after_sync();
-        tc::fence_proxy_async();
-        if (Kt > 0) {
-#pragma unroll
-          for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ss(t_accB, tc::smem_desc(sTAU + 2 * q * PL, PL, 128),
+            tc::mma_f16_ts(dB, tmem + S::T_TAU + ab * (H / 2) + 8 * q,
                            tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
-        }
-        tc::mma_commit(doneF);
-        // the next tile's first layer-1 batch now: acc1 is free (E1 read this tile's last slot
-        // before the tail), so E1's round 0 of the next tile does not wait for it.  Only after a
-        // tile with slot rounds: E1's rdyA arrivals then prove it has consumed every earlier
-        // layer-1 commit (after a Kt = 0 tile nothing would stop this commit from landing two
-        // phases ahead of E1's wait -- the parity would alias)
-        have_l1 = next_exists && Kt > 0;
-        if (have_l1) {
-          tc::mbar_wait(loaded + (buf ^ 1), lph[buf ^ 1]); lph[buf ^ 1] ^= 1;
-          tc::fence_after_sync();
-          tc::fence_proxy_async();
-          layer1(0, buf ^ 1);
-          tc::mma_commit(done1);
-        }
-      }
-    }
-  } else if (role == 1) {
-    // ------------------------------------------------------------------ E2: the pool
-    const int r = threadIdx.x & 127, warp = r >> 5;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    uint32_t tph = 0, d2ph[2] = {0, 0};
-    int nbuf = 1;                 // operand buffer of the next tile
-    tc::mbar_arrive(loaded + 0);  // the first tile's records are E1's
-    for (;;) {
-      tc::mbar_wait(tstart, tph); tph ^= 1;
-      const int Kt = red[4];
-      if (Kt < 0) break;
-      const int m = mrow[r];
-      // the next tile's records: double-buffered, now into the other operand buffer (its last
-      // reader, the tile before this one, has completed: E2 saw its last batch); single-
-      // buffered, after this tile's last layer-2 batch (all its layer-1 MMAs have completed)
-      const bool has_next = ncnt[128] != 0;
-      const long np_next = has_next ? (long)nprow[r] : -1;
-      const int nm_next = has_next ? (int)ncnt[r] : 0;
-      auto fill_next = [&]() {
-        if (has_next) {
-          fill_rec(r, S::A1_NB == 2 ? nbuf : 0, np_next, nm_next, np_next >= 0);
-          cp_async_arrive(loaded + nbuf);
-        }
+        tc::mma_commit(doneB + ab);
+        tc::mma_commit(metaFree + e);
       };
-      if (S::A1_NB == 2) fill_next();
-      uint32_t pool[H];
-#pragma unroll
-      for (int j = 0; j < H; ++j) pool[j] = 0;
-#pragma unroll 1
-      for (int s = 0; s < Kt; ++s) {
-        const int b = s & 1;
-        tc::mbar_wait(done2 + b, d2ph[b]); d2ph[b] ^= 1;
-        tc::fence_after_sync();
-        // pool += Q(a2): acc2 = 2^23 + (W2 a1 + b2) 2^12 (scale folded into W2, magic and bias
-        // added by the bias MMA), rounded to an integer in fp32; the clamps are the ReLU and the
-        // saturation, and masked slots clamp to exactly 2^23 (0)
-        const float hi = (s < m) ? TB_QMAX : TB_QMAGIC;
-#pragma unroll
-        for (int c = 0; c < H / 32; ++c) {   // two 16-column loads in flight per wait
-          uint32_t u[32];
-          tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[16]>(u));
-          tc::tmem_ld16(t_acc2 + b * H + lane_off + c * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(u + 16));
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = fminf(fmaxf(__uint_as_float(u[i]), TB_QMAGIC), hi);
-            pool[c * 32 + i] += __float_as_uint(x);
+      auto peek = [&](int t) -> int {   // wait for tile t's operands, return its Kt (-1: end)
+        tc::mbar_wait(tileReady + t % 3, trph[t % 3]); trph.flip(t % 3);
+        return *reinterpret_cast<volatile int*>(meta(t % 3) + S::M_KT);
+      };
+      int t = 0, Kt = peek(0);
+      int pend = -1, pendK = 0;
+      if (Kt > 0) layer1(0, 0);
+      while (Kt >= 0) {
+        int Ktn = 0;
+        for (int s = 0; s < Kt; ++s) {
+          if (s + 1 < Kt) {
+            layer1(t, s + 1);
+          } else {   // last item of tile t: its A1 buffer is free once these MMAs complete
+            tc::mma_commit(a1Free + (t & 1));
+            Ktn = peek(t + 1);
+            if (Ktn > 0) layer1(t + 1, 0);
           }
-        }
-        tc::fence_before_sync();
-        tc::mbar_arrive(free2 + b);
-      }
-      if (S::A1_NB == 1) fill_next();
-      nbuf ^= 1;
-      if (Kt > 0) {   // tau = pool (f16) -> its operand
-        const uint32_t off = (uint32_t)Kt * TB_QBITS;
-        const float sc = (POOL == 1 && m > 0) ? (1.f / TB_QSCALE) / (float)m : 1.f / TB_QSCALE;
+          const int b = i2 & 1;
+          tc::mbar_wait(rdyA + b, aph[b]); aph.flip(b);              // A2 of item i2 in acc1[b]
+          tc::mbar_wait(free2 + b, f2ph[b] ^ 1); f2ph.flip(b);       // E2 read acc2[b] (item i2-2)
+          tc::fence_after_sync();
+          const uint32_t d2 = tmem + S::T_ACC2 + b * H, a2 = tmem + S::T_ACC1 + b * H;
 #pragma unroll
-        for (int q = 0; q < H / 8; ++q) {
-          uint32_t o[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float lo = (float)(pool[8 * q + 2 * i] - off) * sc;
-            const float hv = (float)(pool[8 * q + 2 * i + 1] - off) * sc;
-            o[i] = tc::cvt_relu_f16x2(lo, hv);
-          }
-          tc::sts128(sTAU + q * PL + r * 16, o[0], o[1], o[2], o[3]);
+          for (int q = 0; q < H / 16; ++q)
+            tc::mma_f16_ts(d2, a2 + 8 * q, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
+          tc::mma_commit(done2 + b);
+          ++i2;
+          if (s == min(LAG, Kt - 1) && pend >= 0) { blend(pend, pendK); pend = -1; }
         }
+        if (Kt == 0) {
+          tc::mma_commit(a1Free + (t & 1));
+          if (pend >= 0) { blend(pend, pendK); pend = -1; }
+          Ktn = peek(t + 1);
+          if (Ktn > 0) layer1(t + 1, 0);
+        }
+        pend = t; pendK = Kt;
+        ++t;
+        Kt = Ktn;
       }
-      tc::mbar_arrive(rdyF);   // release; the MMA thread fences the proxies
+      if (pend >= 0) blend(pend, pendK);
     }
-  } else {
-    // ------------------------------------------------------------------ E1: operands, A2, phi, psi
-    const int r = threadIdx.x & 127, warp = r >> 5, lane = r & 31;
-    const int bar_id = 1 + g;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    uint32_t d1ph = 0, dfph = 0;
-    auto decode = [&](long tl, int pe, long& pp, int& mm, bool& ok) {   // this thread's pixel of tile tl
-      pp = tl / TB_SBT * TB_SBP + (pe & 0xFFFF);
-      ok = tl < ntiles && pp < P;
-      mm = ok ? (pe >> 16) : 0;
-    };
-    // copy row r's e0 of a tile into operand buffer `buf` (its records: fill_rec, by E2)
-    auto fill_e0 = [&](int buf, long pp, bool ok) {
-      const uint32_t eb = sE0 + buf * (C0 / 8) * PL + r * 16;
-      const uint16_t* es = ok ? e0 + pp * C0 : e0;
-#pragma unroll
-      for (int j = 0; j < C0 / 8; ++j) cp_async16z(eb + j * PL, es + 8 * j, ok ? 16u : 0u);
-      cp_async_arrive(loaded + buf);
-    };
-
-    // Tile pipeline: tile ids are claimed three ahead (atomics), the perm entry of the tile
-    // after next is loaded one tile ahead, and the next tile's operands are copied during
-    // this one, so no global latency sits on a critical path.
+  } else if (warp <= 4) {
+    // ---------------------------------------------------------------- loader
+    const int r = (warp - 1) * 32 + lane;
+    const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
+    TbPh mfph, afph;
     int claim = 0;
-    if (r == 0) { red[5] = atomicAdd(sched, 1); red[6] = atomicAdd(sched, 1); claim = atomicAdd(sched, 1); }
-    tc::bar_sync(bar_id, 128);
-    long tile = red[5], ntile = red[6];
-    long p, np;
-    int m, nm;
-    bool pv, npv;
-    decode(tile, tile < ntiles ? (int)__ldg(perm + tile * 128 + r) : 0, p, m, pv);
-    if (tile < ntiles) { fill_rec(r, 0, p, m, pv); fill_e0(0, p, pv); }
-    decode(ntile, ntile < ntiles ? (int)__ldg(perm + ntile * 128 + r) : 0, np, nm, npv);
-    for (int it = 0; tile < ntiles; ++it) {
-      TBP_NOW(tp_t0);
-      const int buf = it & 1;
-      // ---- prologue: publish the counts (and the next tile's pixels, whose records E2 copies);
-      // copy the next tile's e0
-      mrow[r] = (uint8_t)m;
-      nprow[r] = npv ? (long long)np : -1ll;
-      ncnt[r] = (uint8_t)nm;
-      if (r == 0) ncnt[128] = ntile < ntiles ? 1 : 0;
-      {
-        const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
-        if (lane == 0) red[warp] = wm;
-        if (r == 0) { red[5 + (it + 2) % 3] = claim; claim = atomicAdd(sched, 1); }
+    if (r == 0) { ids[0] = atomicAdd(sched, 1); ids[1] = atomicAdd(sched, 1); claim = atomicAdd(sched, 1); }
+    tc::bar_sync(1, 128);
+    long tile = ids[0];
+    uint32_t pe = tile < ntiles ? __ldg(perm + tile * 128 + r) : 0u;
+    for (int t = 0;; ++t) {
+      const int e = t % 3, a = t & 1;
+      uint8_t* M = meta(e);
+      if (tile >= ntiles) {
+        tc::mbar_wait(metaFree + e, mfph[e] ^ 1);
+        if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = -1;
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tileReady + e);
+        break;
       }
-      tc::bar_sync(bar_id, 128);
-      const int Kt = max(max(red[0], red[1]), max(red[2], red[3]));
-      const long nntile = red[5 + (it + 2) % 3];
-      if (r == 0) red[4] = Kt;
-      tc::mbar_arrive(rdyC);
-      tc::mbar_arrive(tstart);
-      float ld0 = 0.f, ld1 = 0.f, ld2 = 0.f;   // consumed after the slot rounds (latency hidden)
-      if (pv) {
-        ld0 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 0) << 16);
-        ld1 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 1) << 16);
-        ld2 = __uint_as_float((uint32_t)__ldg(direct + p * 3 + 2) << 16);
+      const long p = tile / TB_SBT * TB_SBP + (pe & 0xFFFF);
+      const bool pv = p < P;
+      const int m = pv ? (int)(pe >> 16) : 0;
+      // this row's valid records (16-byte loads of the valid prefix only) and e0, L_d
+      constexpr bool V16 = (K * 22) % 16 == 0;
+      constexpr int PS = K < 8 ? K : 8;             // slots per repack pass
+      constexpr int NW = V16 ? PS * 11 / 2 : 1;     // words per pass
+      uint32_t W[NW > 1 ? NW : 1];
+      const int mv = min(m, PS);
+      if constexpr (V16) {
+        const uint4* src = reinterpret_cast<const uint4*>(tbuf + p * (K * 11));
+        const int nc = (mv * 22 + 15) / 16;
+#pragma unroll
+        for (int c = 0; c < NW / 4; ++c) {
+          const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
+          W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
+        }
       }
-      if (ntile < ntiles) fill_e0(buf ^ 1, np, npv);   // buffer buf^1's e0 was last read by the previous tile's accB batch
-      const int nnpe = nntile < ntiles ? (int)__ldg(perm + nntile * 128 + r) : 0;   // decoded next iteration
-      TBP_NOW(tp_t1);
-      TBP_ADD(1, tp_t0, tp_t1);
-      TBP_ADD(10, 0, Kt + 1);
-      TBP_ADD(11, 0, 1);
-      if (Kt == 0) { tc::mbar_wait(done1, d1ph); d1ph ^= 1; }   // the tile's (unused) first layer-1 batch
-      // ---- slot rounds: A2 of slot t -> TMEM
-#pragma unroll 1
-      for (int t = 0; t < Kt; ++t) {
-        TBP_NOW(tp_r0);
-        tc::mbar_wait(done1, d1ph); d1ph ^= 1;   // batch t-1: acc1 holds slot t
-        tc::fence_after_sync();
-        TBP_NOW(tp_r1);
-        TBP_ADD(3, tp_r0, tp_r1);
-        uint32_t u[H];
+      uint4 ev[C0 / 8];
 #pragma unroll
-        for (int c = 0; c < H / 32; ++c)
-          tc::tmem_ld32(t_acc1 + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c));
-        tc::tmem_ld_wait();
-        uint32_t o[H / 2];
+      for (int j = 0; j < C0 / 8; ++j) ev[j] = pv ? tb_ld_nc4(e0 + p * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
+      float ldv[3] = {0.f, 0.f, 0.f};
+      if (pv)
 #pragma unroll
-        for (int i = 0; i < H / 2; ++i)
-          o[i] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));   // b1 is in acc1
+        for (int c = 0; c < 3; ++c) ldv[c] = __uint_as_float((uint32_t)__ldg(direct + p * 3 + c) << 16);
+      const long ntile = ids[(t + 1) & 3];
+      const uint32_t npe = ntile < ntiles ? __ldg(perm + ntile * 128 + r) : 0u;
+      // buffers free: meta / E0 of tile t-3, A1 of tile t-2
+      tc::mbar_wait(metaFree + e, mfph[e] ^ 1); mfph.flip(e);
+      tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);
+      const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B;
+      if constexpr (V16) {
+        TbWindows<0, PS>::run(W, m, a1, 0, r);
+        if constexpr (K > 8) {   // second pass: slots 8..15
+          const uint4* src = reinterpret_cast<const uint4*>(tbuf + p * (K * 11) + 8 * 11);
+          const int m2 = m - 8, nc = m2 > 0 ? (m2 * 22 + 15) / 16 : 0;
 #pragma unroll
-        for (int c = 0; c < H / 32; ++c) tc::tmem_st16(t_a2 + lane_off + 16 * c, o + 16 * c);
-        tc::tmem_st_wait();
-        tc::fence_before_sync();
-        tc::mbar_arrive(rdyA);
-        TBP_NOW(tp_r2);
-        TBP_ADD(4, tp_r1, tp_r2);
+          for (int c = 0; c < NW / 4; ++c) {
+            const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
+            W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
+          }
+          TbWindows<0, K - 8>::run(W, m2, a1, 8, r);
+        }
+      } else {   // rows not 16-byte aligned in global memory: halfword loads (test shapes)
+        const uint16_t* src = tbuf + p * (K * 11);
+        for (int s = 0; s < K; ++s) {
+          uint32_t w[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w[k] = 0;
+          if (s < m) {
+            uint32_t h[12];
+#pragma unroll
+            for (int i = 0; i < 11; ++i) h[i] = __ldg(src + 11 * s + i);
+            h[11] = 0x3F80u;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) w[k] = h[2 * k] | (h[2 * k + 1] << 16);
+            w[6] = 0x3F803F80u;
+          }
+          const uint32_t dst = a1 + (uint32_t)(2 * s) * PL + r * 16;
+          tc::sts128(dst, w[0], w[1], w[2], w[3]);
+          tc::sts128(dst + PL, w[4], w[5], w[6], w[7]);
+        }
       }
-      // ---- final
-      TBP_NOW(tp_f0);
-      tc::mbar_wait(doneF, dfph); dfph ^= 1;     // accB
+#pragma unroll
+      for (int j = 0; j < C0 / 8; ++j)
+        tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[j].x, ev[j].y, ev[j].z, ev[j].w);
+      reinterpret_cast<long long*>(M + S::M_PIX)[r] = pv ? (long long)p : -1ll;
+      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 0] = ldv[0];
+      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 1] = ldv[1];
+      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 2] = ldv[2];
+      M[S::M_CNT + r] = (uint8_t)m;
+      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
+      if (lane == 0) lred[(t & 1) * 4 + warp - 1] = wm;
+      if (r == 0) { ids[(t + 2) & 3] = claim; claim = atomicAdd(sched, 1); }
+      tc::bar_sync(1, 128);
+      if (r == 0) {
+        const int* L = const_cast<const int*>(lred) + (t & 1) * 4;
+        *reinterpret_cast<volatile int*>(M + S::M_KT) = max(max(L[0], L[1]), max(L[2], L[3]));
+      }
+      tc::fence_proxy_async();   // this thread's operand writes -> the tensor core's (async) proxy
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tileReady + e);
+      tile = ntile;
+      pe = npe;
+    }
+  } else if (warp <= 8) {
+    // ---------------------------------------------------------------- E1: A2, phi, psi
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    TbPh trph, d1ph, dbph;
+    int i = 0;
+    auto psi_tile = [&](int u) {
+      const int ab = u & 1;
+      const uint8_t* M = meta(u % 3);
+      tc::mbar_wait(doneB + ab, dbph[ab]); dbph.flip(ab);
       tc::fence_after_sync();
-      TBP_NOW(tp_f1);
-      TBP_ADD(6, tp_f0, tp_f1);
+      uint32_t v[C0];
+#pragma unroll
+      for (int c = 0; c < C0 / 16; ++c)
+        tc::tmem_ld16(tmem + lane_off + S::T_ACCB + ab * C0 + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
+      tc::tmem_ld_wait();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(accBfree + ab);
+      const long long p = reinterpret_cast<const long long*>(M + S::M_PIX)[r];
+      const float fm = (float)M[S::M_CNT + r];
+      const float* ld = reinterpret_cast<const float*>(M + S::M_LD) + 3 * r;
+      const float ld0 = ld[0], ld1 = ld[1], ld2 = ld[2];
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(metaFree + u % 3);
       const float* WO = prm.WO;
       float ps0 = prm.bO[0], ps1 = prm.bO[1], ps2 = prm.bO[2];
       ps0 = fmaf(WO[0 * NO + C0 + 0], ld0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], ld1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], ld2, ps0);
       ps1 = fmaf(WO[1 * NO + C0 + 0], ld0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], ld1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], ld2, ps1);
       ps2 = fmaf(WO[2 * NO + C0 + 0], ld0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], ld1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], ld2, ps2);
-      const float fm = (float)m;
 #pragma unroll
-      for (int c = 0; c < C0 / 16; ++c) {
-        uint32_t u[16];
-        tc::tmem_ld16(t_accB + lane_off + c * 16, u);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int o = c * 16 + i;
-          const float phi = relu(__uint_as_float(u[i]) + prm.bB[o] + prm.wBn[o] * fm);
-          ps0 = fmaf(WO[0 * NO + o], phi, ps0);
-          ps1 = fmaf(WO[1 * NO + o], phi, ps1);
-          ps2 = fmaf(WO[2 * NO + o], phi, ps2);
-        }
+      for (int o = 0; o < C0; ++o) {
+        const float phi = relu(__uint_as_float(v[o]) + prm.bB[o] + prm.wBn[o] * fm);
+        ps0 = fmaf(WO[0 * NO + o], phi, ps0);
+        ps1 = fmaf(WO[1 * NO + o], phi, ps1);
+        ps2 = fmaf(WO[2 * NO + o], phi, ps2);
       }
-      if (pv) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
-      tc::fence_before_sync();
-      TBP_NOW(tp_end);
-      TBP_ADD(8, tp_f1, tp_end);
-      TBP_ADD(9, tp_t0, tp_end);
-      // advance the tile pipeline
-      tile = ntile; p = np; m = nm; pv = npv;
-      ntile = nntile;
-      decode(ntile, nnpe, np, nm, npv);
+      if (p >= 0) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
+    };
+    int pend = -1;
+    for (int t = 0;; ++t) {
+      const int e = t % 3;
+      tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
+      const int Kt = *reinterpret_cast<volatile int*>(meta(e) + S::M_KT);
+      if (Kt < 0) break;
+#pragma unroll 1
+      for (int s = 0; s < Kt; ++s) {
+        const int b = i & 1;
+        tc::mbar_wait(done1 + b, d1ph[b]); d1ph.flip(b);
+        tc::fence_after_sync();
+        const uint32_t ta = tmem + lane_off + S::T_ACC1 + b * H;
+#pragma unroll
+        for (int c = 0; c < H / 32; ++c) {
+          uint32_t u[32], o[16];
+          tc::tmem_ld32(ta + 32 * c, u);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
+          tc::tmem_st16(ta + 16 * c, o);   // A2 over the columns this thread has read (c = 0 first)
+        }
+        tc::tmem_st_wait();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(rdyA + b);
+        ++i;
+        if (s == min(LAG, Kt - 1) && pend >= 0) { psi_tile(pend); pend = -1; }
+      }
+      if (Kt == 0 && pend >= 0) { psi_tile(pend); pend = -1; }
+      pend = t;
     }
-    // stop the MMA warp and E2
-    tc::bar_sync(bar_id, 128);
-    if (r == 0) red[4] = -1;
-    tc::bar_sync(bar_id, 128);
-    tc::mbar_arrive(rdyC);
-    tc::mbar_arrive(tstart);
+    if (pend >= 0) psi_tile(pend);
+  } else {
+    // ---------------------------------------------------------------- E2: the pool, tau
+    constexpr int HC = H / 2;   // channels per warp
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    // the warp's channel half as a compile-time constant, so the b2 addends are constant-bank
+    // operands of the FFMA.SAT (no registers)
+    auto e2 = [&](auto hc) {
+      constexpr int h = decltype(hc)::value;
+      TbPh trph, d2ph, dbph;
+      int i = 0;
+      for (int t = 0;; ++t) {
+        const int e = t % 3, ab = t & 1;
+        tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
+        const int Kt = *reinterpret_cast<volatile int*>(meta(e) + S::M_KT);
+        if (Kt < 0) break;
+        const int m = meta(e)[S::M_CNT + r];
+        uint32_t pool[HC];
+#pragma unroll
+        for (int j = 0; j < HC; ++j) pool[j] = 0;
+#pragma unroll 1
+        for (int s = 0; s < Kt; ++s) {
+          const int b = i & 1;
+          tc::mbar_wait(done2 + b, d2ph[b]); d2ph.flip(b);
+          tc::fence_after_sync();
+          uint32_t u[HC];
+          const uint32_t ta = tmem + lane_off + S::T_ACC2 + b * H + h * HC;
+#pragma unroll
+          for (int c = 0; c < HC / 16; ++c) tc::tmem_ld16(ta + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(u + 16 * c));
+          tc::tmem_ld_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(free2 + b);
+          if (s < m) {
+#pragma unroll
+            for (int j = 0; j < HC; j += 2) {
+              const float v0 = ffma_sat(__uint_as_float(u[j]), 1.f, prm.b2s[h * HC + j]);
+              const float v1 = ffma_sat(__uint_as_float(u[j + 1]), 1.f, prm.b2s[h * HC + j + 1]);
+              const float2 w = __fadd2_rn(make_float2(v0, v1), make_float2(1.f, 1.f));
+              pool[j] += __float_as_uint(w.x);
+              pool[j + 1] += __float_as_uint(w.y);
+            }
+          }
+          ++i;
+        }
+        // tau(t) -> TMEM (its buffer's previous reader, B of tile t-2, has completed)
+        if (t >= 2) { tc::mbar_wait(doneB + ab, dbph[ab]); dbph.flip(ab); }
+        if (Kt > 0) {
+          const uint32_t off = (uint32_t)m * TB_ONE_BITS;
+          const float sc = (POOL == 1 && m > 0) ? TB_QUNIT / (float)m : TB_QUNIT;
+          uint32_t o[HC / 2];
+#pragma unroll
+          for (int j = 0; j < HC / 2; ++j)
+            o[j] = tc::cvt_relu_f16x2((float)(pool[2 * j] - off) * sc, (float)(pool[2 * j + 1] - off) * sc);
+          const uint32_t tt = tmem + lane_off + S::T_TAU + ab * (H / 2) + h * (HC / 2);
+          if constexpr (HC / 2 == 16) tc::tmem_st16(tt, o);
+          else tc::tmem_st8(tt, o);
+          tc::tmem_st_wait();
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) { tc::mbar_arrive(tauRdy + ab); tc::mbar_arrive(metaFree + e); }
+      }
+    };
+    if (warp < 13) e2(TbInt<0>{});
+    else e2(TbInt<1>{});
   }
   tc::fence_before_sync();
   __syncthreads();
-  TBP_FLUSH();
-  if (threadIdx.x < 32) tc::tmem_dealloc<512>(*tptr);
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace gn

@@ -25,7 +25,7 @@ EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glas
            "glassnet_set_kernel_family", "glassnet_get_unique_id", "glassnet_comm_create",
            "glassnet_comm_destroy", "glassnet_tile_rows", "glassnet_forward_sharded",
            "glassnet_destroy", "glassnet_last_error", "glassnet_profile_begin", "glassnet_profile_end",
-           "glassnet_forward_sharded_local"]
+           "glassnet_forward_sharded_local", "glassnet_debug_psi"]
 
 
 class GlassNetError(RuntimeError):
@@ -83,6 +83,8 @@ def lib():
         L.glassnet_profile_end.argtypes = [vp, i32, vp, vp, vp, vp]
         L.glassnet_forward_sharded_local.restype = ctypes.c_int
         L.glassnet_forward_sharded_local.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+        L.glassnet_debug_psi.restype = ctypes.c_int
+        L.glassnet_debug_psi.argtypes = [vp, vp, i32, vp]
         L.glassnet_destroy.restype = None
         L.glassnet_destroy.argtypes = [vp]
         L.glassnet_last_error.restype = ctypes.c_char_p
@@ -175,6 +177,14 @@ class GlassNet:
     def forward_sharded(self, comm, gbuf, direct, tbuf, tcount, out, stream=None):
         _check(lib().glassnet_forward_sharded(self._h, comm._h, _ptr(gbuf), _ptr(direct), _ptr(tbuf),
                                               _ptr(tcount), _ptr(out), _stream(stream)))
+        return out
+
+    def debug_psi(self, batch, stream=None):
+        """psi of the last forward ([batch][H][W][3] fp32 device tensor; test/diagnostic)."""
+        import torch
+        d = self.dims
+        out = torch.empty((batch, d.height, d.width, 3), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(lib().glassnet_debug_psi(self._h, _ptr(out), batch, _stream(stream)))
         return out
 
     def workspace_bytes(self):

@@ -60,3 +60,53 @@ def window_oracle(cfg, weights, frame, rows, cols, margin=64, seed=1, mask=None)
 def errs(gpu, ref):
     e = np.abs(np.asarray(gpu, np.float64) - ref)
     return float(e.max()), float(e.mean())
+
+
+def _crop(H, W, u, rows, cols, margin):
+    a = max(0, (rows[0] - margin) // u * u)
+    b = min(H, -(-(rows[1] + margin) // u) * u)
+    c = max(0, (cols[0] - margin) // u * u)
+    e = min(W, -(-(cols[1] + margin) // u) * u)
+    return a, b, c, e
+
+
+def band_oracle(cfg, weights, fr, frame_idx=0, margin=40, threads=None, band=None):
+    """Full-frame oracle output of frame `frame_idx` of the stored inputs `fr` (synth.Frames),
+    computed as row bands of the frame, each from a crop extended by `margin` rows (aligned to
+    2^(L-1)), in a thread pool (the C oracle releases the GIL).  Bitwise equal to the
+    full-frame oracle when the margin covers the receptive field (pinned in
+    test_window_oracle.py for margin 40)."""
+    import concurrent.futures as cf
+    import os
+    H, W, L = cfg.height, cfg.width, cfg.levels
+    u = 1 << (L - 1)
+    threads = threads or max(1, os.cpu_count() or 1)
+    if band is None:
+        band = max(u, -(-H // (2 * threads)) // u * u)
+    w64 = weights.astype(np.float64)
+    out = np.zeros((H, W, 3), np.float64)
+
+    def run(r0):
+        r1 = min(H, r0 + band)
+        a, b, _, _ = _crop(H, W, u, (r0, r1), (0, W), margin)
+        sub = synth.Frames(fr.gbuf[frame_idx:frame_idx + 1, a:b], fr.direct[frame_idx:frame_idx + 1, a:b],
+                           fr.tbuf[frame_idx:frame_idx + 1, a:b], fr.tcount[frame_idx:frame_idx + 1, a:b],
+                           fr.precision)
+        g, d, t, n = sub.as64()
+        dims = oracle.make_dims(b - a, W, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool)
+        o = oracle.forward(dims, w64, g[0], d[0], t[0], n[0])
+        out[r0:r1] = o[r0 - a:r1 - a]
+
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, range(0, H, band)))
+    return out
+
+
+def frames_from_device(g, d, t, n, precision="bf16"):
+    """Device input tensors -> synth.Frames of their stored bits (host)."""
+    import torch
+    if precision == "bf16":
+        cv = lambda x: x.cpu().view(torch.int16).numpy().view(np.uint16)
+    else:
+        cv = lambda x: x.cpu().numpy()
+    return synth.Frames(cv(g), cv(d), cv(t), n.cpu().numpy(), precision)
