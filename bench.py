@@ -344,6 +344,9 @@ def run_ours(args):
 
 
 if __name__ == "__main__":
+    if os.environ.get("GN_BENCH_TRACE"):   # diagnostic: dump Python stacks after N s (hang triage)
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["GN_BENCH_TRACE"]), exit=True)
     a = parse()
     if a.impl == "reference":
         run_reference(a)

@@ -635,6 +635,18 @@ extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int
   return GLASSNET_OK;
 }
 
+#ifdef GN_TB_PROF
+extern "C" int glassnet_debug_tb_prof(unsigned long long* out32, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out32, gn::gn_tb_prof, 32 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(gn::gn_tb_prof, z, sizeof z);
+  }
+  return 0;
+}
+#endif
+
 #ifdef GN_MBAR_WATCHDOG
 static unsigned int* gn_wd_host = nullptr;
 // diagnostic: map a host log the mbarrier watchdog writes before it traps (read after a failure)

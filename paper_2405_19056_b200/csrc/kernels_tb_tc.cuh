@@ -18,24 +18,27 @@
 // loader, so their bits (NaN/Inf allowed, reading R4) never reach shared memory.
 //
 // Pool (R5): a2 = ReLU(W2 a1 + b2) enters as Q = round(a2 * 2^12) via
-//   v = sat(acc2 + b2 2^-11)        (W2 pre-scaled by 2^-11: one FFMA.SAT = bias, ReLU and the
+//   v = sat(acc2 + b2 2^-11)        (W2 pre-scaled by 2^-11: one FADD.SAT = bias, ReLU and the
 //                                    saturation at a2 = 2048)
 //   pool += bits(1 + v) - bits(1)   (v + 1 has ulp 2^-23, i.e. 2^-12 in a2 units)
 // -- integer adds, so any order of the valid slots gives the same bits.
 //
-// Warp roles (one CTA per SM, 17 warps):
-//   w0       MMA: one thread issues every tcgen05.mma / commit
-//   w1..w4   loader: claims tiles, reads the count-sorted perm, the valid records (16-byte
-//            loads of the valid prefix only), e0 and L_d; repacks the records into the K=16
-//            slot windows (A1, 2 buffers), e0 into its operand (E0, 3 buffers), per-tile meta
-//   w5..w8   E1: A2 = bf16(ReLU(acc1)) written back INTO acc1's first H/2 columns (layer 2
-//            reads its A operand from TMEM); per tile, one tile late: phi, psi -> HBM
-//   w9..w16  E2: two warps per TMEM lane quadrant, H/2 channels each: the fixed-point pool;
-//            per tile tau -> f16 -> TMEM (the B MMA's A operand)
-// Software pipeline: acc1 and acc2 are 2-deep rings, so layer 1 of item i+1 and E1 of item
-// i+1 overlap layer 2 of item i, and E2 of item i overlaps both.  B of tile t (e0 part + tau
-// part) is issued after layer 2 of tile t+1's item min(1, Kt-1), E1's phi/psi of tile t right
-// after that item's epilogue (the pool of tile t has then had a full item to finish).
+// Warp roles (one CTA per SM, 22 warps):
+//   w0        issuer A (one thread): layer 1 of every item (+ its commit), B of every tile
+//   w1        issuer B (one thread): layer 2 of every item (+ its commit).  One thread issues a
+//             tcgen05.mma only every ~50 cycles; two reach the N=64 pipe rate (ubench_multi2)
+//   w2..w5    loader: claims tiles, reads the count-sorted perm, the valid records (16-byte
+//             loads of the valid prefix only), e0 and L_d; repacks the records into the K=16
+//             slot windows (A1 ring), e0 into its operand (E0 ring), per-tile meta
+//   w6..w13   E1: two warps per TMEM lane quadrant, H/2 channels each: A2 = bf16(ReLU(acc1))
+//             written back INTO acc1 (layer 2 reads its A operand from TMEM); phi / psi -> HBM
+//   w14..w21  E2: two warps per quadrant, H/2 channels each: the fixed-point pool, tau -> f16 ->
+//             TMEM (the B MMA's A operand)
+// Software pipeline: acc1 is a 3-deep ring (issuer A runs up to 2 items ahead of issuer B),
+// acc2 2-deep; the tensor pipe orders nothing across the two issuers, so A writes acc1[j % 3]
+// only after layer 2 of item j-3 (its previous reader) has completed.  B of tile u is issued
+// by A before layer 1 of item last(u) + 4 and phi / psi by E1 right after that item (B's MMAs
+// precede it in A's issue order, so they have completed).
 // Hand-offs are mbarriers; each waiter is provably at most one phase behind.
 #pragma once
 #include <cuda_bf16.h>
@@ -45,6 +48,28 @@
 #include "tc_ptx.cuh"
 
 namespace gn {
+
+#ifdef GN_TB_PROF
+// Diagnostic build only (-DGN_TB_PROF): 32-bit clock() intervals accumulated in registers
+// (constant indices, so the array is scalarised), flushed once per role by one thread at the
+// role's end; summed over CTAs (glassnet_debug_tb_prof).  Indices: tools/tb_breakdown.py.
+__device__ unsigned long long gn_tb_prof[32];
+#define TBP_DECL() uint32_t tbp_acc[32] = {}
+#define TBP_NOW(v) const uint32_t v = (uint32_t)clock()
+#define TBP_ADD(i, a) (tbp_acc[i] += (uint32_t)clock() - (a))
+#define TBP_CNT(i, n) (tbp_acc[i] += (uint32_t)(n))
+#define TBP_FLUSH_IF(c)                                                              \
+  if (c) {                                                                           \
+    _Pragma("unroll") for (int i_ = 0; i_ < 32; ++i_)                                \
+      if (tbp_acc[i_]) atomicAdd(&gn_tb_prof[i_], (unsigned long long)tbp_acc[i_]); \
+  }
+#else
+#define TBP_DECL()
+#define TBP_NOW(v)
+#define TBP_ADD(i, a)
+#define TBP_CNT(i, n)
+#define TBP_FLUSH_IF(c)
+#endif
 
 constexpr uint32_t TB_ONE_BITS = 0x3F800000u;   // bits of 1.0f (the pool's per-fragment offset)
 constexpr float TB_VSCALE = 1.0f / 2048.0f;     // a2 -> v = a2 2^-11 (saturation at a2 = 2048)
@@ -59,7 +84,7 @@ struct TbParams {
   float wBn[32];         // B weight of the count channel n
   float WO[3 * 35];      // [3][C0+3]: output 1x1 over [d0 ; L_d] (L_d part zero if R does not take it)
   float bO[4];
-  float b2s[64];         // b2 2^-11 (the pool's FFMA.SAT addend)
+  float b2s[64];         // b2 2^-11 (the pool's FADD.SAT addend)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -153,20 +178,32 @@ struct TbLayout {
   static constexpr int WBT_B = C0 * H * 2;            // f16
   static constexpr int WIMG_B = W1_B + W2_B + WBE_B + WBT_B;
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBE = OFF_W2 + W2_B, OFF_WBT = OFF_WBE + WBE_B;
-  static constexpr int NA = 2, NE = 3;                // A1 ring, E0 / meta ring
-  static constexpr int OFF_A1 = (WIMG_B + 1023) / 1024 * 1024;
-  static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
-  // per-tile meta: pixel ids, counts, L_d (E1's psi needs them one tile late), Kt, tile id
+  // per-tile meta: pixel ids, counts, L_d (E2's psi needs them one tile late), Kt
   static constexpr int M_PIX = 0, M_LD = 128 * 8, M_CNT = M_LD + 128 * 12, M_KT = M_CNT + 128, META_B = M_KT + 16;
-  static constexpr int OFF_META = OFF_E0 + NE * E0_B;
-  static constexpr int NBAR = 24;
+  // ASYNC (K = 8): the loader cp.asyncs each row's valid record bytes into a raw staging ring
+  // one tile ahead (row stride an odd multiple of 16 B: conflict-free 16-byte reads) and repacks
+  // from there; otherwise it loads into registers
+  static constexpr bool ASYNC = K == 8;
+  static constexpr int RAW_ROW = ((K * 22 + 15) / 16 | 1) * 16, RAW_B = 128 * RAW_ROW;
+  static constexpr int NE = ASYNC ? 6 : 5;            // E0 / meta ring (tiles the loader may run ahead)
+  static constexpr int OFF_A1 = (WIMG_B + 1023) / 1024 * 1024;
+  static constexpr int REST = NE * E0_B + NE * META_B + 64 * 8 + 128 + 3072 + (ASYNC ? 2 * RAW_B : 0);
+  static constexpr int LIMIT = 232448 - 1024;
+  static constexpr int NA = OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;   // A1 ring
+  static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
+  static constexpr int OFF_RAW = OFF_E0 + NE * E0_B;
+  static constexpr int OFF_META = OFF_RAW + (ASYNC ? 2 * RAW_B : 0);
+  static constexpr int NBAR = 40;
   static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
-  static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch
-  static constexpr int SMEM = OFF_MISC + 64;
-  static constexpr int NWARP = 17, THREADS = 32 * NWARP;
-  static constexpr int T_ACC1 = 0, T_ACC2 = 2 * H, T_ACCB = 4 * H, T_TAU = 4 * H + 2 * C0;   // TMEM columns
-  static_assert(T_TAU + H <= 512, "TMEM");
-  static_assert(SMEM <= 232448 - 1024, "shared memory");
+  static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch, blend queue
+  static constexpr int OFF_PSX = OFF_MISC + 128;      // psi partials of the h = 1 E1 warps [2][4][32][3] f32
+  static constexpr int SMEM = OFF_PSX + 2 * 4 * 32 * 3 * 4;
+  static constexpr int NWARP = 22, THREADS = 32 * NWARP;   // 2 MMA issuers, 4 loader, 8 E1, 8 E2
+  // TMEM columns: acc1 ring of 3 (A2 written over its first H/2 columns), acc2 ring of 2,
+  // accB x 2, tau x 4 (f16 pairs; E2 writes tau(u) once B(u-4) has completed)
+  static constexpr int T_ACC1 = 0, T_ACC2 = 3 * H, T_ACCB = 5 * H, T_TAU = 5 * H + 2 * C0;
+  static_assert(T_TAU + 4 * (H / 2) <= 512, "TMEM");
+  static_assert(SMEM <= LIMIT, "shared memory");
 };
 
 // layer-1 window repack of one record (8 words) from the row's words W starting at halfword 11s
@@ -194,6 +231,9 @@ __device__ __forceinline__ void tb_window(const uint32_t* W, bool valid, uint32_
 template <int S, int NS>
 struct TbWindows {   // slots S..S+NS-1 of a pass whose words start at the pass's first record
   __device__ __forceinline__ static void run(const uint32_t* W, int m_rel, uint32_t a1, int slot0, int r) {
+#ifdef GN_ABL_LOADER
+    return;   // ablation (diagnostic builds): no repack / stores
+#endif
     if constexpr (NS > 0) {
       uint32_t o[8];
       tb_window<S>(W, S < m_rel, o);
@@ -204,6 +244,14 @@ struct TbWindows {   // slots S..S+NS-1 of a pass whose words start at the pass'
     }
   }
 };
+
+// 16-byte cp.async with zero fill: copies `bytes` (0..16) from src, zeros the rest of the 16
+__device__ __forceinline__ void cp_async16z(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t tb_ld_nc(const uint32_t* p) {
   uint32_t v;
@@ -216,9 +264,11 @@ __device__ __forceinline__ uint4 tb_ld_nc4(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
-__device__ __forceinline__ float ffma_sat(float a, float b, float c) {
+// FADD.SAT: clamp(a + c, 0, 1) in one instruction; c can be a constant-bank operand (an FFMA
+// with an immediate multiplier would need c in a register, i.e. an LDC per use)
+__device__ __forceinline__ float fadd_sat(float a, float c) {
   float d;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  asm("add.rn.sat.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(c));
   return d;
 }
 
@@ -232,43 +282,47 @@ struct TbPh {
   __device__ __forceinline__ void flip(int i) { v ^= 1u << i; }
 };
 
+// 22 warps: the busiest SM sub-partitions hold 6 of them, so 16,384 / (6 x 32) registers
 template <int K, int H, int C0, int POOL>
-__global__ void __launch_bounds__(TbLayout<K, H, C0>::THREADS, 1)
+__global__ void __maxnreg__(80)
 k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, const uint16_t* __restrict__ direct,
         const uint8_t* __restrict__ wimg, const __grid_constant__ TbParams prm, const uint32_t* __restrict__ perm,
         float* __restrict__ psi, long P, int* __restrict__ sched) {
   using S = TbLayout<K, H, C0>;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t PL = S::PL;
-  constexpr int NO = C0 + 3;
-  constexpr int LAG = 1;   // B / psi of tile t follow item min(LAG, Kt-1) of tile t+1
+  constexpr int NO = C0 + 3, NE = S::NE, NA = S::NA;
+  constexpr int LAGI = 4;   // B of tile u: issued by A before layer 1 of item last(u) + LAGI, psi by E1 after it
   static_assert(C0 <= 32 && (H == 32 || H == 64), "TbParams sizes / epilogue chunks");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
-  uint64_t* tileReady = bars + 0;   // [3] loader -> all (4 warp arrivals)
-  uint64_t* metaFree = bars + 3;    // [3] MMA commit (B) + E1 (4) + E2 (8) -> loader
-  uint64_t* a1Free = bars + 6;      // [2] MMA commit after the tile's last layer-1 MMA -> loader
-  uint64_t* done1 = bars + 8;       // [2] commit -> E1 (acc1 ring)
-  uint64_t* rdyA = bars + 10;       // [2] E1 (4) -> MMA: A2 in acc1
-  uint64_t* done2 = bars + 12;      // [2] commit -> E2 (acc2 ring)
-  uint64_t* free2 = bars + 14;      // [2] E2 (8) -> MMA: acc2 read
-  uint64_t* tauRdy = bars + 16;     // [2] E2 (8) -> MMA: tau of the tile in TMEM
-  uint64_t* doneB = bars + 18;      // [2] commit -> E1 (psi) and E2 (tau buffer reuse)
-  uint64_t* accBfree = bars + 20;   // [2] E1 (4) -> MMA: accB read
+  uint64_t* tileReady = bars + 0;   // [NE] loader -> all (4 warp arrivals)
+  uint64_t* metaFree = bars + 6;    // [NE] E1 (8, psi) + E2 (8, counts read) -> loader
+  uint64_t* a1Free = bars + 12;     // [NA] E1 (8): the tile's last layer-1 MMA has completed -> loader
+  uint64_t* done1 = bars + 15;      // [3] issuer A's commit of layer 1 of item i -> E1
+  uint64_t* rdyA = bars + 18;       // [3] E1 (8) -> issuer B: A2 of item i in acc1[i % 3]
+  uint64_t* done2 = bars + 21;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
+  uint64_t* free2 = bars + 25;      // [2] E2 (8) -> issuer B: acc2[i % 2] read
+  uint64_t* tauRdy = bars + 27;     // [4] E2 (8) -> issuer A: tau of tile u in TMEM tau[u % 4]
+  uint64_t* doneB = bars + 31;      // [4] issuer A's commit of B(u) -> E1 (psi), E2 (tau[u % 4] reuse)
+  uint64_t* accBfree = bars + 35;   // [2] E1 (8, psi) -> issuer A: accB read
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_MISC);
   volatile int* lred = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 16);   // [2][4] warp max counts
-  volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 48);    // [4] claimed tile ids
-  auto meta = [&](int e) -> uint8_t* { return smem + S::OFF_META + e * S::META_B; };
+  volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 64);    // [8] claimed tile ids
+  volatile int* total = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 96);  // items in the launch (A -> B)
+  auto meta = [&](int t) -> uint8_t* { return smem + S::OFF_META + (t % NE) * S::META_B; };
 
+  TBP_DECL();
   for (int i = threadIdx.x; i < S::WIMG_B / 16; i += blockDim.x)
     reinterpret_cast<int4*>(smem)[i] = reinterpret_cast<const int4*>(wimg)[i];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 3; ++i) { tc::mbar_init(tileReady + i, 4); tc::mbar_init(metaFree + i, 13); }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(a1Free + i, 1); tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 4);
-      tc::mbar_init(done2 + i, 1); tc::mbar_init(free2 + i, 8); tc::mbar_init(tauRdy + i, 8);
-      tc::mbar_init(doneB + i, 1); tc::mbar_init(accBfree + i, 4);
-    }
+    for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, 4); tc::mbar_init(metaFree + i, 16); }
+    for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 8);
+    for (int i = 0; i < 3; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 8); }
+    for (int i = 0; i < 4; ++i) tc::mbar_init(done2 + i, 1);
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(free2 + i, 8); tc::mbar_init(accBfree + i, 8); }
+    for (int i = 0; i < 4; ++i) { tc::mbar_init(tauRdy + i, 8); tc::mbar_init(doneB + i, 1); }
+    *total = 0x7FFFFFFF;
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<512>(tptr);
@@ -279,138 +333,254 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   const uint32_t tmem = *tptr;
   const long ntiles = (P + TB_SBP - 1) / TB_SBP * TB_SBT;
 
-  if (warp == 0) {
-    // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
-      const uint32_t sWBE = tc::smem_u32(smem + S::OFF_WBE), sWBT = tc::smem_u32(smem + S::OFF_WBT);
-      const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
-      constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
-      constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
-      constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
+  if (warp <= 1) {
+    // ---------------------------------------------------------------- MMA issuers (one thread each):
+    // A = layer 1 + B, B = layer 2.  One thread can issue a tcgen05.mma only every ~50 cycles;
+    // two reach the N=64 pipe rate (tools/ubench_multi2.cu).  Across the two threads the
+    // tensor pipe gives no ordering, so A issues layer 1 of item j into acc1[j % 3] only after
+    // layer 2 of item j-3 (its previous reader) has COMPLETED (done2 commit).
+    const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
+    const uint32_t sWBE = tc::smem_u32(smem + S::OFF_WBE), sWBT = tc::smem_u32(smem + S::OFF_WBT);
+    const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
+    constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
+    constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
+    constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
+    if (warp == 0 && lane == 0) {
+      // ------------------------------------------------ issuer A: layer 1 of every item, B of every tile
       const uint64_t dW1 = tc::smem_desc(sW1, H * 16, 128);
-      TbPh trph, aph, f2ph, tph, bfph;
-      int i1 = 0, i2 = 0;
-      auto layer1 = [&](int t, int s) {   // tile t's slot s -> acc1[i1 & 1]
-        const uint32_t a = sA1 + (uint32_t)(t & 1) * S::A1_B + (uint32_t)(2 * s) * PL;
-        tc::mma_f16_ss(tmem + S::T_ACC1 + (i1 & 1) * H, tc::smem_desc(a, PL, 128), dW1, ID_T, 0);
-        tc::mma_commit(done1 + (i1 & 1));
-        ++i1;
+      TbPh trph, d2ph, tph, bfph;
+      TBP_NOW(tot0);
+      int ct = 0, cs = 0, cK = 0, nL1 = 0;
+      // blend queue (tile, due item): at most LAGI + 1 tiles pending (every tile has >= 1 item),
+      // registers with constant indices
+      int bqt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bqd[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bqn = 0;
+      auto peek = [&](int t) -> int {   // wait for tile t's operands, return its Kt (-1: end)
+        TBP_NOW(w0);
+        tc::mbar_wait(tileReady + t % NE, trph[t % NE]); trph.flip(t % NE);
+        TBP_ADD(0, w0);
+        TBP_CNT(19, 1);
+        return *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
       };
-      auto blend = [&](int u, int Ku) {   // B of tile u: accB = e0 W_B,e0^T + tau W_B,tau^T
-        const int ab = u & 1, e = u % 3;
-        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);   // E1 read tile u-2's accB
-        tc::mbar_wait(tauRdy + ab, tph[ab]); tph.flip(ab);           // E2 wrote tau(u) (even Ku = 0)
+      auto blend = [&]() {   // B of the queue's front tile u: accB = e0 W_B,e0^T + tau W_B,tau^T
+        const int u = bqt[0];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) { bqt[k] = bqt[k + 1]; bqd[k] = bqd[k + 1]; }
+        --bqn;
+        const int ab = u & 1;
+        TBP_NOW(w0);
+        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);   // E2 read tile u-2's accB
+        tc::mbar_wait(tauRdy + (u & 3), tph[u & 3]); tph.flip(u & 3);   // E2 wrote tau(u)
+        TBP_ADD(3, w0);
         tc::fence_after_sync();
+        TBP_NOW(bl0);
         const uint32_t dB = tmem + S::T_ACCB + ab * C0;
 #pragma unroll
         for (int q = 0; q < C0 / 16; ++q)
-          tc::mma_f16_ss(dB, tc::smem_desc(sE0 + (uint32_t)e * S::E0_B + 2 * q * PL, PL, 128),
+          tc::mma_f16_ss(dB, tc::smem_desc(sE0 + (uint32_t)(u % NE) * S::E0_B + 2 * q * PL, PL, 128),
                          tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-        if (Ku > 0)
 #pragma unroll
-          for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ts(dB, tmem + S::T_TAU + ab * (H / 2) + 8 * q,
-                           tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
-        tc::mma_commit(doneB + ab);
-        tc::mma_commit(metaFree + e);
+        for (int q = 0; q < H / 16; ++q)
+          tc::mma_f16_ts(dB, tmem + S::T_TAU + (u & 3) * (H / 2) + 8 * q,
+                         tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
+        tc::mma_commit(doneB + (u & 3));
+        TBP_ADD(23, bl0);
       };
-      auto peek = [&](int t) -> int {   // wait for tile t's operands, return its Kt (-1: end)
-        tc::mbar_wait(tileReady + t % 3, trph[t % 3]); trph.flip(t % 3);
-        return *reinterpret_cast<volatile int*>(meta(t % 3) + S::M_KT);
+      auto push_tile = [&](int t, int Kt) {   // due: LAGI items after the tile's last item
+        const int d = nL1 + Kt - 1 + LAGI;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == bqn) { bqt[k] = t; bqd[k] = d; }
+        ++bqn;
       };
-      int t = 0, Kt = peek(0);
-      int pend = -1, pendK = 0;
-      if (Kt > 0) layer1(0, 0);
-      while (Kt >= 0) {
-        int Ktn = 0;
-        for (int s = 0; s < Kt; ++s) {
-          if (s + 1 < Kt) {
-            layer1(t, s + 1);
-          } else {   // last item of tile t: its A1 buffer is free once these MMAs complete
-            tc::mma_commit(a1Free + (t & 1));
-            Ktn = peek(t + 1);
-            if (Ktn > 0) layer1(t + 1, 0);
-          }
-          const int b = i2 & 1;
-          tc::mbar_wait(rdyA + b, aph[b]); aph.flip(b);              // A2 of item i2 in acc1[b]
-          tc::mbar_wait(free2 + b, f2ph[b] ^ 1); f2ph.flip(b);       // E2 read acc2[b] (item i2-2)
+      cK = peek(0);
+      if (cK >= 0) push_tile(0, cK);
+      while (cK >= 0) {
+        // B of the tiles due now, BEFORE a possible wait for the loader (which may wait for these
+        // tiles' psi to free a meta slot)
+        TBP_NOW(bq0);
+        while (bqn > 0 && bqd[0] <= nL1) blend();
+        TBP_ADD(31, bq0);
+        if (cs >= cK) {   // next tile (every tile has >= 1 item: Kt = max(1, max n))
+          ++ct;
+          cK = peek(ct);
+          cs = 0;
+          if (cK < 0) break;
+          push_tile(ct, cK);
+        }
+        if (nL1 >= 3) {   // acc1[nL1 % 3]'s previous reader, layer 2 of item nL1-3, has completed
+          const int pb = (nL1 - 3) & 3;
+          TBP_NOW(w1);
+          tc::mbar_wait(done2 + pb, d2ph[pb]); d2ph.flip(pb);
+          TBP_ADD(2, w1);
           tc::fence_after_sync();
-          const uint32_t d2 = tmem + S::T_ACC2 + b * H, a2 = tmem + S::T_ACC1 + b * H;
-#pragma unroll
-          for (int q = 0; q < H / 16; ++q)
-            tc::mma_f16_ts(d2, a2 + 8 * q, tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
-          tc::mma_commit(done2 + b);
-          ++i2;
-          if (s == min(LAG, Kt - 1) && pend >= 0) { blend(pend, pendK); pend = -1; }
         }
-        if (Kt == 0) {
-          tc::mma_commit(a1Free + (t & 1));
-          if (pend >= 0) { blend(pend, pendK); pend = -1; }
-          Ktn = peek(t + 1);
-          if (Ktn > 0) layer1(t + 1, 0);
-        }
-        pend = t; pendK = Kt;
-        ++t;
-        Kt = Ktn;
+        TBP_NOW(l0);
+        const uint32_t a = sA1 + (uint32_t)(ct % NA) * S::A1_B + (uint32_t)(2 * cs) * PL;
+        tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H, tc::smem_desc(a, PL, 128), dW1, ID_T, 0);
+        tc::mma_commit(done1 + nL1 % 3);
+        TBP_ADD(20, l0);
+        TBP_CNT(18, 1);
+        ++nL1; ++cs;
       }
-      if (pend >= 0) blend(pend, pendK);
+      // wake issuer B, which waits for rdyA of item nL1 (it does not exist): first let layer 2 of
+      // the last items complete -- their rdyA phases must be fully arrived by E1 before this
+      // extra arrival, or it would over-arrive an open phase
+      for (int k = (nL1 >= 3 ? nL1 - 3 : 0); k < nL1; ++k) { tc::mbar_wait(done2 + (k & 3), d2ph[k & 3]); d2ph.flip(k & 3); }
+      *total = nL1;
+      tc::mbar_arrive_cnt(rdyA + nL1 % 3, 8);
+      while (bqn > 0) blend();
+      TBP_ADD(4, tot0);
+      TBP_FLUSH_IF(true);
+    } else if (warp == 1 && lane == 0) {
+      // ------------------------------------------------ issuer B: layer 2 of every item
+      TbPh aph, f2ph;
+      TBP_NOW(tot0);
+      for (int i = 0;; ++i) {
+        const int a3 = i % 3, b = i & 1;
+        TBP_NOW(w0);
+        tc::mbar_wait(rdyA + a3, aph[a3]); aph.flip(a3);             // A2 of item i in acc1[i % 3]
+        TBP_ADD(1, w0);
+        if (i >= *total) break;
+        TBP_NOW(w1);
+        tc::mbar_wait(free2 + b, f2ph[b] ^ 1); f2ph.flip(b);         // E2 read acc2[b] (item i-2)
+        TBP_ADD(11, w1);
+        tc::fence_after_sync();
+        const uint32_t d2 = tmem + S::T_ACC2 + b * H, a2 = tmem + S::T_ACC1 + a3 * H;
+        TBP_NOW(l2a);
+#pragma unroll
+        for (int q = 0; q < H / 16; ++q)
+          tc::mma_f16_ts(d2, a2 + (q / (H / 32)) * (H / 2) + (q % (H / 32)) * 8,   // A2 half h at column h H/2
+                         tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
+        tc::mma_commit(done2 + (i & 3));
+        TBP_ADD(21, l2a);
+      }
+      TBP_ADD(22, tot0);
+      TBP_FLUSH_IF(true);
     }
-  } else if (warp <= 4) {
+  } else if (warp <= 5) {
     // ---------------------------------------------------------------- loader
-    const int r = (warp - 1) * 32 + lane;
+    const int r = (warp - 2) * 32 + lane;
     const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
     TbPh mfph, afph;
     int claim = 0;
-    if (r == 0) { ids[0] = atomicAdd(sched, 1); ids[1] = atomicAdd(sched, 1); claim = atomicAdd(sched, 1); }
+    // tile ids are claimed three ahead by thread 0 (ids ring of 8), perm entries read one tile
+    // ahead of the tile whose copies are issued
+    if (r == 0) {
+      ids[0] = atomicAdd(sched, 1); ids[1] = atomicAdd(sched, 1); ids[2] = atomicAdd(sched, 1);
+      claim = atomicAdd(sched, 1);
+    }
     tc::bar_sync(1, 128);
+    auto perm_of = [&](long tl) -> uint32_t { return tl < ntiles ? __ldg(perm + tl * 128 + r) : 0u; };
+    auto decode = [&](long tl, uint32_t pe, long& p, int& m) {
+      p = tl / TB_SBT * TB_SBP + (pe & 0xFFFF);
+      m = (tl < ntiles && p < P) ? (int)(pe >> 16) : 0;
+      if (!(tl < ntiles && p < P)) p = -1;
+    };
+    // ASYNC: issue tile tl's copies -- the row's valid record bytes into raw buffer rb (zero fill
+    // beyond them), e0 straight into its operand slot (K-major planes) -- and return L_d
+    auto issue = [&](long tl, uint32_t pe, int rb, int es, float (&ldv)[3]) {
+      long p; int m;
+      decode(tl, pe, p, m);
+      const uint32_t raw = tc::smem_u32(smem + S::OFF_RAW) + rb * S::RAW_B + r * S::RAW_ROW;
+      const char* src = p >= 0 ? reinterpret_cast<const char*>(tbuf + p * (K * 11)) : reinterpret_cast<const char*>(tbuf);
+      const int vb = m * 22;
+#pragma unroll
+      for (int c = 0; c < (K * 22 + 15) / 16; ++c)
+        cp_async16z(raw + 16 * c, src + 16 * c, (uint32_t)min(max(vb - 16 * c, 0), 16));
+      const uint16_t* es_src = p >= 0 ? e0 + p * C0 : e0;
+#pragma unroll
+      for (int j = 0; j < C0 / 8; ++j)
+        cp_async16z(sE0 + (uint32_t)es * S::E0_B + j * PL + r * 16, es_src + 8 * j, p >= 0 ? 16u : 0u);
+      ldv[0] = ldv[1] = ldv[2] = 0.f;
+      if (p >= 0)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ldv[c] = __uint_as_float((uint32_t)__ldg(direct + p * 3 + c) << 16);
+    };
     long tile = ids[0];
-    uint32_t pe = tile < ntiles ? __ldg(perm + tile * 128 + r) : 0u;
+    uint32_t pe = perm_of(tile);
+    long ntile = ids[1];
+    uint32_t npe = perm_of(ntile);
+    float ldc[3] = {0.f, 0.f, 0.f};
+    if constexpr (S::ASYNC) {   // tile 0's copies (its operand slots are fresh: slot 0 counts as waited)
+      if (tile < ntiles) issue(tile, pe, 0, 0, ldc);
+      cp_async_commit();
+      mfph.flip(0);
+    }
+    TBP_NOW(tot0);
     for (int t = 0;; ++t) {
-      const int e = t % 3, a = t & 1;
-      uint8_t* M = meta(e);
-      if (tile >= ntiles) {
-        tc::mbar_wait(metaFree + e, mfph[e] ^ 1);
+      const int e = t % NE, a = t % NA;
+      uint8_t* M = meta(t);
+      if (tile >= ntiles) {   // end marker (ASYNC: this slot was waited for one iteration ago)
+        if constexpr (!S::ASYNC) tc::mbar_wait(metaFree + e, mfph[e] ^ 1);
         if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = -1;
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tileReady + e);
+        if constexpr (S::ASYNC) cp_async_wait_all();
+        TBP_ADD(7, tot0);
+        TBP_FLUSH_IF(r == 0);
         break;
       }
-      const long p = tile / TB_SBT * TB_SBP + (pe & 0xFFFF);
-      const bool pv = p < P;
-      const int m = pv ? (int)(pe >> 16) : 0;
-      // this row's valid records (16-byte loads of the valid prefix only) and e0, L_d
-      constexpr bool V16 = (K * 22) % 16 == 0;
+      TBP_NOW(ld0);
+      long p; int m;
+      decode(tile, pe, p, m);
+      const bool pv = p >= 0;
+      float ldv[3] = {0.f, 0.f, 0.f};
       constexpr int PS = K < 8 ? K : 8;             // slots per repack pass
+      constexpr bool V16 = (K * 22) % 16 == 0;
       constexpr int NW = V16 ? PS * 11 / 2 : 1;     // words per pass
       uint32_t W[NW > 1 ? NW : 1];
-      const int mv = min(m, PS);
-      if constexpr (V16) {
-        const uint4* src = reinterpret_cast<const uint4*>(tbuf + p * (K * 11));
-        const int nc = (mv * 22 + 15) / 16;
+      uint4 ev[C0 / 8];
+      if constexpr (S::ASYNC) {
+        // the next tile's copies first (its E0 / meta slot: tile t+1-NE's consumers are done), then
+        // this tile's (issued one iteration ago) are waited for
+        float ldn[3];
+        TBP_NOW(w0);
+        tc::mbar_wait(metaFree + (t + 1) % NE, mfph[(t + 1) % NE] ^ 1); mfph.flip((t + 1) % NE);
+        TBP_ADD(5, w0);
+        if (ntile < ntiles) issue(ntile, npe, (t + 1) & 1, (t + 1) % NE, ldn);
+        cp_async_commit();
+        cp_async_wait_1();
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { ldv[c] = ldc[c]; ldc[c] = ldn[c]; }
+        const uint32_t raw = tc::smem_u32(smem + S::OFF_RAW) + (t & 1) * S::RAW_B + r * S::RAW_ROW;
 #pragma unroll
         for (int c = 0; c < NW / 4; ++c) {
-          const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
-          W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
+          uint32_t x0, x1, x2, x3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(raw + 16 * c));
+          W[4 * c] = x0; W[4 * c + 1] = x1; W[4 * c + 2] = x2; W[4 * c + 3] = x3;
         }
+      } else {
+        // this row's valid records (16-byte loads of the valid prefix only) and e0, L_d
+        const int mv = min(m, PS);
+        if constexpr (V16) {
+          const uint4* src = reinterpret_cast<const uint4*>(tbuf + (pv ? p : 0) * (K * 11));
+          const int nc = (mv * 22 + 15) / 16;
+#pragma unroll
+          for (int c = 0; c < NW / 4; ++c) {
+            const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
+            W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < C0 / 8; ++j) ev[j] = pv ? tb_ld_nc4(e0 + p * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
+        if (pv)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ldv[c] = __uint_as_float((uint32_t)__ldg(direct + p * 3 + c) << 16);
+        TBP_NOW(w0);
+        tc::mbar_wait(metaFree + e, mfph[e] ^ 1); mfph.flip(e);   // meta / E0 of tile t-NE
+        TBP_ADD(5, w0);
       }
-      uint4 ev[C0 / 8];
-#pragma unroll
-      for (int j = 0; j < C0 / 8; ++j) ev[j] = pv ? tb_ld_nc4(e0 + p * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
-      float ldv[3] = {0.f, 0.f, 0.f};
-      if (pv)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ldv[c] = __uint_as_float((uint32_t)__ldg(direct + p * 3 + c) << 16);
-      const long ntile = ids[(t + 1) & 3];
-      const uint32_t npe = ntile < ntiles ? __ldg(perm + ntile * 128 + r) : 0u;
-      // buffers free: meta / E0 of tile t-3, A1 of tile t-2
-      tc::mbar_wait(metaFree + e, mfph[e] ^ 1); mfph.flip(e);
-      tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);
+      const long nntile = ids[(t + 2) & 7];   // written before the last bar.sync
+      const uint32_t nnpe = perm_of(nntile);
+      TBP_NOW(w1);
+      tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);       // A1 of tile t-NA
+      TBP_ADD(6, w1);
+      TBP_NOW(st0);
       const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B;
       if constexpr (V16) {
         TbWindows<0, PS>::run(W, m, a1, 0, r);
         if constexpr (K > 8) {   // second pass: slots 8..15
-          const uint4* src = reinterpret_cast<const uint4*>(tbuf + p * (K * 11) + 8 * 11);
+          const uint4* src = reinterpret_cast<const uint4*>(tbuf + (pv ? p : 0) * (K * 11) + 8 * 11);
           const int m2 = m - 8, nc = m2 > 0 ? (m2 * 22 + 15) / 16 : 0;
 #pragma unroll
           for (int c = 0; c < NW / 4; ++c) {
@@ -420,7 +590,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           TbWindows<0, K - 8>::run(W, m2, a1, 8, r);
         }
       } else {   // rows not 16-byte aligned in global memory: halfword loads (test shapes)
-        const uint16_t* src = tbuf + p * (K * 11);
+        const uint16_t* src = tbuf + (pv ? p : 0) * (K * 11);
         for (int s = 0; s < K; ++s) {
           uint32_t w[8];
 #pragma unroll
@@ -439,164 +609,236 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           tc::sts128(dst + PL, w[4], w[5], w[6], w[7]);
         }
       }
+      if constexpr (!S::ASYNC)
 #pragma unroll
-      for (int j = 0; j < C0 / 8; ++j)
-        tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[j].x, ev[j].y, ev[j].z, ev[j].w);
+        for (int j = 0; j < C0 / 8; ++j)
+          tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[j].x, ev[j].y, ev[j].z, ev[j].w);
       reinterpret_cast<long long*>(M + S::M_PIX)[r] = pv ? (long long)p : -1ll;
       reinterpret_cast<float*>(M + S::M_LD)[3 * r + 0] = ldv[0];
       reinterpret_cast<float*>(M + S::M_LD)[3 * r + 1] = ldv[1];
       reinterpret_cast<float*>(M + S::M_LD)[3 * r + 2] = ldv[2];
       M[S::M_CNT + r] = (uint8_t)m;
       const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
-      if (lane == 0) lred[(t & 1) * 4 + warp - 1] = wm;
-      if (r == 0) { ids[(t + 2) & 3] = claim; claim = atomicAdd(sched, 1); }
+      if (lane == 0) lred[(t & 1) * 4 + warp - 2] = wm;
+      if (r == 0) { ids[(t + 3) & 7] = claim; claim = atomicAdd(sched, 1); }
+      TBP_ADD(25, st0);
+      TBP_NOW(w2);
       tc::bar_sync(1, 128);
+      TBP_ADD(8, w2);
       if (r == 0) {
         const int* L = const_cast<const int*>(lred) + (t & 1) * 4;
-        *reinterpret_cast<volatile int*>(M + S::M_KT) = max(max(L[0], L[1]), max(L[2], L[3]));
+        // Kt >= 1 even for a tile of empty pixels (one item of zero records, pooled by nobody): every
+        // tile then advances the item pipeline, which bounds how far a blocked consumer can lag
+        // (deadlock freedom of the rings)
+        *reinterpret_cast<volatile int*>(M + S::M_KT) = max(1, max(max(L[0], L[1]), max(L[2], L[3])));
       }
-      tc::fence_proxy_async();   // this thread's operand writes -> the tensor core's (async) proxy
+      tc::fence_proxy_async();   // this thread's operand writes (and its waited cp.asyncs) -> async proxy
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tileReady + e);
-      tile = ntile;
-      pe = npe;
+      TBP_ADD(26, ld0);
+      tile = ntile; pe = npe;
+      ntile = nntile; npe = nnpe;
     }
-  } else if (warp <= 8) {
-    // ---------------------------------------------------------------- E1: A2, phi, psi
-    const int q = warp & 3, r = q * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    TbPh trph, d1ph, dbph;
-    int i = 0;
-    auto psi_tile = [&](int u) {
-      const int ab = u & 1;
-      const uint8_t* M = meta(u % 3);
-      tc::mbar_wait(doneB + ab, dbph[ab]); dbph.flip(ab);
-      tc::fence_after_sync();
-      uint32_t v[C0];
-#pragma unroll
-      for (int c = 0; c < C0 / 16; ++c)
-        tc::tmem_ld16(tmem + lane_off + S::T_ACCB + ab * C0 + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
-      tc::tmem_ld_wait();
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(accBfree + ab);
-      const long long p = reinterpret_cast<const long long*>(M + S::M_PIX)[r];
-      const float fm = (float)M[S::M_CNT + r];
-      const float* ld = reinterpret_cast<const float*>(M + S::M_LD) + 3 * r;
-      const float ld0 = ld[0], ld1 = ld[1], ld2 = ld[2];
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(metaFree + u % 3);
-      const float* WO = prm.WO;
-      float ps0 = prm.bO[0], ps1 = prm.bO[1], ps2 = prm.bO[2];
-      ps0 = fmaf(WO[0 * NO + C0 + 0], ld0, ps0); ps0 = fmaf(WO[0 * NO + C0 + 1], ld1, ps0); ps0 = fmaf(WO[0 * NO + C0 + 2], ld2, ps0);
-      ps1 = fmaf(WO[1 * NO + C0 + 0], ld0, ps1); ps1 = fmaf(WO[1 * NO + C0 + 1], ld1, ps1); ps1 = fmaf(WO[1 * NO + C0 + 2], ld2, ps1);
-      ps2 = fmaf(WO[2 * NO + C0 + 0], ld0, ps2); ps2 = fmaf(WO[2 * NO + C0 + 1], ld1, ps2); ps2 = fmaf(WO[2 * NO + C0 + 2], ld2, ps2);
-#pragma unroll
-      for (int o = 0; o < C0; ++o) {
-        const float phi = relu(__uint_as_float(v[o]) + prm.bB[o] + prm.wBn[o] * fm);
-        ps0 = fmaf(WO[0 * NO + o], phi, ps0);
-        ps1 = fmaf(WO[1 * NO + o], phi, ps1);
-        ps2 = fmaf(WO[2 * NO + o], phi, ps2);
-      }
-      if (p >= 0) { psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2; }
-    };
-    int pend = -1;
-    for (int t = 0;; ++t) {
-      const int e = t % 3;
-      tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
-      const int Kt = *reinterpret_cast<volatile int*>(meta(e) + S::M_KT);
-      if (Kt < 0) break;
-#pragma unroll 1
-      for (int s = 0; s < Kt; ++s) {
-        const int b = i & 1;
-        tc::mbar_wait(done1 + b, d1ph[b]); d1ph.flip(b);
+  } else if (warp <= 13) {
+    // ---------------------------------------------------------------- E1: A2 = bf16(ReLU(acc1)) -> TMEM; psi
+    // two warps per TMEM lane quadrant, H/2 channels each; half h writes its A2 (H/4 packed
+    // columns) over the first columns it has itself read: columns [h H/2, h H/2 + H/4).
+    // psi of tile u right after item last(u) + LAGI: issuer A issued B of tile u before layer 1
+    // of that item, in order, so its doneB has completed by then (no wait on the item chain);
+    // the pair (h = 0, 1) splits accB's columns and adds the halves through shared memory.
+    auto e1 = [&](auto hc) {
+      constexpr int h = decltype(hc)::value;
+      constexpr int HC = H / 2, CH = C0 / 2;
+      const int q = warp & 3, r = q * 32 + lane;
+      const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+      float* psx = reinterpret_cast<float*>(smem + S::OFF_PSX);
+      TbPh trph, d1ph, dbph;
+      int i = 0;
+      int pqt[6] = {0, 0, 0, 0, 0, 0}, pqd[6] = {0, 0, 0, 0, 0, 0}, pqn = 0;   // pending psi: (tile, due item)
+      auto psi_tile = [&]() {
+        const int u = pqt[0];
+  #pragma unroll
+        for (int k = 0; k < 5; ++k) { pqt[k] = pqt[k + 1]; pqd[k] = pqd[k + 1]; }
+        --pqn;
+        const int ab = u & 1;
+        const uint8_t* M = meta(u);
+        TBP_NOW(w0);
+        tc::mbar_wait(doneB + (u & 3), dbph[u & 3]); dbph.flip(u & 3);
+        TBP_ADD(28, w0);
         tc::fence_after_sync();
-        const uint32_t ta = tmem + lane_off + S::T_ACC1 + b * H;
-#pragma unroll
-        for (int c = 0; c < H / 32; ++c) {
-          uint32_t u[32], o[16];
-          tc::tmem_ld32(ta + 32 * c, u);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int k = 0; k < 16; ++k) o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
-          tc::tmem_st16(ta + 16 * c, o);   // A2 over the columns this thread has read (c = 0 first)
-        }
-        tc::tmem_st_wait();
+        uint32_t v[CH];
+        if constexpr (CH == 16) tc::tmem_ld16(tmem + lane_off + S::T_ACCB + ab * C0 + h * CH, *reinterpret_cast<uint32_t(*)[16]>(v));
+        else tc::tmem_ld8(tmem + lane_off + S::T_ACCB + ab * C0 + h * CH, *reinterpret_cast<uint32_t(*)[8]>(v));
+        tc::tmem_ld_wait();
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(rdyA + b);
-        ++i;
-        if (s == min(LAG, Kt - 1) && pend >= 0) { psi_tile(pend); pend = -1; }
+        if (lane == 0) tc::mbar_arrive(accBfree + ab);
+#ifdef GN_ABL_PSI
+        if (u >= 0) { __syncwarp(); if (lane == 0) tc::mbar_arrive(metaFree + u % NE); return; }
+#endif
+        const float fm = (float)M[S::M_CNT + r];
+        const float* WO = prm.WO;
+        float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f;
+  #pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int o = h * CH + k;
+          const float phi = relu(__uint_as_float(v[k]) + prm.bB[o] + prm.wBn[o] * fm);
+          ps0 = fmaf(WO[0 * NO + o], phi, ps0);
+          ps1 = fmaf(WO[1 * NO + o], phi, ps1);
+          ps2 = fmaf(WO[2 * NO + o], phi, ps2);
+        }
+        float* px = psx + ((u & 1) * 4 + q) * 96 + 3 * lane;
+        if (h == 1) { px[0] = ps0; px[1] = ps1; px[2] = ps2; }
+        tc::bar_sync(2 + q, 64);
+        if (h == 0) {
+          const long long p = reinterpret_cast<const long long*>(M + S::M_PIX)[r];
+          const float* ld = reinterpret_cast<const float*>(M + S::M_LD) + 3 * r;
+          const float ld0 = ld[0], ld1 = ld[1], ld2 = ld[2];
+          float o0 = prm.bO[0] + ps0 + px[0], o1 = prm.bO[1] + ps1 + px[1], o2 = prm.bO[2] + ps2 + px[2];
+          o0 = fmaf(WO[0 * NO + C0 + 0], ld0, o0); o0 = fmaf(WO[0 * NO + C0 + 1], ld1, o0); o0 = fmaf(WO[0 * NO + C0 + 2], ld2, o0);
+          o1 = fmaf(WO[1 * NO + C0 + 0], ld0, o1); o1 = fmaf(WO[1 * NO + C0 + 1], ld1, o1); o1 = fmaf(WO[1 * NO + C0 + 2], ld2, o1);
+          o2 = fmaf(WO[2 * NO + C0 + 0], ld0, o2); o2 = fmaf(WO[2 * NO + C0 + 1], ld1, o2); o2 = fmaf(WO[2 * NO + C0 + 2], ld2, o2);
+          if (p >= 0) { psi[p * 3 + 0] = o0; psi[p * 3 + 1] = o1; psi[p * 3 + 2] = o2; }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(metaFree + u % NE);
+      };
+      TBP_NOW(tot0);
+      for (int t = 0;; ++t) {
+        const int e = t % NE;
+        TBP_NOW(w9);
+        tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
+        TBP_ADD(10, w9);
+        const int Kt = *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
+        if (Kt < 0) break;
+        {   // queue this tile's psi: LAGI items after its last item
+          const int d = i + Kt - 1 + LAGI;
+  #pragma unroll
+          for (int k = 0; k < 6; ++k)
+            if (k == pqn) { pqt[k] = t; pqd[k] = d; }
+          ++pqn;
+        }
+  #pragma unroll 1
+        for (int s = 0; s < Kt; ++s) {
+          const int a3 = i % 3;
+          TBP_NOW(w0);
+          // one warp polls the barrier, the group of 8 E1 warps is released by a named barrier
+          if (warp == 6) tc::mbar_wait(done1 + a3, d1ph[a3]);
+          d1ph.flip(a3);
+          tc::bar_sync(6, 256);
+          TBP_ADD(9, w0);
+          TBP_NOW(w1);
+          tc::fence_after_sync();
+          if (s == Kt - 1 && lane == 0) tc::mbar_arrive(a1Free + t % NA);   // the tile's layer-1 MMAs are done
+          const uint32_t ta = tmem + lane_off + S::T_ACC1 + a3 * H + h * HC;
+          uint32_t u[HC], o[HC / 2];
+          if constexpr (HC == 32) tc::tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(u));
+          else tc::tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(u));
+          tc::tmem_ld_wait();
+  #pragma unroll
+          for (int k = 0; k < HC / 2; ++k) o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
+          if constexpr (HC == 32) tc::tmem_st16(ta, o);
+          else tc::tmem_st8(ta, o);
+          tc::tmem_st_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(rdyA + a3);
+          TBP_ADD(16, w1);
+          TBP_NOW(w2);
+          while (pqn > 0 && pqd[0] <= i) psi_tile();
+          TBP_ADD(27, w2);
+          ++i;
+        }
       }
-      if (Kt == 0 && pend >= 0) { psi_tile(pend); pend = -1; }
-      pend = t;
-    }
-    if (pend >= 0) psi_tile(pend);
+      while (pqn > 0) psi_tile();
+      TBP_ADD(12, tot0);
+
+    };
+    // the half h as a compile-time constant: psi's weights are then constant-bank operands
+    if (warp < 10) e1(TbInt<0>{});
+    else e1(TbInt<1>{});
+    TBP_FLUSH_IF(warp == 8 && lane == 0);
   } else {
     // ---------------------------------------------------------------- E2: the pool, tau
     constexpr int HC = H / 2;   // channels per warp
     const int q = warp & 3, r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     // the warp's channel half as a compile-time constant, so the b2 addends are constant-bank
-    // operands of the FFMA.SAT (no registers)
+    // operands of the FADD.SAT (no registers)
     auto e2 = [&](auto hc) {
       constexpr int h = decltype(hc)::value;
       TbPh trph, d2ph, dbph;
       int i = 0;
+      TBP_NOW(tot0);
       for (int t = 0;; ++t) {
-        const int e = t % 3, ab = t & 1;
+        const int e = t % NE, ab = t & 1;
         tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
-        const int Kt = *reinterpret_cast<volatile int*>(meta(e) + S::M_KT);
+        const int Kt = *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
         if (Kt < 0) break;
-        const int m = meta(e)[S::M_CNT + r];
+        const int m = meta(t)[S::M_CNT + r];
         uint32_t pool[HC];
 #pragma unroll
         for (int j = 0; j < HC; ++j) pool[j] = 0;
 #pragma unroll 1
         for (int s = 0; s < Kt; ++s) {
           const int b = i & 1;
-          tc::mbar_wait(done2 + b, d2ph[b]); d2ph.flip(b);
+          TBP_NOW(w0);
+          if (warp == 14) tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // one warp polls, the
+          d2ph.flip(i & 3);                                               // group of 8 follows
+          tc::bar_sync(7, 256);
+          TBP_ADD(13, w0);
+          TBP_NOW(w1);
           tc::fence_after_sync();
           uint32_t u[HC];
           const uint32_t ta = tmem + lane_off + S::T_ACC2 + b * H + h * HC;
 #pragma unroll
           for (int c = 0; c < HC / 16; ++c) tc::tmem_ld16(ta + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(u + 16 * c));
           tc::tmem_ld_wait();
+          TBP_ADD(24, w1);
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(free2 + b);
+#ifndef GN_ABL_E2ALU
           if (s < m) {
+#else
+          if (s < m && m > 100) {   // ablation (diagnostic builds): the pool's arithmetic skipped
+#endif
 #pragma unroll
             for (int j = 0; j < HC; j += 2) {
-              const float v0 = ffma_sat(__uint_as_float(u[j]), 1.f, prm.b2s[h * HC + j]);
-              const float v1 = ffma_sat(__uint_as_float(u[j + 1]), 1.f, prm.b2s[h * HC + j + 1]);
+              const float v0 = fadd_sat(__uint_as_float(u[j]), prm.b2s[h * HC + j]);
+              const float v1 = fadd_sat(__uint_as_float(u[j + 1]), prm.b2s[h * HC + j + 1]);
               const float2 w = __fadd2_rn(make_float2(v0, v1), make_float2(1.f, 1.f));
               pool[j] += __float_as_uint(w.x);
               pool[j + 1] += __float_as_uint(w.y);
             }
           }
           ++i;
+          TBP_ADD(17, w1);
         }
-        // tau(t) -> TMEM (its buffer's previous reader, B of tile t-2, has completed)
-        if (t >= 2) { tc::mbar_wait(doneB + ab, dbph[ab]); dbph.flip(ab); }
-        if (Kt > 0) {
+        // tau(t) -> TMEM, once B of tile t-4 (the last reader of this tau buffer) has completed
+        TBP_NOW(w5);
+        if (t >= 4) { tc::mbar_wait(doneB + (t & 3), dbph[t & 3]); dbph.flip(t & 3); }
+        TBP_ADD(14, w5);
+        {
           const uint32_t off = (uint32_t)m * TB_ONE_BITS;
           const float sc = (POOL == 1 && m > 0) ? TB_QUNIT / (float)m : TB_QUNIT;
           uint32_t o[HC / 2];
 #pragma unroll
           for (int j = 0; j < HC / 2; ++j)
             o[j] = tc::cvt_relu_f16x2((float)(pool[2 * j] - off) * sc, (float)(pool[2 * j + 1] - off) * sc);
-          const uint32_t tt = tmem + lane_off + S::T_TAU + ab * (H / 2) + h * (HC / 2);
+          const uint32_t tt = tmem + lane_off + S::T_TAU + (t & 3) * (H / 2) + h * (HC / 2);
           if constexpr (HC / 2 == 16) tc::tmem_st16(tt, o);
           else tc::tmem_st8(tt, o);
           tc::tmem_st_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) { tc::mbar_arrive(tauRdy + (t & 3)); tc::mbar_arrive(metaFree + e); }
         }
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) { tc::mbar_arrive(tauRdy + ab); tc::mbar_arrive(metaFree + e); }
       }
+      TBP_ADD(15, tot0);
+      TBP_FLUSH_IF(warp == 16 && lane == 0);
     };
-    if (warp < 13) e2(TbInt<0>{});
+    if (warp < 18) e2(TbInt<0>{});
     else e2(TbInt<1>{});
   }
   tc::fence_before_sync();

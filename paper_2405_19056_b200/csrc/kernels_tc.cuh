@@ -129,7 +129,7 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
     pack_kmajor(w1, H, 16, false, img);
   }
   // W2 [H][H], scaled by 2^-11 (exact: a power of two), so acc2 = (W2 a1) 2^-11 and the pool's
-  // FFMA.SAT with b2 2^-11 is ReLU + saturation at a2 = 2048 in one instruction
+  // FADD.SAT with b2 2^-11 is ReLU + saturation at a2 = 2048 in one instruction
   std::vector<float> w2((size_t)H * H, 0.f);
   for (int o = 0; o < H; ++o)
     for (int i = 0; i < H; ++i) w2[(size_t)o * H + i] = rb(T2W[o * H + i]) * TB_VSCALE;
