@@ -58,9 +58,9 @@ def build_lib(force=False, verbose=True):
     return LIB
 
 
-def build_profile_lib(verbose=True, name="libglassnet_prof.so", defines=("GN_PROFILE_TB",)):
+def build_profile_lib(verbose=True, name="libglassnet_prof.so", defines=("GN_TB_PROF",)):
     """Diagnostic variant (bench configuration's T kernel only): by default with the T
-    kernel's clock64 phase counters (-DGN_PROFILE_TB); `defines` selects ablation switches."""
+    kernel's per-role clock64 counters (-DGN_TB_PROF); `defines` selects ablation switches."""
     global LIB
     keep = LIB
     LIB = os.path.join(PKG, name)

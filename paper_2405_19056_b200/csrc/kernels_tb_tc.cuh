@@ -230,17 +230,20 @@ __device__ __forceinline__ void tb_window(const uint32_t* W, bool valid, uint32_
 
 template <int S, int NS>
 struct TbWindows {   // slots S..S+NS-1 of a pass whose words start at the pass's first record
-  __device__ __forceinline__ static void run(const uint32_t* W, int m_rel, uint32_t a1, int slot0, int r) {
+  // lim: slots at or beyond the tile's item count are never read by layer 1 -- not written
+  __device__ __forceinline__ static void run(const uint32_t* W, int m_rel, uint32_t a1, int slot0, int r, int lim) {
 #ifdef GN_ABL_LOADER
     return;   // ablation (diagnostic builds): no repack / stores
 #endif
     if constexpr (NS > 0) {
-      uint32_t o[8];
-      tb_window<S>(W, S < m_rel, o);
-      const uint32_t dst = a1 + (uint32_t)(2 * (slot0 + S)) * (128 * 16) + r * 16;
-      tc::sts128(dst, o[0], o[1], o[2], o[3]);
-      tc::sts128(dst + 128 * 16, o[4], o[5], o[6], o[7]);
-      TbWindows<S + 1, NS - 1>::run(W, m_rel, a1, slot0, r);
+      if (slot0 + S < lim) {
+        uint32_t o[8];
+        tb_window<S>(W, S < m_rel, o);
+        const uint32_t dst = a1 + (uint32_t)(2 * (slot0 + S)) * (128 * 16) + r * 16;
+        tc::sts128(dst, o[0], o[1], o[2], o[3]);
+        tc::sts128(dst + 128 * 16, o[4], o[5], o[6], o[7]);
+      }
+      TbWindows<S + 1, NS - 1>::run(W, m_rel, a1, slot0, r, lim);
     }
   }
 };
@@ -572,13 +575,32 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       }
       const long nntile = ids[(t + 2) & 7];   // written before the last bar.sync
       const uint32_t nnpe = perm_of(nntile);
+      reinterpret_cast<long long*>(M + S::M_PIX)[r] = pv ? (long long)p : -1ll;
+      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 0] = ldv[0];
+      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 1] = ldv[1];
+      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 2] = ldv[2];
+      M[S::M_CNT + r] = (uint8_t)m;
+      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
+      if (lane == 0) lred[(t & 1) * 4 + warp - 2] = wm;
+      if (r == 0) { ids[(t + 3) & 7] = claim; claim = atomicAdd(sched, 1); }
+      TBP_NOW(w2);
+      tc::bar_sync(1, 128);
+      TBP_ADD(8, w2);
+      // Kt >= 1 even for a tile of empty pixels (one item of zero records, pooled by nobody): every
+      // tile then advances the item pipeline, which bounds how far a blocked consumer can lag
+      // (deadlock freedom of the rings)
+      int Kt;
+      {
+        const int* L = const_cast<const int*>(lred) + (t & 1) * 4;
+        Kt = max(1, max(max(L[0], L[1]), max(L[2], L[3])));
+      }
       TBP_NOW(w1);
       tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);       // A1 of tile t-NA
       TBP_ADD(6, w1);
       TBP_NOW(st0);
       const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B;
       if constexpr (V16) {
-        TbWindows<0, PS>::run(W, m, a1, 0, r);
+        TbWindows<0, PS>::run(W, m, a1, 0, r, Kt);
         if constexpr (K > 8) {   // second pass: slots 8..15
           const uint4* src = reinterpret_cast<const uint4*>(tbuf + (pv ? p : 0) * (K * 11) + 8 * 11);
           const int m2 = m - 8, nc = m2 > 0 ? (m2 * 22 + 15) / 16 : 0;
@@ -587,11 +609,11 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
             const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
             W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
           }
-          TbWindows<0, K - 8>::run(W, m2, a1, 8, r);
+          TbWindows<0, K - 8>::run(W, m2, a1, 8, r, Kt);
         }
       } else {   // rows not 16-byte aligned in global memory: halfword loads (test shapes)
         const uint16_t* src = tbuf + (pv ? p : 0) * (K * 11);
-        for (int s = 0; s < K; ++s) {
+        for (int s = 0; s < Kt; ++s) {
           uint32_t w[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) w[k] = 0;
@@ -613,25 +635,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
 #pragma unroll
         for (int j = 0; j < C0 / 8; ++j)
           tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[j].x, ev[j].y, ev[j].z, ev[j].w);
-      reinterpret_cast<long long*>(M + S::M_PIX)[r] = pv ? (long long)p : -1ll;
-      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 0] = ldv[0];
-      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 1] = ldv[1];
-      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 2] = ldv[2];
-      M[S::M_CNT + r] = (uint8_t)m;
-      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
-      if (lane == 0) lred[(t & 1) * 4 + warp - 2] = wm;
-      if (r == 0) { ids[(t + 3) & 7] = claim; claim = atomicAdd(sched, 1); }
       TBP_ADD(25, st0);
-      TBP_NOW(w2);
-      tc::bar_sync(1, 128);
-      TBP_ADD(8, w2);
-      if (r == 0) {
-        const int* L = const_cast<const int*>(lred) + (t & 1) * 4;
-        // Kt >= 1 even for a tile of empty pixels (one item of zero records, pooled by nobody): every
-        // tile then advances the item pipeline, which bounds how far a blocked consumer can lag
-        // (deadlock freedom of the rings)
-        *reinterpret_cast<volatile int*>(M + S::M_KT) = max(1, max(max(L[0], L[1]), max(L[2], L[3])));
-      }
+      if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = Kt;
       tc::fence_proxy_async();   // this thread's operand writes (and its waited cp.asyncs) -> async proxy
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tileReady + e);
