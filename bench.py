@@ -2,11 +2,14 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 
-One step = one forward pass of the whole hot path (T, F, B, R; all §8(a) rows) over one
-batch of 32 synthetic 1920x1080 K=8 frames per GPU (weak scaling: each rank owns its own
-32 frames, no data-path collective).  Inputs (13.7 GB per rank) are larger than L2, so
-no flush is needed between steps.  Timing: CUDA events on the launching stream, barrier
-+ synchronize on both sides, max over ranks.  Prints ONE JSON line on rank 0.
+One step = one forward pass of the whole hot path (T, F, B, R; all §8(a) rows) over the
+configs[3] batch: 32 synthetic 1920x1080 K=8 frames, split data-parallel over the ranks
+(rank r of N owns frames [32r/N, 32(r+1)/N); no data-path collective; strong scaling of the
+fixed 32-frame batch, --weak gives every rank its own 32).  Inputs (13.7 GB per step) are
+larger than L2, so no flush is needed between steps.  Timing: CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks.  Prints ONE JSON line on rank 0;
+at N=1 it also carries configs[1] (fps) and configs[2] (latency) lines and a batch sweep
+(ms/frame at 4/8/16/32 frames: the data-parallel scaling prediction).
 
 --impl reference times the fp64 CPU oracle (oracle/, the reference arm of this tier) on
 a bounded row band of the same workload on the host cores.
@@ -28,7 +31,7 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
-METRIC = "GlassNet frames/sec at 1920x1080 K=8 (configs[3], batch 32 frames per GPU)"
+METRIC = "GlassNet frames/sec at 1920x1080 K=8 (configs[3], 32-frame batch data-parallel over the GPUs)"
 
 
 def parse():
@@ -41,6 +44,8 @@ def parse():
     ap.add_argument("--family", default="tc", choices=["tc", "simt"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weak", action="store_true", help="every rank runs the full 32-frame batch")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c1/c2 lines and the batch sweep")
     return ap.parse_args()
 
 
@@ -136,6 +141,18 @@ class ClockSampler:
                 "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
+def cpu_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_oracle_band(cfg, rows=(0, 272), frame=0):
     """Oracle (single thread, fp64) on a row band of one frame; returns (seconds, fraction of frame)."""
     import oracle
@@ -174,12 +191,58 @@ def run_reference(args):
                       "config": {"workload": cfg.name, "height": cfg.height, "width": cfg.width,
                                  "k_slots": cfg.k_slots, "sample_rows": list(band)},
                       "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "oracle",
-                                       "sample": sample},
+                                       "sample": sample, **cpu_info()},
                       "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0}}))
 
 
 # ----------------------------------------------------------------------------- our arm
+def _time_forward(run, steps, warmup):
+    import torch
+    for _ in range(warmup):
+        run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def run_extras(net, cfg, g, d, t, n, args):
+    """N=1 only: the configs[3] batch sweep (ms/frame at 4/8/16/32 frames of the same handle and
+    inputs: the data-parallel scaling prediction -- rank r of N runs 32/N frames), configs[1]
+    fps (4 x 512^2 K=8) and configs[2] latency (one 1280x720 K=8 frame, disc mask)."""
+    import torch
+    from paper_2405_19056_b200 import GlassNet, make_dims
+    from synth import device as sdev
+    out = torch.empty((cfg.batch, cfg.height, cfg.width, 3), dtype=torch.float32, device="cuda")
+    sweep = {}
+    for b in (4, 8, 16, 32):
+        ms = _time_forward(lambda: net.forward(g[:b], d[:b], t[:b], n[:b], out[:b]), max(3, args.steps), 2)
+        sweep[str(b)] = {"ms_per_forward": ms, "ms_per_frame": ms / b}
+    full = sweep["32"]["ms_per_frame"]
+    pred = {str(N): full / sweep[str(32 // N)]["ms_per_frame"] for N in (2, 4, 8)}
+    res = {"batch_sweep_c3": sweep, "predicted_dp_efficiency_c3": pred}
+    for name in ("c1", "c2"):
+        c = synth.CONFIGS[name]
+        w = synth.make_weights(c.widths, c.levels, c.t_hidden, seed=0, bf16_weights=True)
+        net2 = GlassNet(w, make_dims(c.height, c.width, c.k_slots, c.widths, c.t_hidden, c.levels, max_batch=c.batch,
+                                     pool=c.pool))
+        m = synth.disc_mask(1, c.height, c.width) if c.tcount_mode == "discs" else None
+        g2, d2, t2, n2 = sdev.alloc_and_fill(c, nframes=c.batch, seed=1, mask=m)
+        o2 = torch.empty((c.batch, c.height, c.width, 3), dtype=torch.float32, device="cuda")
+        ms = _time_forward(lambda: net2.forward(g2, d2, t2, n2, o2), 20, 5)
+        res[name] = {"workload": f"{name}: {c.width}x{c.height}, K={c.k_slots}, batch {c.batch}",
+                     "ms_per_forward": ms, "frames_per_s": c.batch * 1000.0 / ms, "ms_per_frame": ms / c.batch,
+                     "l2": "inputs (>= 190 MB) larger than L2; back-to-back forwards"}
+        net2.close()
+        del g2, d2, t2, n2, o2
+    return res
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -195,7 +258,15 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[args.config]
     tiles_mode = args.config == "c4"        # configs[4]: ONE frame split in row tiles (strong scaling)
-    B = 1 if tiles_mode else cfg.batch
+    if tiles_mode:
+        B, f0 = 1, 0
+    elif args.weak:
+        B, f0 = cfg.batch, rank * cfg.batch
+    else:                                   # configs[3]: the 32-frame batch split over the ranks
+        f0 = cfg.batch * rank // world
+        B = cfg.batch * (rank + 1) // world - f0
+        if B < 1:
+            raise SystemExit(f"{world} ranks for a {cfg.batch}-frame batch")
     H, W, K = cfg.height, cfg.width, cfg.k_slots
     w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True)
     dims = make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, precision=cfg.precision, max_batch=B,
@@ -214,8 +285,8 @@ def run_ours(args):
         comm = gb.Comm(uid[0], world, rank)
         run = lambda: net.forward_sharded(comm, g, d, t, n, out)
     else:
-        # inputs resident in HBM: this rank's own 32 frames (weak scaling)
-        g, d, t, n = sdev.alloc_and_fill(cfg, nframes=B, seed=1, frame0=rank * B)
+        # inputs resident in HBM: this rank's frames of the batch
+        g, d, t, n = sdev.alloc_and_fill(cfg, nframes=B, seed=1, frame0=f0)
         out = torch.empty((B, H, W, 3), dtype=torch.float32, device="cuda")
         run = lambda: net.forward(g, d, t, n, out)
     mean_n = float(n.float().mean().item())
@@ -241,13 +312,13 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = float(tmax.item())
-    frames_per_step = 1 if tiles_mode else world * B
+    frames_per_step = 1 if tiles_mode else (world * cfg.batch if args.weak else cfg.batch)
     value = frames_per_step * args.steps / (ms / 1000.0)
 
     # per-stage times (events after every launch, same stream; a second pass of K steps)
     # (a row tile also builds x16 for its halo exchange: one more launch than the full frame)
     launches = net.launches_per_forward(B) + (1 if tiles_mode and args.family == "tc" else 0)
-    net.profile_begin(launches * args.steps + 2)
+    net.profile_begin((launches + 1) * args.steps + 2)   # + the start mark of each forward
     for _ in range(args.steps):
         run()
     stages = net.profile_end()
@@ -261,7 +332,16 @@ def run_ours(args):
     top_name, (top_ms, top_cnt) = top
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    # the burst figure: the step is milliseconds long and the sampled clocks stay at max (the
+    # sustained figure was measured under a seconds-long power-capped loop at ~1335 MHz)
+    clk_sum = clk.summary()
+    sustained_regime = (clk_sum.get("sm_mhz") or 0) < 0.9 * (clk_sum.get("sm_max_mhz") or 1)
+    if "bf16_tflops" in peaks:
+        peak_tf = peaks["bf16_tflops_sustained"] if sustained_regime else peaks["bf16_tflops"]
+        peak_src = ("MEASURED_PEAKS.json " + ("bf16_tflops_sustained (clocks below max during the run)" if sustained_regime
+                    else "bf16_tflops (burst: ms-long step, clocks at max during the run)"))
+    else:
+        peak_tf, peak_src = 1590.0, "fallback 1.59 PF/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
     stage_flops = {"T_B_psi": flops["T"] + flops["B"], "conv_F0": flops["F0"], "conv_F1": flops["F1"],
                    "conv_F2": flops["F2"], "conv_F3": flops["F3"], "conv_R3": flops["R3"], "conv_R2": flops["R2"],
                    "conv_R1": flops["R1"]}
@@ -276,7 +356,8 @@ def run_ours(args):
         roof = {"kernel": top_name, "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved / peak_tf, "traffic": traffic,
                 "alg_flops_per_launch": stage_flops[top_name] * B, "launch_ms": top_ms / top_cnt,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
+                "peak_source": peak_src,
+                "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", peak_tf)}
     else:
         roof = {"kernel": top_name, "bound": "hbm", "achieved": None, "peak": peaks.get("hbm_gbs"),
                 "unit": "GB/s", "frac": None, "traffic": None}
@@ -286,6 +367,12 @@ def run_ours(args):
     whole = {"alg_tflops_per_step": total_alg / 1e12,
              "achieved_tflops": total_alg / (ms / args.steps / 1000.0) / 1e12,
              "frac_of_peak": total_alg / (ms / args.steps / 1000.0) / 1e12 / peak_tf}
+    conv_names = [k for k in stage_flops if k.startswith("conv_")]
+    conv_ms = sum(stages[k][0] for k in conv_names if k in stages) / args.steps
+    if conv_ms > 0:   # north_star: >= 60% of tensor peak on the conv layers (useful FLOPs / time)
+        conv_fl = sum(stage_flops[k] for k in conv_names) * B
+        whole["conv_layers"] = {"ms_per_step": conv_ms, "alg_tflops": conv_fl / (conv_ms / 1000.0) / 1e12,
+                                "frac_of_peak": conv_fl / (conv_ms / 1000.0) / 1e12 / peak_tf}
 
     # end to end: public C-ABI call with pinned HOST buffers (H2D + forward + D2H inside)
     e2e = None
@@ -314,7 +401,10 @@ def run_ours(args):
         s, frac = cpu_oracle_band(cfg, band)
         cpu = {"value": frac / s, "unit": "frames/s", "cores": 1, "kind": "oracle",
                "sample": f"frame 0 rows [{band[0]},{band[1]}) of {H} ({frac * 100:.1f}% of one {W}x{H} K={K} frame), "
-                         f"fp64 C oracle single-threaded, {s:.1f} s; value = fraction/time"}
+                         f"fp64 C oracle single-threaded, {s:.1f} s; value = fraction/time", **cpu_info()}
+    extra = None
+    if rank == 0 and world == 1 and not tiles_mode and not args.no_extra and args.config == "c3":
+        extra = run_extras(net, cfg, g, d, t, n, args)
     if rank == 0:
         if tiles_mode:
             cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, one frame in {world} row tiles, n~U{{0..{K}}}",
@@ -323,20 +413,22 @@ def run_ours(args):
                     "mean_valid_fragments": mean_n}
             metric = f"GlassNet frames/sec at 3840x2160 K=16 (configs[4], one frame row-tiled over {world} GPU)"
         else:
-            cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, {B} frames per GPU, n~U{{0..{K}}}",
-                    "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world} (frames)",
+            cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, batch {frames_per_step} frames, n~U{{0..{K}}}",
+                    "frames_per_gpu": B, "global_batch": frames_per_step, "parallelism": f"dp{world} (frames)",
                     "kernel_family": args.family, "l2": "inputs (13.7 GB/rank) larger than L2; no flush",
                     "mean_valid_fragments": mean_n}
             metric = METRIC
         line = {"metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "ms_per_frame": ms / args.steps / frames_per_step, "higher_is_better": True,
-                "scaling": "strong" if tiles_mode else "weak", "vs_baseline": None, "dtype": "bf16",
+                "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded generator, synth/)",
                 "config": cfgj,
                 "roofline": roof, "whole_step": whole, "stages": stage_report,
-                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk_sum,
                 "gpu_launches": launches * args.steps}
+        if extra:
+            line["extra"] = extra
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
