@@ -232,3 +232,28 @@ def test_repeated_forwards_bitwise(cuda_ok):
             out = net.forward(g, d, t, n)
             assert torch.equal(out, first)
         net.close()
+
+
+def test_output_guard_bands(cuda_ok):
+    """Out-of-bounds write check (compute-sanitizer is closed on this pool): the output tensor is a
+    view into a larger buffer whose guard bands (before and after) hold a NaN pattern; after
+    forwards of ragged shapes (T tiles past the last pixel, K = 3 / 8 / 16) the guards are intact."""
+    import torch
+    from synth import device
+    for H, W, B, K in ((40, 136, 2, 8), (24, 72, 1, 16), (32, 48, 3, 3)):
+        cfg = _cfg("g", H, W, B, K, "bf16")
+        net = net_for(cfg)
+        g, d, t, n = device.alloc_and_fill(cfg)
+        G = 4096
+        size = B * H * W * 3
+        buf = torch.full((G + size + G,), float("nan"), dtype=torch.float32, device="cuda")
+        buf.view(torch.int32)[:G] = 0x7FC01234
+        buf.view(torch.int32)[G + size:] = 0x7FC04321
+        out = buf[G:G + size].view(B, H, W, 3)
+        for _ in range(3):
+            net.forward(g, d, t, n, out)
+        torch.cuda.synchronize()
+        head, tail = buf.view(torch.int32)[:G], buf.view(torch.int32)[G + size:]
+        assert bool((head == 0x7FC01234).all()) and bool((tail == 0x7FC04321).all()), (H, W, B, K)
+        assert bool(torch.isfinite(out).all())
+        net.close()
