@@ -54,7 +54,7 @@ static int run_tile_steps(glassnet_t net, int nranks, int rank, const void* gbuf
                           const void* tbuf, const uint8_t* tcount, float* out, cudaStream_t st,
                           int (*exch)(void*, glassnet_t, int, cudaStream_t), void* ctx) {
   gn::Step steps[64];
-  const int n = gn::tc_steps(net, steps, 64);
+  const int n = gn::tc_steps(net, steps, 64, true);
   net->prof.mark(nullptr, st);
   for (int i = 0; i < n; ++i) {
     int rc = steps[i].kind == gn::ST_EXCH ? exch(ctx, net, steps[i].idx, st)
@@ -129,7 +129,7 @@ extern "C" int glassnet_forward_sharded_local(glassnet_t* nets, int32_t nranks, 
       return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "forward_sharded_local needs all handles on one device");
   }
   gn::Step steps[64];
-  const int n = gn::tc_steps(nets[0], steps, 64);
+  const int n = gn::tc_steps(nets[0], steps, 64, true);
   for (int r = 0; r < nranks; ++r) nets[r]->prof.mark(nullptr, st);
   for (int i = 0; i < n; ++i) {
     if (steps[i].kind != gn::ST_EXCH) {

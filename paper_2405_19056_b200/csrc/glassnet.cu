@@ -342,15 +342,16 @@ static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* 
 // ------------------------------------------------------------------------ forward (tensor-core family)
 namespace gn {
 
-int tc_steps(const glassnet* net, Step* out, int max) {
+int tc_steps(const glassnet* net, Step* out, int max, bool tile) {
   const int L = net->d.levels;
   int n = 0;
   auto push = [&](int kind, int idx) { if (n < max) out[n] = Step{kind, idx}; ++n; };
   push(ST_PREP, 0);
   push(ST_EXCH, TEN_X);
   push(ST_CONV, 0);
+  if (tile) push(ST_TB, 0);   // launched on its own stream: overlaps F1.. and the halo exchanges
   for (int l = 1; l < L; ++l) { push(ST_EXCH, TEN_E + l - 1); push(ST_CONV, l); }
-  push(ST_TB, 0);
+  if (!tile) push(ST_TB, 0);
   push(ST_EXCH, TEN_E + L - 1);
   push(ST_CONV, 4 + L - 1);
   for (int l = L - 1; l >= 2; --l) {
@@ -423,8 +424,24 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
     }
     case ST_TB: {
       const bf* e0 = (const bf*)G.e[0] + (size_t)h * G.W[0] * c[0];
-      int rc = tc_launch_tb(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, st);
-      net->prof.mark("T_B_psi", st);
+      if (!tile) {
+        int rc = tc_launch_tb(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, st);
+        net->prof.mark("T_B_psi", st);
+        return rc;
+      }
+      // row tile: T needs e0's interior rows only (no halo) -> its own stream after F0
+      if (!s->tb_st &&
+          (cudaStreamCreateWithFlags(&s->tb_st, cudaStreamNonBlocking) != cudaSuccess ||
+           cudaEventCreateWithFlags(&s->ev_e0, cudaEventDisableTiming) != cudaSuccess ||
+           cudaEventCreateWithFlags(&s->ev_tb, cudaEventDisableTiming) != cudaSuccess))
+        return gn_fail(GLASSNET_ERR_CUDA, "T stream / events");
+      cudaEventRecord(s->ev_e0, st);
+      cudaStreamWaitEvent(s->tb_st, s->ev_e0, 0);
+      net->prof.mark(nullptr, s->tb_st);
+      int rc = tc_launch_tb(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, s->tb_st);
+      net->prof.mark("T_B_psi", s->tb_st);
+      cudaEventRecord(s->ev_tb, s->tb_st);
+      net->prof.mark(nullptr, st);   // the main stream's stages time from here
       return rc;
     }
     case ST_UP: {
@@ -444,6 +461,7 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       g.rows_f = G.rows[0]; g.rows_f_buf = G.rows[0] + 2 * h; g.grow0_f = G.grow0[0];
       g.rows_c_buf = G.rows[1] + 2 * h; g.grow0_c = G.grow0[1]; g.Hc_full = G.Hfull[1]; g.halo = h;
       const dim3 grid((unsigned)((G.W[0] / 2 + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
+      if (tile) cudaStreamWaitEvent(st, s->ev_tb, 0);   // psi from T's stream
       ew::k_output<<<grid, 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g);
       net->prof.mark("output", st);
       return 0;

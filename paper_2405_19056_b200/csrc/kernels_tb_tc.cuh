@@ -7,15 +7,18 @@
 // superblocks of TB_SBT tiles and a pre-pass (k_tb_sort) orders each superblock's pixels by
 // their valid count n, so a tile runs only as many slot "items" as its largest count.
 //
-// Slot independence BY CONSTRUCTION (reading R5).  Every record is repacked into its own
-// K=16 window: slot s of a row = K-columns [16s, 16s+16) = [11 features, 1, 1, 1, 0, 0], and
-// W1's window = [W1 (depth column x 2^-7), b1 as three exact bf16 pieces, 0, 0].  So layer 1
-// of EVERY slot is the same single MMA instruction shape over a window at the same column
-// offsets (the bias summed inside it), layer 2 the same four TMEM-A MMAs, and the pool an
-// exact integer sum: a fragment's contribution does not depend on the slot it arrived in
-// (measured in tools/ubench_t2.cu: one K=16 MMA sums its products position-independently;
-// round 1's split windows did not).  Masked slots (k >= n) are zero windows written by the
-// loader, so their bits (NaN/Inf allowed, reading R4) never reach shared memory.
+// Slot independence BY CONSTRUCTION (reading R5).  Every record gets its own K=16 window: slot s
+// of a row = K-columns [16s, 16s+16).  Even slots: [11 features, 0, 1, 1, 1, 0]; odd slots
+// (copied from the 4-byte-aligned word before the record): [f, 11 features, 1, 1, 1, 0] where f is
+// the previous (valid) record's last feature.  W1's window variants: even = [W1 (depth column x
+// 2^-7), 0, b1 as three exact bf16 pieces, 0], odd = [0, W1, b1 pieces, 0].  So layer 1 of EVERY
+// slot is ONE MMA whose non-zero products are the same 14 (11 + the bias pieces), summed inside
+// one instruction -- position-independently (tools/ubench_t2.cu, Part A: a K=16 MMA's sum does not
+// depend on the columns its products sit in; round 1's windows split across two MMAs did) -- then
+// the same four TMEM-A layer-2 MMAs, and the pool is an exact integer sum: a fragment's
+// contribution does not depend on the slot it arrived in.  Masked slots (k >= n) are zero-filled
+// (cp.async with source size 0, or stores), so their bits (NaN/Inf allowed, reading R4) never
+// reach shared memory; the odd window's f is a valid record's finite feature times a zero weight.
 //
 // Pool (R5): a2 = ReLU(W2 a1 + b2) enters as Q = round(a2 * 2^12) via
 //   v = sat(acc2 + b2 2^-11)        (W2 pre-scaled by 2^-11: one FADD.SAT = bias, ReLU and the
@@ -172,7 +175,7 @@ struct TbLayout {
   static constexpr int PL = 128 * 16;                 // one 8-column K-plane of a 128-row operand
   static constexpr int A1_B = K * 2 * PL;             // a tile's layer-1 operand: slot s = planes 2s, 2s+1
   static constexpr int E0_B = (C0 / 8) * PL;          // a tile's e0 operand
-  static constexpr int W1_B = 2 * H * 16;             // [2 planes][H][8]: W1 | b1 pieces | 0
+  static constexpr int W1_B = 2 * 2 * H * 16;         // [variant][2 planes][H][8] (see the loader)
   static constexpr int W2_B = H * H * 2;
   static constexpr int WBE_B = C0 * C0 * 2;
   static constexpr int WBT_B = C0 * H * 2;            // f16
@@ -180,19 +183,16 @@ struct TbLayout {
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBE = OFF_W2 + W2_B, OFF_WBT = OFF_WBE + WBE_B;
   // per-tile meta: pixel ids, counts, L_d (E2's psi needs them one tile late), Kt
   static constexpr int M_PIX = 0, M_LD = 128 * 8, M_CNT = M_LD + 128 * 12, M_KT = M_CNT + 128, META_B = M_KT + 16;
-  // ASYNC (K = 8): the loader cp.asyncs each row's valid record bytes into a raw staging ring
-  // one tile ahead (row stride an odd multiple of 16 B: conflict-free 16-byte reads) and repacks
-  // from there; otherwise it loads into registers
-  static constexpr bool ASYNC = K == 8;
-  static constexpr int RAW_ROW = ((K * 22 + 15) / 16 | 1) * 16, RAW_B = 128 * RAW_ROW;
-  static constexpr int NE = ASYNC ? 6 : 5;            // E0 / meta ring (tiles the loader may run ahead)
+  // CP (K even, so every row's records start 4-byte aligned): each record is copied by 4-byte
+  // cp.asyncs straight into its slot window, one tile ahead; otherwise halfword loads + stores
+  static constexpr bool CP = K % 2 == 0;
+  static constexpr int NE = CP ? 6 : 5;               // E0 / meta ring (tiles the loader may run ahead)
   static constexpr int OFF_A1 = (WIMG_B + 1023) / 1024 * 1024;
-  static constexpr int REST = NE * E0_B + NE * META_B + 64 * 8 + 128 + 3072 + (ASYNC ? 2 * RAW_B : 0);
+  static constexpr int REST = NE * E0_B + NE * META_B + 64 * 8 + 128 + 3072;
   static constexpr int LIMIT = 232448 - 1024;
   static constexpr int NA = OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;   // A1 ring
   static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
-  static constexpr int OFF_RAW = OFF_E0 + NE * E0_B;
-  static constexpr int OFF_META = OFF_RAW + (ASYNC ? 2 * RAW_B : 0);
+  static constexpr int OFF_META = OFF_E0 + NE * E0_B;
   static constexpr int NBAR = 40;
   static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch, blend queue
@@ -206,47 +206,11 @@ struct TbLayout {
   static_assert(SMEM <= LIMIT, "shared memory");
 };
 
-// layer-1 window repack of one record (8 words) from the row's words W starting at halfword 11s
-template <int S>
-__device__ __forceinline__ void tb_window(const uint32_t* W, bool valid, uint32_t (&o)[8]) {
-  constexpr uint32_t ONE = 0x3F80u;   // bf16 1.0
-  if ((S & 1) == 0) {
-    constexpr int a = 11 * S / 2;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) o[k] = W[a + k];
-    o[5] = (W[a + 5] & 0xFFFFu) | (ONE << 16);
-  } else {
-    constexpr int a = (11 * S - 1) / 2;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) o[k] = __byte_perm(W[a + k], W[a + k + 1], 0x5432);
-    o[5] = (W[a + 5] >> 16) | (ONE << 16);
-  }
-  o[6] = ONE | (ONE << 16);
-  o[7] = 0;
-  if (!valid)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = 0;
+// 4-byte cp.async with zero fill beyond `bytes` (0..4), cached in L1 (a record row's sectors
+// serve its 6 copies per slot)
+__device__ __forceinline__ void cp_async4z(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
-
-template <int S, int NS>
-struct TbWindows {   // slots S..S+NS-1 of a pass whose words start at the pass's first record
-  // lim: slots at or beyond the tile's item count are never read by layer 1 -- not written
-  __device__ __forceinline__ static void run(const uint32_t* W, int m_rel, uint32_t a1, int slot0, int r, int lim) {
-#ifdef GN_ABL_LOADER
-    return;   // ablation (diagnostic builds): no repack / stores
-#endif
-    if constexpr (NS > 0) {
-      if (slot0 + S < lim) {
-        uint32_t o[8];
-        tb_window<S>(W, S < m_rel, o);
-        const uint32_t dst = a1 + (uint32_t)(2 * (slot0 + S)) * (128 * 16) + r * 16;
-        tc::sts128(dst, o[0], o[1], o[2], o[3]);
-        tc::sts128(dst + 128 * 16, o[4], o[5], o[6], o[7]);
-      }
-      TbWindows<S + 1, NS - 1>::run(W, m_rel, a1, slot0, r, lim);
-    }
-  }
-};
 
 // 16-byte cp.async with zero fill: copies `bytes` (0..16) from src, zeros the rest of the 16
 __device__ __forceinline__ void cp_async16z(uint32_t dst, const void* src, uint32_t bytes) {
@@ -318,6 +282,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   TBP_DECL();
   for (int i = threadIdx.x; i < S::WIMG_B / 16; i += blockDim.x)
     reinterpret_cast<int4*>(smem)[i] = reinterpret_cast<const int4*>(wimg)[i];
+  if constexpr (S::CP)   // every window's constant columns 12..15 = [1, 1, 1, 0] (the copies never touch them)
+    for (int i = threadIdx.x; i < NA * K * 128; i += blockDim.x) {
+      const int b = i / (K * 128), k = (i / 128) % K, row = i % 128;
+      *reinterpret_cast<uint2*>(smem + S::OFF_A1 + b * S::A1_B + (2 * k + 1) * PL + row * 16 + 8) =
+          make_uint2(0x3F803F80u, 0x00003F80u);
+    }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, 4); tc::mbar_init(metaFree + i, 16); }
     for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 8);
@@ -350,7 +320,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
     if (warp == 0 && lane == 0) {
       // ------------------------------------------------ issuer A: layer 1 of every item, B of every tile
-      const uint64_t dW1 = tc::smem_desc(sW1, H * 16, 128);
+      const uint64_t dW1 = tc::smem_desc(sW1, H * 16, 128), dW1o = tc::smem_desc(sW1 + 2 * H * 16, H * 16, 128);
       TbPh trph, d2ph, tph, bfph;
       TBP_NOW(tot0);
       int ct = 0, cs = 0, cK = 0, nL1 = 0;
@@ -419,7 +389,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         }
         TBP_NOW(l0);
         const uint32_t a = sA1 + (uint32_t)(ct % NA) * S::A1_B + (uint32_t)(2 * cs) * PL;
-        tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H, tc::smem_desc(a, PL, 128), dW1, ID_T, 0);
+        tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H, tc::smem_desc(a, PL, 128),
+                       (S::CP && (cs & 1)) ? dW1o : dW1, ID_T, 0);
         tc::mma_commit(done1 + nL1 % 3);
         TBP_ADD(20, l0);
         TBP_CNT(18, 1);
@@ -479,17 +450,22 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       m = (tl < ntiles && p < P) ? (int)(pe >> 16) : 0;
       if (!(tl < ntiles && p < P)) p = -1;
     };
-    // ASYNC: issue tile tl's copies -- the row's valid record bytes into raw buffer rb (zero fill
-    // beyond them), e0 straight into its operand slot (K-major planes) -- and return L_d
-    auto issue = [&](long tl, uint32_t pe, int rb, int es, float (&ldv)[3]) {
+    // CP: issue tile tl's copies into A1 buffer ab and E0 slot es: each valid record by six 4-byte
+    // cp.asyncs into its window (columns 0..11; even slots start at the record and zero-fill the
+    // column after it, odd slots start one halfword early), e0 by 16-byte cp.asyncs into its
+    // K-major planes; returns L_d
+    auto issue = [&](long tl, uint32_t pe, int ab, int es, float (&ldv)[3]) {
       long p; int m;
       decode(tl, pe, p, m);
-      const uint32_t raw = tc::smem_u32(smem + S::OFF_RAW) + rb * S::RAW_B + r * S::RAW_ROW;
-      const char* src = p >= 0 ? reinterpret_cast<const char*>(tbuf + p * (K * 11)) : reinterpret_cast<const char*>(tbuf);
-      const int vb = m * 22;
-#pragma unroll
-      for (int c = 0; c < (K * 22 + 15) / 16; ++c)
-        cp_async16z(raw + 16 * c, src + 16 * c, (uint32_t)min(max(vb - 16 * c, 0), 16));
+      const char* src = reinterpret_cast<const char*>(tbuf + (p >= 0 ? p : 0) * (K * 11));
+      const uint32_t a1 = sA1 + (uint32_t)ab * S::A1_B + r * 16;
+      for (int k = 0; k < m; ++k) {
+        const char* rs = src + 22 * k - 2 * (k & 1);
+        const uint32_t w0 = a1 + (uint32_t)(2 * k) * PL, w1 = w0 + PL;
+        cp_async4z(w0, rs, 4u); cp_async4z(w0 + 4, rs + 4, 4u); cp_async4z(w0 + 8, rs + 8, 4u);
+        cp_async4z(w0 + 12, rs + 12, 4u); cp_async4z(w1, rs + 16, 4u);
+        cp_async4z(w1 + 4, rs + 20, (k & 1) ? 4u : 2u);
+      }
       const uint16_t* es_src = p >= 0 ? e0 + p * C0 : e0;
 #pragma unroll
       for (int j = 0; j < C0 / 8; ++j)
@@ -504,21 +480,22 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     long ntile = ids[1];
     uint32_t npe = perm_of(ntile);
     float ldc[3] = {0.f, 0.f, 0.f};
-    if constexpr (S::ASYNC) {   // tile 0's copies (its operand slots are fresh: slot 0 counts as waited)
+    if constexpr (S::CP) {   // tile 0's copies (its operand slots are fresh: they count as waited)
       if (tile < ntiles) issue(tile, pe, 0, 0, ldc);
       cp_async_commit();
       mfph.flip(0);
+      afph.flip(0);
     }
     TBP_NOW(tot0);
     for (int t = 0;; ++t) {
       const int e = t % NE, a = t % NA;
       uint8_t* M = meta(t);
-      if (tile >= ntiles) {   // end marker (ASYNC: this slot was waited for one iteration ago)
-        if constexpr (!S::ASYNC) tc::mbar_wait(metaFree + e, mfph[e] ^ 1);
+      if (tile >= ntiles) {   // end marker (CP: this slot was waited for one iteration ago)
+        if constexpr (!S::CP) tc::mbar_wait(metaFree + e, mfph[e] ^ 1);
         if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = -1;
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tileReady + e);
-        if constexpr (S::ASYNC) cp_async_wait_all();
+        if constexpr (S::CP) cp_async_wait_all();
         TBP_ADD(7, tot0);
         TBP_FLUSH_IF(r == 0);
         break;
@@ -528,42 +505,23 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       decode(tile, pe, p, m);
       const bool pv = p >= 0;
       float ldv[3] = {0.f, 0.f, 0.f};
-      constexpr int PS = K < 8 ? K : 8;             // slots per repack pass
-      constexpr bool V16 = (K * 22) % 16 == 0;
-      constexpr int NW = V16 ? PS * 11 / 2 : 1;     // words per pass
-      uint32_t W[NW > 1 ? NW : 1];
       uint4 ev[C0 / 8];
-      if constexpr (S::ASYNC) {
-        // the next tile's copies first (its E0 / meta slot: tile t+1-NE's consumers are done), then
-        // this tile's (issued one iteration ago) are waited for
-        float ldn[3];
+      if constexpr (S::CP) {
+        // the next tile's copies first (its E0 / meta slot: tile t+1-NE's consumers are done; its A1
+        // buffer: tile t+1-NA's layer-1 MMAs are done), then this tile's (issued one iteration ago)
+        float ldn[3] = {0.f, 0.f, 0.f};
         TBP_NOW(w0);
         tc::mbar_wait(metaFree + (t + 1) % NE, mfph[(t + 1) % NE] ^ 1); mfph.flip((t + 1) % NE);
         TBP_ADD(5, w0);
-        if (ntile < ntiles) issue(ntile, npe, (t + 1) & 1, (t + 1) % NE, ldn);
+        TBP_NOW(w1);
+        tc::mbar_wait(a1Free + (t + 1) % NA, afph[(t + 1) % NA] ^ 1); afph.flip((t + 1) % NA);
+        TBP_ADD(6, w1);
+        if (ntile < ntiles) issue(ntile, npe, (t + 1) % NA, (t + 1) % NE, ldn);
         cp_async_commit();
         cp_async_wait_1();
 #pragma unroll
         for (int c = 0; c < 3; ++c) { ldv[c] = ldc[c]; ldc[c] = ldn[c]; }
-        const uint32_t raw = tc::smem_u32(smem + S::OFF_RAW) + (t & 1) * S::RAW_B + r * S::RAW_ROW;
-#pragma unroll
-        for (int c = 0; c < NW / 4; ++c) {
-          uint32_t x0, x1, x2, x3;
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(raw + 16 * c));
-          W[4 * c] = x0; W[4 * c + 1] = x1; W[4 * c + 2] = x2; W[4 * c + 3] = x3;
-        }
       } else {
-        // this row's valid records (16-byte loads of the valid prefix only) and e0, L_d
-        const int mv = min(m, PS);
-        if constexpr (V16) {
-          const uint4* src = reinterpret_cast<const uint4*>(tbuf + (pv ? p : 0) * (K * 11));
-          const int nc = (mv * 22 + 15) / 16;
-#pragma unroll
-          for (int c = 0; c < NW / 4; ++c) {
-            const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
-            W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
-          }
-        }
 #pragma unroll
         for (int j = 0; j < C0 / 8; ++j) ev[j] = pv ? tb_ld_nc4(e0 + p * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
         if (pv)
@@ -594,47 +552,41 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         const int* L = const_cast<const int*>(lred) + (t & 1) * 4;
         Kt = max(1, max(max(L[0], L[1]), max(L[2], L[3])));
       }
-      TBP_NOW(w1);
-      tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);       // A1 of tile t-NA
-      TBP_ADD(6, w1);
       TBP_NOW(st0);
-      const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B;
-      if constexpr (V16) {
-        TbWindows<0, PS>::run(W, m, a1, 0, r, Kt);
-        if constexpr (K > 8) {   // second pass: slots 8..15
-          const uint4* src = reinterpret_cast<const uint4*>(tbuf + (pv ? p : 0) * (K * 11) + 8 * 11);
-          const int m2 = m - 8, nc = m2 > 0 ? (m2 * 22 + 15) / 16 : 0;
-#pragma unroll
-          for (int c = 0; c < NW / 4; ++c) {
-            const uint4 v = c < nc ? tb_ld_nc4(src + c) : make_uint4(0, 0, 0, 0);
-            W[4 * c] = v.x; W[4 * c + 1] = v.y; W[4 * c + 2] = v.z; W[4 * c + 3] = v.w;
-          }
-          TbWindows<0, K - 8>::run(W, m2, a1, 8, r, Kt);
+      const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + r * 16;
+      if constexpr (S::CP) {
+        // masked slots the tile's items reach: zero columns 0..11 (the constant columns stay)
+        for (int k = m; k < Kt; ++k) {
+          tc::sts128(a1 + (uint32_t)(2 * k) * PL, 0u, 0u, 0u, 0u);
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a1 + (uint32_t)(2 * k + 1) * PL), "r"(0u), "r"(0u)
+                       : "memory");
         }
-      } else {   // rows not 16-byte aligned in global memory: halfword loads (test shapes)
+      } else {   // halfword loads (K odd: rows not 4-byte aligned); even-slot window layout for all slots
+        TBP_NOW(w1);
+        tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);     // A1 of tile t-NA
+        TBP_ADD(6, w1);
         const uint16_t* src = tbuf + (pv ? p : 0) * (K * 11);
-        for (int s = 0; s < Kt; ++s) {
+        for (int k = 0; k < Kt; ++k) {
           uint32_t w[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) w[k] = 0;
-          if (s < m) {
-            uint32_t h[12];
+          for (int i = 0; i < 8; ++i) w[i] = 0;
+          if (k < m) {
+            uint32_t hv[12];
 #pragma unroll
-            for (int i = 0; i < 11; ++i) h[i] = __ldg(src + 11 * s + i);
-            h[11] = 0x3F80u;
+            for (int i = 0; i < 11; ++i) hv[i] = __ldg(src + 11 * k + i);
+            hv[11] = 0;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) w[k] = h[2 * k] | (h[2 * k + 1] << 16);
-            w[6] = 0x3F803F80u;
+            for (int i = 0; i < 6; ++i) w[i] = hv[2 * i] | (hv[2 * i + 1] << 16);
           }
-          const uint32_t dst = a1 + (uint32_t)(2 * s) * PL + r * 16;
-          tc::sts128(dst, w[0], w[1], w[2], w[3]);
-          tc::sts128(dst + PL, w[4], w[5], w[6], w[7]);
+          w[6] = 0x3F803F80u;   // columns 12, 13 = 1
+          w[7] = 0x00003F80u;   // column 14 = 1, column 15 = 0
+          tc::sts128(a1 + (uint32_t)(2 * k) * PL, w[0], w[1], w[2], w[3]);
+          tc::sts128(a1 + (uint32_t)(2 * k + 1) * PL, w[4], w[5], w[6], w[7]);
         }
-      }
-      if constexpr (!S::ASYNC)
 #pragma unroll
         for (int j = 0; j < C0 / 8; ++j)
           tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[j].x, ev[j].y, ev[j].z, ev[j].w);
+      }
       TBP_ADD(25, st0);
       if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = Kt;
       tc::fence_proxy_async();   // this thread's operand writes (and its waited cp.asyncs) -> async proxy

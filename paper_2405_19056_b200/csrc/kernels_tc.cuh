@@ -53,6 +53,10 @@ struct TcState {
   uint8_t* tb_wimg = nullptr;   // T+B weight image (K-major, no-swizzle planes)
   cudaStream_t sort_st = nullptr;   // the count sort runs here, beside the F encoder
   cudaEvent_t ev_fwd = nullptr, ev_sorted = nullptr;
+  // row tiles: T runs on its own stream right after F0 (it needs no halo), overlapping the rest
+  // of the encoder/decoder and their halo exchanges; the output stage waits for it
+  cudaStream_t tb_st = nullptr;
+  cudaEvent_t ev_e0 = nullptr, ev_tb = nullptr;
   TbParams tb_prm;              // bB, wBn, WO (c0+3 wide), bO (kernel parameters)
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
@@ -117,14 +121,14 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   net->tc_state = s;
   auto rb = [](float v) { return h_bf16f(h_bf16(v)); };
   std::vector<uint8_t> img;
-  // W1 as one K=16 window [H][16]: the record's 11 weights (depth column x 2^-7 when
-  // normalising; bf16-exact), then b1 as three exact bf16 pieces (the record window carries
-  // 1.0 in those columns, kernels_tb_tc.cuh), then zeros
-  {
+  // W1 as K=16 windows [H][16], two variants (kernels_tb_tc.cuh): even = the record's 11 weights
+  // (depth column x 2^-7 when normalising; bf16-exact) at columns 0..10, odd = at columns 1..11;
+  // both: b1 as three exact bf16 pieces at columns 12..14 (the record window carries 1.0 there)
+  for (int v = 0; v < 2; ++v) {
     std::vector<float> w1((size_t)H * 16, 0.f);
     for (int n = 0; n < H; ++n) {
-      for (int i = 0; i < 11; ++i) w1[(size_t)n * 16 + i] = rb(T1W[n * 11 + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
-      split3(T1b[n], w1[(size_t)n * 16 + 11], w1[(size_t)n * 16 + 12], w1[(size_t)n * 16 + 13]);
+      for (int i = 0; i < 11; ++i) w1[(size_t)n * 16 + v + i] = rb(T1W[n * 11 + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
+      split3(T1b[n], w1[(size_t)n * 16 + 12], w1[(size_t)n * 16 + 13], w1[(size_t)n * 16 + 14]);
     }
     pack_kmajor(w1, H, 16, false, img);
   }
@@ -443,6 +447,9 @@ inline void tc_release(glassnet* net) {
   if (s->sched) cudaFree(s->sched);
   if (s->perm) cudaFree(s->perm);
   if (s->sort_st) cudaStreamDestroy(s->sort_st);
+  if (s->tb_st) cudaStreamDestroy(s->tb_st);
+  if (s->ev_e0) cudaEventDestroy(s->ev_e0);
+  if (s->ev_tb) cudaEventDestroy(s->ev_tb);
   if (s->ev_fwd) cudaEventDestroy(s->ev_fwd);
   if (s->ev_sorted) cudaEventDestroy(s->ev_sorted);
   delete s;

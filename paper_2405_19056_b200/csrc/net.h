@@ -40,7 +40,8 @@ namespace gn {
 enum StepKind { ST_PREP = 0, ST_CONV = 1, ST_TB = 2, ST_UP = 3, ST_OUT = 4, ST_EXCH = 5 };
 enum TensorId { TEN_X = 0, TEN_E = 1, TEN_Y = 5, TEN_D = 9, TEN_Z = 13 };   // TEN_E + l, ...
 struct Step { int kind; int idx; };   // CONV: conv slot (l = F_l, 4+l = R_l); UP: level; EXCH: tensor
-int tc_steps(const struct ::glassnet* net, Step* out, int max);
+// tile = true: the row-tile order (T right after F0, on its own stream; see tc_run_step)
+int tc_steps(const struct ::glassnet* net, Step* out, int max, bool tile = false);
 int tc_prepare_tile(struct ::glassnet* net, int nranks, int rank, int row0, int rows);
 int tc_run_step(struct ::glassnet* net, bool tile, const Step& s, const void* gbuf, const void* direct, const void* tbuf,
                 const uint8_t* tcount, float* out, int B, cudaStream_t st);
