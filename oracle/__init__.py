@@ -7,7 +7,10 @@ cpu_baseline / --impl reference legs may import this package.  The product packa
 Parity status per function:
   og_conv3x3  pinned (P2 Toeplitz, P7 identity, P8 stride, torch conv2d)
   og_up2      pinned (P9 constant / ramp closed form / torch interpolate)
-  og_T_pixel  pinned (P1 hand-expanded golden, P3 permutation, P4 garbage, P5 empty, P6 duplicate)
+  og_T_pixel  pinned (P1 hand-expanded golden, P3 permutation, P4 garbage, P5 empty, P6 duplicate);
+              sigma_cond (N1) pinned by P1s (hand-expanded golden with sigma), P15 (zero sigma
+              weights = the unconditioned network, bitwise) and P16 (records with zero weights:
+              every fragment is h(sigma), n = 2 gives exactly 2 h(sigma)) and P10 (torch-fp64)
   og_forward  pinned (P10 torch-fp64 composition, P11 homogeneity, P13 tiles, P14 shift)
 """
 from __future__ import annotations
@@ -35,7 +38,7 @@ def build(force=False):
 class Dims(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("K", ctypes.c_int), ("L", ctypes.c_int),
                 ("c", ctypes.c_int * 4), ("h", ctypes.c_int), ("pool", ctypes.c_int),
-                ("r_takes_ld", ctypes.c_int), ("input_norm", ctypes.c_int)]
+                ("r_takes_ld", ctypes.c_int), ("input_norm", ctypes.c_int), ("sigma_cond", ctypes.c_int)]
 
 
 _P = ctypes.POINTER(ctypes.c_double)
@@ -61,14 +64,15 @@ def lib():
 
 
 def make_dims(H, W, K, widths, t_hidden, levels=None, pool="sum", r_takes_ld=True,
-              input_norm=True) -> Dims:
+              input_norm=True, sigma_cond=False) -> Dims:
     levels = len(widths) if levels is None else levels
     c = (ctypes.c_int * 4)(*(list(widths) + [0] * (4 - len(widths))))
     return Dims(H, W, K, levels, c, t_hidden, 1 if pool == "mean" else 0,
-                1 if r_takes_ld else 0, 1 if input_norm else 0)
+                1 if r_takes_ld else 0, 1 if input_norm else 0, 1 if sigma_cond else 0)
 
 
 def dims_from_cfg(cfg, H=None, W=None, **kw) -> Dims:
+    kw.setdefault("sigma_cond", bool(getattr(cfg, "extra", {}).get("sigma_cond", False)))
     return make_dims(cfg.height if H is None else H, cfg.width if W is None else W,
                      cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool, **kw)
 
@@ -152,13 +156,17 @@ def up2(v, H2, W2):
     return out
 
 
-def T_pixel(d: Dims, W1, b1, W2, b2, records, n):
+def T_pixel(d: Dims, W1, b1, W2, b2, records, n, sigma=None):
+    """tau of one pixel; sigma [c0] = the scene features (used only when d.sigma_cond)."""
     rec = _c64(records)
     assert rec.shape == (d.K, 11)
     W1, b1, W2, b2 = _c64(W1), _c64(b1), _c64(W2), _c64(b2)
+    sg = _c64(np.zeros(max(d.c[0], 1)) if sigma is None else sigma)
+    if d.sigma_cond:
+        assert sigma is not None and sg.shape == (d.c[0],)
     tau = np.zeros(d.h + 1)
     lib().og_T_pixel(ctypes.byref(d), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(rec),
-                     int(n), _ptr(tau))
+                     int(n), _ptr(sg), _ptr(tau))
     return tau
 
 
@@ -174,7 +182,7 @@ def split_weights(d: Dims, weights):
         out[name] = w[p:p + n].reshape(shape)
         p += n
 
-    take("T1.W", (h, 11)); take("T1.b", (h,)); take("T2.W", (h, h)); take("T2.b", (h,))
+    take("T1.W", (h, 11 + (c[0] if d.sigma_cond else 0))); take("T1.b", (h,)); take("T2.W", (h, h)); take("T2.b", (h,))
     cin = 15
     for l in range(L):
         take(f"F{l}.W", (c[l], 3, 3, cin)); take(f"F{l}.b", (c[l],)); cin = c[l]

@@ -11,7 +11,10 @@
  *                  which presumes bounded inputs).
  *   2. F (scene encoder): e0 = ReLU(conv3x3_s1(x)), e_l = ReLU(conv3x3_s2(e_{l-1})).
  *   3. T (Eq. eq:SymmetricNN): tau = g(h(b_1),...,h(b_t)) = sum_i h(b_i), h a
- *      shared 2-layer ReLU MLP over each VALID fragment record (k < min(n,K)); the sum is
+ *      shared 2-layer ReLU MLP over each VALID fragment record (k < min(n,K)) -- or, with
+ *      sigma_cond (the paper's literal h(b_i, sigma), "sigma is a
+ *      scene representation"), over the concatenation [b_i ; sigma], sigma = e0 at the pixel
+ *      (the scene encoder's level-0 features, reading N1); the sum is
  *      taken per channel over the values sorted ascending (a pure function of the
  *      multiset -> exactly permutation invariant, table:OrderLoss P:666-679);
  *      tau = [sum, n] (or [sum/n, n] in mean mode, 0 when n = 0).
@@ -37,6 +40,7 @@ typedef struct {
   int pool;        /* 0 = sum, 1 = mean                         */
   int r_takes_ld;  /* 1: output 1x1 takes [d0; L_d] (reading R15) */
   int input_norm;  /* 1: power-of-two input normalisation (R9)    */
+  int sigma_cond;  /* 1: h(b, sigma), sigma = e0 at the pixel (N1) */
 } og_dims;
 
 typedef struct {        /* optional per-layer dumps (any pointer may be NULL) */
@@ -59,7 +63,7 @@ static int lvl_size(int n, int l) { /* ceil(n / 2^l) */
 size_t og_weight_count(const og_dims* d) {
   size_t n = 0;
   int h = d->h;
-  n += (size_t)h * 11 + h;                 /* T1 */
+  n += (size_t)h * (11 + (d->sigma_cond ? d->c[0] : 0)) + h;   /* T1 */
   n += (size_t)h * h + h;                  /* T2 */
   int cin = 15;
   for (int l = 0; l < d->L; ++l) { n += (size_t)d->c[l] * 9 * cin + d->c[l]; cin = d->c[l]; }
@@ -123,10 +127,13 @@ static int cmp_double(const void* a, const void* b) {
 }
 
 /* T for one pixel (Eq. eq:SymmetricNN; readings R2-R7).
- * rec: [K][11] raw records; n: valid count (clamped to K); tau_out: [h+1]. */
+ * rec: [K][11] raw records; n: valid count (clamped to K); sigma: [c0] scene features at the
+ * pixel (used only with d->sigma_cond: layer 1 then takes [record ; sigma], W1 [h][11 + c0]);
+ * tau_out: [h+1]. */
 void og_T_pixel(const og_dims* d, const double* W1, const double* b1, const double* W2,
-                const double* b2, const double* rec, int n, double* tau_out) {
+                const double* b2, const double* rec, int n, const double* sigma, double* tau_out) {
   int h = d->h, K = d->K;
+  const int ns = d->sigma_cond ? d->c[0] : 0, nin = 11 + ns;
   int m = n < K ? n : K;
   double* a2 = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1) * h);
   double* a1 = (double*)malloc(sizeof(double) * (size_t)h);
@@ -135,9 +142,10 @@ void og_T_pixel(const og_dims* d, const double* W1, const double* b1, const doub
     double r[11];
     for (int i = 0; i < 11; ++i) r[i] = rec[(size_t)k * 11 + i];
     if (d->input_norm) r[7] = r[7] * 0x1p-7;            /* record depth (R9) */
-    for (int o = 0; o < h; ++o) {                        /* h layer 1 */
+    for (int o = 0; o < h; ++o) {                        /* h layer 1 over [b ; sigma] */
       double acc = b1[o];
-      for (int i = 0; i < 11; ++i) acc += W1[(size_t)o * 11 + i] * r[i];
+      for (int i = 0; i < 11; ++i) acc += W1[(size_t)o * nin + i] * r[i];
+      for (int j = 0; j < ns; ++j) acc += W1[(size_t)o * nin + 11 + j] * sigma[j];
       a1[o] = relu(acc);
     }
     for (int o = 0; o < h; ++o) {                        /* h layer 2 */
@@ -169,7 +177,7 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
 
   /* ---- unpack the weight blob (SURVEY.md §8(b) order) ---- */
   const double* p = wts;
-  const double *T1W = p; p += (size_t)h * 11; const double* T1b = p; p += h;
+  const double *T1W = p; p += (size_t)h * (11 + (d->sigma_cond ? c[0] : 0)); const double* T1b = p; p += h;
   const double *T2W = p; p += (size_t)h * h;  const double* T2b = p; p += h;
   const double *FW[4], *Fb[4];
   int cin = 15;
@@ -205,7 +213,8 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
   /* ---- 3. T ---- */
   double* tau = (double*)malloc(sizeof(double) * P * (h + 1));
   for (size_t q = 0; q < P; ++q)
-    og_T_pixel(d, T1W, T1b, T2W, T2b, tbuf + q * (size_t)K * 11, (int)tcount[q], tau + q * (h + 1));
+    og_T_pixel(d, T1W, T1b, T2W, T2b, tbuf + q * (size_t)K * 11, (int)tcount[q], e[0] + q * c[0],
+               tau + q * (h + 1));
   /* ---- 4. B ---- */
   double* phi = (double*)malloc(sizeof(double) * P * c[0]);
   for (size_t q = 0; q < P; ++q)

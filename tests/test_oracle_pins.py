@@ -159,6 +159,9 @@ def torch_forward(dims, wts, g, dr, tb, n):
     rs = torch.ones(11, dtype=torch.float64)
     rs[7] = 1 / 128
     rec = tb * rs
+    if dims.sigma_cond:   # N1: h's input is [record ; e0 at the pixel]
+        sig = e[0][0].permute(1, 2, 0)[:, :, None, :].expand(-1, -1, dims.K, -1)
+        rec = torch.cat([rec, sig], -1)
     m = torch.from_numpy(np.minimum(n.astype(np.int64), dims.K))
     mask = torch.arange(dims.K)[None, None, :] < m[..., None]
     a1 = Fnn.relu(rec @ wd["T1.W"].T + wd["T1.b"])
@@ -303,3 +306,78 @@ def test_R5_pool_fixed_point_range():
     assert tau[64] == 1.0
     print(f"max per-fragment a2 over {recs.shape[0] // 3 * 16} records: {amax:.3f} (saturation 2048)")
     assert 0.0 < amax < 2048.0 / 16
+
+
+# ----------------------------------------------------------------------------- N1: h(b, sigma)
+def test_P1s_T_pixel_sigma_hand_expanded():
+    """N1: the paper's literal h(b_i, sigma) (Eq. eq:SymmetricNN), layer 1
+    over [record ; sigma]; a hand-expanded single pixel (tests/golden/p1s_T_pixel_sigma.json)."""
+    g = json.load(open(os.path.join(GOLDEN, "p1s_T_pixel_sigma.json")))
+    for pool, key in (("sum", "tau_sum"), ("mean", "tau_mean")):
+        d = oracle.make_dims(1, 1, g["K"], (g["c0"], 4, 8), g["h"], pool=pool, input_norm=False, sigma_cond=True)
+        tau = oracle.T_pixel(d, g["W1"], g["b1"], g["W2"], g["b2"], g["records"], 2, sigma=g["sigma"])
+        assert list(tau) == g[key], (pool, tau)
+    d = oracle.make_dims(1, 1, g["K"], (g["c0"], 4, 8), g["h"], input_norm=False, sigma_cond=True)
+    assert list(oracle.T_pixel(d, g["W1"], g["b1"], g["W2"], g["b2"], g["records"], 1, sigma=g["sigma"])) == g["tau_n1"]
+    assert list(oracle.T_pixel(d, g["W1"], g["b1"], g["W2"], g["b2"], g["records"], 2, sigma=[0, 0])) == g["tau_sigma0"]
+
+
+def _sigma_blob(widths, h, levels, zero_sigma_cols=False, zero_record_cols=False, seed=0):
+    w = synth.make_weights(widths, levels, h, seed=seed, sigma_cond=True).astype(np.float64)
+    c0 = widths[0]
+    T1 = w[:h * (11 + c0)].reshape(h, 11 + c0)
+    if zero_sigma_cols:
+        T1[:, 11:] = 0.0
+    if zero_record_cols:
+        T1[:, :11] = 0.0
+    return w
+
+
+def test_P15_sigma_cond_with_zero_sigma_weights_is_the_unconditioned_network():
+    """N1 reduces to the pinned network: with the sigma columns of T1.W zero, the sigma-conditioned
+    forward equals the unconditioned forward (same remaining weights) bitwise."""
+    widths, h, L = (16, 32, 64), 32, 3
+    cfg = synth.Config("s", 20, 24, 1, 4, L, widths, h, "fp32")
+    fr = synth.gen_frames(cfg, seed=2)
+    g, dr, tb, n = fr.as64()
+    ws = _sigma_blob(widths, h, L, zero_sigma_cols=True)
+    T1 = ws[:h * (11 + widths[0])].reshape(h, 11 + widths[0])
+    wu = np.concatenate([T1[:, :11].reshape(-1), ws[h * (11 + widths[0]):]])
+    ds = oracle.make_dims(20, 24, 4, widths, h, sigma_cond=True)
+    du = oracle.make_dims(20, 24, 4, widths, h)
+    assert oracle.weight_count(ds) == ws.size and oracle.weight_count(du) == wu.size
+    a = oracle.forward(ds, ws, g[0], dr[0], tb[0], n[0])
+    b = oracle.forward(du, wu, g[0], dr[0], tb[0], n[0])
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_P16_sigma_only_fragments():
+    """N1: with the record columns of T1.W zero every valid fragment gives the same h(sigma), so a
+    pixel with n = 2 pools exactly 2 h(sigma) whatever its records, and sigma changes tau."""
+    widths, h = (16, 32, 64), 32
+    w = _sigma_blob(widths, h, 3, zero_record_cols=True)
+    dims = oracle.make_dims(1, 1, 4, widths, h, sigma_cond=True)
+    wd = oracle.split_weights(dims, w)
+    rng2 = np.random.default_rng(3)
+    sigma = rng2.uniform(0, 2, 16)
+    rec_a, rec_b = rng2.standard_normal((4, 11)), rng2.standard_normal((4, 11))
+    one = oracle.T_pixel(dims, wd["T1.W"], wd["T1.b"], wd["T2.W"], wd["T2.b"], rec_a, 1, sigma=sigma)
+    two = oracle.T_pixel(dims, wd["T1.W"], wd["T1.b"], wd["T2.W"], wd["T2.b"], rec_b, 2, sigma=sigma)
+    assert np.array_equal(two[:h], 2.0 * one[:h]) and two[h] == 2.0
+    other = oracle.T_pixel(dims, wd["T1.W"], wd["T1.b"], wd["T2.W"], wd["T2.b"], rec_a, 1, sigma=sigma + 0.5)
+    assert not np.array_equal(other[:h], one[:h])
+
+
+@pytest.mark.parametrize("H,W,K,widths,h", [(20, 24, 4, (16, 32, 64), 32), (16, 24, 8, (16, 16, 32, 32), 16)])
+def test_P10s_sigma_forward_equals_torch_composition(H, W, K, widths, h):
+    """P10 for N1: the sigma-conditioned oracle forward == an independent torch-fp64 composition in
+    which h's layer 1 reads [record ; e0 at the pixel] (<= 1e-12)."""
+    cfg = synth.Config("t", H, W, 1, K, len(widths), tuple(widths), h, "fp32")
+    fr = synth.gen_frames(cfg, seed=4)
+    g, dr, tb, n = fr.as64()
+    wts = synth.make_weights(widths, len(widths), h, seed=0, sigma_cond=True).astype(np.float64)
+    dims = oracle.make_dims(H, W, K, widths, h, sigma_cond=True)
+    out, dump = oracle.forward(dims, wts, g[0], dr[0], tb[0], n[0], dump=True)
+    ref, tau = torch_forward(dims, wts, g[0], dr[0], tb[0], n[0])
+    np.testing.assert_allclose(dump["tau"], tau, rtol=1e-13, atol=1e-12)
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-12)
