@@ -46,17 +46,19 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--weak", action="store_true", help="every rank runs the full 32-frame batch")
     ap.add_argument("--no-extra", action="store_true", help="skip the c1/c2 lines and the batch sweep")
+    ap.add_argument("--sigma-cond", action="store_true",
+                    help="SURVEY §8(f) N1: h(b, sigma) (layer 1 over [record ; e0]); not the headline network")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------------------- helpers
-def alg_flops_per_frame(cfg, mean_n):
+def alg_flops_per_frame(cfg, mean_n, sigma_cond=False):
     """Algorithmic FLOPs per frame (valid fragments only, unpadded)."""
     H, W = cfg.height, cfg.width
     c, h, L = cfg.widths, cfg.t_hidden, cfg.levels
     P = H * W
     macs = {}
-    macs["T"] = P * mean_n * (11 * h + h * h)
+    macs["T"] = P * mean_n * ((11 + (c[0] if sigma_cond else 0)) * h + h * h)
     macs["F0"] = P * 9 * 15 * c[0]
     for l in range(1, L):
         macs[f"F{l}"] = (P >> (2 * l)) * 9 * c[l - 1] * c[l]
@@ -268,9 +270,10 @@ def run_ours(args):
         if B < 1:
             raise SystemExit(f"{world} ranks for a {cfg.batch}-frame batch")
     H, W, K = cfg.height, cfg.width, cfg.k_slots
-    w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True)
+    w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True,
+                           sigma_cond=args.sigma_cond)
     dims = make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, precision=cfg.precision, max_batch=B,
-                     pool=cfg.pool)
+                     pool=cfg.pool, sigma_cond=args.sigma_cond)
     net = GlassNet(w, dims)
     net.set_kernel_family(args.family == "tc")
     stream = torch.cuda.current_stream()
@@ -318,12 +321,12 @@ def run_ours(args):
     # per-stage times (events after every launch, same stream; a second pass of K steps)
     # (a row tile also builds x16 for its halo exchange: one more launch than the full frame)
     launches = net.launches_per_forward(B) + (1 if tiles_mode and args.family == "tc" else 0)
-    net.profile_begin((launches + 1) * args.steps + 2)   # + the start mark of each forward
+    net.profile_begin((launches + 3) * args.steps + 2)   # + start marks (a row tile restarts around T's stream)
     for _ in range(args.steps):
         run()
     stages = net.profile_end()
     torch.cuda.synchronize()
-    flops = alg_flops_per_frame(cfg, mean_n)
+    flops = alg_flops_per_frame(cfg, mean_n, args.sigma_cond)
     if tiles_mode:   # this rank's share of the frame
         flops = {k: v * rows / H for k, v in flops.items()}
     step_ms = sum(v[0] for v in stages.values()) / args.steps
@@ -416,6 +419,7 @@ def run_ours(args):
             cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, batch {frames_per_step} frames, n~U{{0..{K}}}",
                     "frames_per_gpu": B, "global_batch": frames_per_step, "parallelism": f"dp{world} (frames)",
                     "kernel_family": args.family, "l2": "inputs (13.7 GB/rank) larger than L2; no flush",
+                    "sigma_cond": args.sigma_cond,
                     "mean_valid_fragments": mean_n}
             metric = METRIC
         line = {"metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,

@@ -31,7 +31,10 @@
  *
  * Weights: one little-endian fp32 host blob, in this order (conv weights OHWI,
  * cross-correlation, tap (ky,kx) reads offset (ky-1,kx-1)):
- *   T1.W[h][11] T1.b[h] T2.W[h][h] T2.b[h]
+ *   T1.W[h][11] T1.b[h] T2.W[h][h] T2.b[h]   (GLASSNET_FLAG_SIGMA_COND: T1.W[h][11 + c0] --
+ *                                             the paper's h(b_i, sigma), Eq. eq:SymmetricNN
+ *                                             P:308-316, layer 1 over [record ; e0 at the
+ *                                             pixel])
  *   F0.W[c0][3][3][15] F0.b ... F_{L-1}.W[c_{L-1}][3][3][c_{L-2}] F_{L-1}.b
  *   B.W[c0][c0+h+1] B.b[c0]                 concat order [e0, tau_sum, n]
  *   R_{L-1}.W[c_{L-2}][3][3][c_{L-1}] R_{L-1}.b ... R_1.W[c0][3][3][c1] R_1.b
@@ -60,7 +63,8 @@ enum { GLASSNET_OK = 0, GLASSNET_ERR_INVALID_ARGUMENT = 1, GLASSNET_ERR_UNSUPPOR
 enum { GLASSNET_BF16 = 0, GLASSNET_FP32 = 1 };          /* storage + math mode         */
 enum { GLASSNET_POOL_SUM = 0, GLASSNET_POOL_MEAN = 1 };  /* g of Eq. eq:SymmetricNN     */
 enum { GLASSNET_FLAG_R_TAKES_LD = 1u << 0,               /* reading R15, default on     */
-       GLASSNET_FLAG_INPUT_NORM = 1u << 1 };             /* reading R9, default on      */
+       GLASSNET_FLAG_INPUT_NORM = 1u << 1,               /* reading R9, default on      */
+       GLASSNET_FLAG_SIGMA_COND = 1u << 2 };             /* N1, default off: h(b, sigma) */
 
 typedef struct glassnet* glassnet_t;
 typedef struct glassnet_comm* glassnet_comm_t;

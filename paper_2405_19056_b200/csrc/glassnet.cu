@@ -73,7 +73,8 @@ extern "C" size_t glassnet_weight_count(const glassnet_dims* d) {
   if (validate_dims(d) != GLASSNET_OK) return 0;
   const int h = d->t_hidden, L = d->levels;
   const int* c = d->widths;
-  size_t n = (size_t)h * 11 + h + (size_t)h * h + h;
+  const int nin = 11 + ((d->flags & GLASSNET_FLAG_SIGMA_COND) ? d->widths[0] : 0);   // N1: [record ; e0]
+  size_t n = (size_t)h * nin + h + (size_t)h * h + h;
   int cin = 15;
   for (int l = 0; l < L; ++l) { n += (size_t)c[l] * 9 * cin + c[l]; cin = c[l]; }
   n += (size_t)c[0] * (c[0] + h + 1) + c[0];
@@ -131,7 +132,9 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   // ---- parse the blob (documented order) ----
   const float* p = weights;
   std::vector<const float*> FW(L), Fb(L), RW(L), Rb(L);
-  const float *T1W = p; p += (size_t)h * 11; const float* T1b = p; p += h;
+  const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
+  const int nin = 11 + (sig ? c[0] : 0);
+  const float *T1W = p; p += (size_t)h * nin; const float* T1b = p; p += h;
   const float *T2W = p; p += (size_t)h * h; const float* T2b = p; p += h;
   int cin = 15;
   for (int l = 0; l < L; ++l) { FW[l] = p; p += (size_t)c[l] * 9 * cin; Fb[l] = p; p += c[l]; cin = c[l]; }
@@ -143,7 +146,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
 
   // ---- SIMT packs ----
   std::vector<float> tb;
-  for (int i = 0; i < h * 11; ++i) tb.push_back(W(T1W[i]));
+  for (int i = 0; i < h * nin; ++i) tb.push_back(W(T1W[i]));
   for (int i = 0; i < h; ++i) tb.push_back(T1b[i]);
   for (int i = 0; i < h * h; ++i) tb.push_back(W(T2W[i]));
   for (int i = 0; i < h; ++i) tb.push_back(T2b[i]);
@@ -303,13 +306,14 @@ static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* 
   for (int l = 1; l < L; ++l) conv(e[l - 1], l - 1, c[l - 1], l, c[l], 2, e[l], 0);
   {  // T + B + psi
     const int NB = c[0] + h + 1, NO = c[0] + (ld ? 3 : 0);
-    const size_t smem = sizeof(float) * (h * 11 + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3);
+    const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
+    const size_t smem = sizeof(float) * (h * (11 + (sig ? c[0] : 0)) + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3);
     const unsigned g = nblk(P0, 128);
 #define TB_LAUNCH(HH, CC)                                                                              \
   {                                                                                                    \
     auto kfn = gn::k_tb_simt<T, HH, CC>;                                                               \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                \
-    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e[0], direct, net->w_tb, net->psi, P0, K, d.pool, ld, norm); \
+    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e[0], direct, net->w_tb, net->psi, P0, K, d.pool, ld, norm, sig ? 1 : 0); \
   }
     if (h == 64 && c[0] == 32) TB_LAUNCH(64, 32)
     else if (h == 64 && c[0] == 16) TB_LAUNCH(64, 16)

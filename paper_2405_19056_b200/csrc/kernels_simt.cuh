@@ -136,19 +136,20 @@ __device__ __forceinline__ bool rec_less(const T* a, const T* b) {
 //   tau = [sum over valid fragments (canonical order) of h(b), m]  (Eq. eq:SymmetricNN)
 //   phi = ReLU(W_B [e0; tau] + b_B)
 //   psi = W_O[:, :c0] phi + W_O[:, c0:] L_d + b_O                    (reading R15)
-// wts (fp32): W1[H][11] b1[H] W2[H][H] b2[H] WB[C0][C0+H+1] bB[C0] WO[3][NO] bO[3]
+// wts (fp32): W1[H][NIN] b1[H] W2[H][H] b2[H] WB[C0][C0+H+1] bB[C0] WO[3][NO] bO[3],
+// NIN = 11 (+ C0 with sigma, N1: h's layer 1 over [record ; e0 at the pixel])
 template <typename T, int H, int C0>
 __global__ void __launch_bounds__(128) k_tb_simt(
     const T* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const T* __restrict__ e0,
     const T* __restrict__ direct, const float* __restrict__ wts, float* __restrict__ psi,
-    long P, int K, int pool, int r_takes_ld, int norm) {
+    long P, int K, int pool, int r_takes_ld, int norm, int sigma) {
   extern __shared__ float sw[];
-  const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0);
-  const int nw = H * 11 + H + H * H + H + C0 * NB + C0 + 3 * NO + 3;
+  const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0), NIN = 11 + (sigma ? C0 : 0);
+  const int nw = H * NIN + H + H * H + H + C0 * NB + C0 + 3 * NO + 3;
   for (int i = threadIdx.x; i < nw; i += blockDim.x) sw[i] = wts[i];
   __syncthreads();
   const float* W1 = sw;
-  const float* b1 = W1 + H * 11;
+  const float* b1 = W1 + H * NIN;
   const float* W2 = b1 + H;
   const float* b2 = W2 + H * H;
   const float* WB = b2 + H;
@@ -168,6 +169,19 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     while (j > 0 && rec_less(rec + k * 11, rec + idx[j - 1] * 11)) { idx[j] = idx[j - 1]; --j; }
     idx[j] = k;
   }
+  float ev[C0];
+#pragma unroll
+  for (int i = 0; i < C0; i += 8) load8(e0 + p * C0 + i, ev + i);
+  // the layer-1 part every fragment of the pixel shares: b1 (+ W1,sigma e0 with N1)
+  float u1[H];
+#pragma unroll
+  for (int o = 0; o < H; ++o) {
+    float a = b1[o];
+    if (sigma)
+#pragma unroll
+      for (int j = 0; j < C0; ++j) a = fmaf(W1[o * NIN + 11 + j], ev[j], a);
+    u1[o] = a;
+  }
   float s[H];
 #pragma unroll
   for (int o = 0; o < H; ++o) s[o] = 0.f;
@@ -180,9 +194,9 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     float a1[H];
 #pragma unroll
     for (int o = 0; o < H; ++o) {
-      float a = b1[o];
+      float a = u1[o];
 #pragma unroll
-      for (int i = 0; i < 11; ++i) a = fmaf(W1[o * 11 + i], x[i], a);
+      for (int i = 0; i < 11; ++i) a = fmaf(W1[o * NIN + i], x[i], a);
       a1[o] = relu(a);
     }
 #pragma unroll 4
@@ -197,9 +211,6 @@ __global__ void __launch_bounds__(128) k_tb_simt(
 #pragma unroll
     for (int o = 0; o < H; ++o) s[o] = __fdiv_rn(s[o], (float)m);
   }
-  float ev[C0];
-#pragma unroll
-  for (int i = 0; i < C0; i += 8) load8(e0 + p * C0 + i, ev + i);
   float ld[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) ld[i] = to_f(direct[p * 3 + i]);

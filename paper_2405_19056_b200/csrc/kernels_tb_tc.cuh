@@ -88,6 +88,7 @@ struct TbParams {
   float WO[3 * 35];      // [3][C0+3]: output 1x1 over [d0 ; L_d] (L_d part zero if R does not take it)
   float bO[4];
   float b2s[64];         // b2 2^-11 (the pool's FADD.SAT addend)
+  int sigma;             // N1: layer 1 also reads e0 at the pixel (W1,sigma)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -179,8 +180,10 @@ struct TbLayout {
   static constexpr int W2_B = H * H * 2;
   static constexpr int WBE_B = C0 * C0 * 2;
   static constexpr int WBT_B = C0 * H * 2;            // f16
-  static constexpr int WIMG_B = W1_B + W2_B + WBE_B + WBT_B;
+  static constexpr int W1E_B = H * C0 * 2;            // N1: W1's sigma part [C0/8 planes][H][8]
+  static constexpr int WIMG_B = W1_B + W2_B + WBE_B + WBT_B + W1E_B;
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBE = OFF_W2 + W2_B, OFF_WBT = OFF_WBE + WBE_B;
+  static constexpr int OFF_W1E = OFF_WBT + WBT_B;
   // per-tile meta: pixel ids, counts, L_d (E2's psi needs them one tile late), Kt
   static constexpr int M_PIX = 0, M_LD = 128 * 8, M_CNT = M_LD + 128 * 12, M_KT = M_CNT + 128, META_B = M_KT + 16;
   // CP (K even, so every row's records start 4-byte aligned): each record is copied by 4-byte
@@ -314,6 +317,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     // layer 2 of item j-3 (its previous reader) has COMPLETED (done2 commit).
     const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
     const uint32_t sWBE = tc::smem_u32(smem + S::OFF_WBE), sWBT = tc::smem_u32(smem + S::OFF_WBT);
+    const uint32_t sW1E = tc::smem_u32(smem + S::OFF_W1E);
     const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
     constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
     constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
@@ -391,6 +395,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         const uint32_t a = sA1 + (uint32_t)(ct % NA) * S::A1_B + (uint32_t)(2 * cs) * PL;
         tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H, tc::smem_desc(a, PL, 128),
                        (S::CP && (cs & 1)) ? dW1o : dW1, ID_T, 0);
+        if (prm.sigma)   // N1: + e0 W1,sigma^T, the same two MMAs for every slot of the pixel
+#pragma unroll
+          for (int q = 0; q < C0 / 16; ++q)
+            tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H,
+                           tc::smem_desc(sE0 + (uint32_t)(ct % NE) * S::E0_B + 2 * q * PL, PL, 128),
+                           tc::smem_desc(sW1E + 2 * q * H * 16, H * 16, 128), ID_T, 1);
         tc::mma_commit(done1 + nL1 % 3);
         TBP_ADD(20, l0);
         TBP_CNT(18, 1);

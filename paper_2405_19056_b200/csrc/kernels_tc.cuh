@@ -124,10 +124,12 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   // W1 as K=16 windows [H][16], two variants (kernels_tb_tc.cuh): even = the record's 11 weights
   // (depth column x 2^-7 when normalising; bf16-exact) at columns 0..10, odd = at columns 1..11;
   // both: b1 as three exact bf16 pieces at columns 12..14 (the record window carries 1.0 there)
+  const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
+  const int nin = 11 + (sig ? C0 : 0);   // N1: T1.W rows are [record weights ; sigma weights]
   for (int v = 0; v < 2; ++v) {
     std::vector<float> w1((size_t)H * 16, 0.f);
     for (int n = 0; n < H; ++n) {
-      for (int i = 0; i < 11; ++i) w1[(size_t)n * 16 + v + i] = rb(T1W[n * 11 + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
+      for (int i = 0; i < 11; ++i) w1[(size_t)n * 16 + v + i] = rb(T1W[n * nin + i]) * ((norm && i == 7) ? 0.0078125f : 1.f);
       split3(T1b[n], w1[(size_t)n * 16 + 12], w1[(size_t)n * 16 + 13], w1[(size_t)n * 16 + 14]);
     }
     pack_kmajor(w1, H, 16, false, img);
@@ -146,6 +148,14 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   }
   pack_kmajor(wbe, C0, C0, false, img);
   pack_kmajor(wbt, C0, H, true, img);   // f16: tau is an f16 operand (reading R19)
+  {   // N1: W1's sigma part [H][C0] (layer 1 += e0 W1,sigma^T: two more MMAs per item from the
+      // tile's e0 operand); zeros (and unused) without GLASSNET_FLAG_SIGMA_COND
+    std::vector<float> w1e((size_t)H * C0, 0.f);
+    if (sig)
+      for (int n = 0; n < H; ++n)
+        for (int j = 0; j < C0; ++j) w1e[(size_t)n * C0 + j] = rb(T1W[n * nin + 11 + j]);
+    pack_kmajor(w1e, H, C0, false, img);
+  }
   TbParams& prm = s->tb_prm;
   memset(&prm, 0, sizeof prm);
   for (int o = 0; o < C0; ++o) prm.bB[o] = Bb[o];
@@ -155,6 +165,7 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
     for (int i = 0; i < C0 + 3; ++i) prm.WO[j * (C0 + 3) + i] = i < NO ? rb(OW[(size_t)j * NO + i]) : 0.f;
   for (int j = 0; j < 3; ++j) prm.bO[j] = Ob[j];
   for (int o = 0; o < H; ++o) prm.b2s[o] = T2b[o] * TB_VSCALE;
+  prm.sigma = sig ? 1 : 0;
   s->perm_cap = ((long)d.max_batch * d.height * d.width + TB_SBP - 1) / TB_SBP * TB_SBP;
   if (cudaMalloc(&s->tb_wimg, img.size()) != cudaSuccess || cudaMalloc(&s->sched, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&s->perm, s->perm_cap * sizeof(uint32_t)) != cudaSuccess)

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("GN_LIB", os.path.join(_HERE, "libglassnet.so"))   # G
 GLASSNET_ABI_VERSION = 1
 BF16, FP32 = 0, 1
 POOL_SUM, POOL_MEAN = 0, 1
-FLAG_R_TAKES_LD, FLAG_INPUT_NORM = 1, 2
+FLAG_R_TAKES_LD, FLAG_INPUT_NORM, FLAG_SIGMA_COND = 1, 2, 4
 ERRORS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CUDA", 4: "NCCL", 5: "OUT_OF_MEMORY"}
 
 EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glassnet_forward_host",
@@ -99,10 +99,11 @@ def _check(rc):
 
 
 def make_dims(height, width, k_slots, widths, t_hidden, levels=None, precision="bf16", max_batch=1,
-              pool="sum", r_takes_ld=True, input_norm=True) -> Dims:
+              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False) -> Dims:
     levels = len(widths) if levels is None else levels
     w = (ctypes.c_int32 * 4)(*(list(widths)[:levels] + [0] * (4 - levels)))
-    flags = (FLAG_R_TAKES_LD if r_takes_ld else 0) | (FLAG_INPUT_NORM if input_norm else 0)
+    flags = ((FLAG_R_TAKES_LD if r_takes_ld else 0) | (FLAG_INPUT_NORM if input_norm else 0)
+             | (FLAG_SIGMA_COND if sigma_cond else 0))
     return Dims(GLASSNET_ABI_VERSION, height, width, max_batch, k_slots, levels, w, t_hidden,
                 BF16 if precision == "bf16" else FP32, POOL_MEAN if pool == "mean" else POOL_SUM, flags)
 

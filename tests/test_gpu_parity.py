@@ -21,6 +21,7 @@ def _cfg(name, H, W, B, K, prec, net=None, **kw):
     return synth.Config(name, H, W, B, K, n["levels"], n["widths"], n["t_hidden"], prec, **kw)
 
 
+
 def _run(cfg, fr, family=None, net=None):
     import torch
     net = net or net_for(cfg)
@@ -257,3 +258,69 @@ def test_output_guard_bands(cuda_ok):
         assert bool((head == 0x7FC01234).all()) and bool((tail == 0x7FC04321).all()), (H, W, B, K)
         assert bool(torch.isfinite(out).all())
         net.close()
+
+
+# ------------------------------------------------------------------ N1: sigma-conditioned h
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("H,W,K,B", [(40, 136, 8, 2), (32, 72, 16, 1), (24, 48, 3, 1)])
+def test_sigma_cond_bf16_parity(cuda_ok, family, H, W, K, B):
+    """SURVEY §8(f) N1 (the paper's h(b_i, sigma), sigma = e0 at the pixel): both kernel
+    families vs the sigma-conditioned oracle, bf16 tolerance."""
+    cfg = _cfg("sg", H, W, B, K, "bf16", extra={"sigma_cond": True})
+    fr = synth.gen_frames(cfg)
+    out, _ = _run(cfg, fr, family)
+    w = weights_for(cfg)
+    for b in range(B):
+        mx, mean = errs(out[b], oracle_full(cfg, w, fr, b))
+        print(f"N1 {family} {H}x{W} K={K} frame {b}: max {mx:.3e} mean {mean:.3e}")
+        assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1]
+
+
+def test_sigma_cond_fp32_check_mode(cuda_ok):
+    """N1 in the fp32 check mode (c0 network): max abs <= 1e-4 vs the oracle."""
+    cfg = synth.Config("sg32", 64, 64, 1, 4, 3, (16, 32, 64), 32, "fp32", extra={"sigma_cond": True})
+    fr = synth.gen_frames(cfg)
+    out, _ = _run(cfg, fr)
+    mx, _ = errs(out[0], oracle_full(cfg, weights_for(cfg), fr))
+    print(f"N1 fp32: max {mx:.3e}")
+    assert mx <= FP32_TOL
+
+
+def test_sigma_cond_every_record_in_every_slot(cuda_ok):
+    """N1 keeps bit-exact slot invariance: all K cyclic rotations of full pixels give bitwise the same
+    psi (the sigma MMAs are the same for every slot of a pixel)."""
+    import torch
+    from synth import device
+    K = 8
+    cfg = _cfg("sgr", 128, 256, 2, K, "bf16", extra={"sigma_cond": True})
+    net = net_for(cfg)
+    g, d, t, n = device.alloc_and_fill(cfg, seed=5)
+    n.fill_(K)
+    net.forward(g, d, t, n)
+    psi0 = net.debug_psi(cfg.batch).clone()
+    for k in range(1, K):
+        net.forward(g, d, torch.roll(t, shifts=k, dims=3).contiguous(), n)
+        psi = net.debug_psi(cfg.batch)
+        torch.cuda.synchronize()
+        assert torch.equal(psi.view(torch.int32), psi0.view(torch.int32)), k
+    net.close()
+
+
+def test_full_frame_c1_sigma_cond(cuda_ok):
+    """N1 at configs[1] size, every pixel of all 4 frames vs the banded oracle."""
+    import torch
+    from synth import device
+    c = synth.CONFIGS["c1"]
+    cfg = synth.Config("c1s", c.height, c.width, c.batch, c.k_slots, c.levels, c.widths, c.t_hidden, "bf16",
+                       extra={"sigma_cond": True})
+    net = net_for(cfg)
+    g, d, t, n = device.alloc_and_fill(cfg)
+    out = net.forward(g, d, t, n)
+    torch.cuda.synchronize()
+    w = weights_for(cfg)
+    for f in range(cfg.batch):
+        ref = band_oracle(cfg, w, frames_from_device(g[f:f + 1], d[f:f + 1], t[f:f + 1], n[f:f + 1]))
+        mx, mean = errs(out[f].cpu().numpy(), ref)
+        print(f"FULLFRAME N1 c1 frame {f}: max abs {mx:.3e} mean abs {mean:.3e}")
+        assert mx <= BF16_TOL[0] and mean <= BF16_TOL[1]
+    net.close()
