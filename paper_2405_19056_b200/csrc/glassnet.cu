@@ -527,12 +527,17 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
   const size_t es = d.precision == GLASSNET_BF16 ? 2 : 4;
   const size_t P = (size_t)d.height * d.width;
   const size_t MB = (size_t)d.max_batch;
-  if (!net->st_g) {  // device staging, allocated once per handle on first use
-    CUDA_TRY(cudaMalloc(&net->st_g, MB * P * 12 * es));
-    CUDA_TRY(cudaMalloc(&net->st_d, MB * P * 3 * es));
-    CUDA_TRY(cudaMalloc(&net->st_t, MB * P * d.k_slots * 11 * es));
-    CUDA_TRY(cudaMalloc(&net->st_n, MB * P));
-    CUDA_TRY(cudaMalloc((void**)&net->st_o, MB * P * 3 * sizeof(float)));
+  if (!net->st_g) {  // device staging, allocated once per handle on first use (all or nothing)
+    void *g = nullptr, *dd = nullptr, *t = nullptr, *n = nullptr, *o = nullptr;
+    const bool ok = cudaMalloc(&g, MB * P * 12 * es) == cudaSuccess && cudaMalloc(&dd, MB * P * 3 * es) == cudaSuccess &&
+                    cudaMalloc(&t, MB * P * d.k_slots * 11 * es) == cudaSuccess && cudaMalloc(&n, MB * P) == cudaSuccess &&
+                    cudaMalloc(&o, MB * P * 3 * sizeof(float)) == cudaSuccess;
+    if (!ok) {
+      for (void* q : {g, dd, t, n, o}) if (q) cudaFree(q);
+      cudaGetLastError();
+      return gn_fail(GLASSNET_ERR_OUT_OF_MEMORY, "forward_host staging buffers");
+    }
+    net->st_g = g; net->st_d = dd; net->st_t = t; net->st_n = n; net->st_o = (float*)o;
   }
   if (!net->st_in) {
     CUDA_TRY(cudaStreamCreateWithFlags(&net->st_in, cudaStreamNonBlocking));
@@ -541,20 +546,27 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
   // Pipelined in chunks of frames: the copy-in of chunk i+1 (stream st_in) and the copy-out of
   // chunk i-1 (st_out) overlap the forward of chunk i (the caller's stream); chunks use
   // disjoint frame ranges of the staging buffers, and frames are independent (R21), so the
-  // result equals one whole-batch forward bit for bit.
+  // result equals one whole-batch forward bit for bit.  On any error the function still
+  // drains all three streams (no copy may touch the caller's buffers after it returns) and
+  // destroys its events.
   cudaStream_t st = (cudaStream_t)stream;
   const int CF = batch < 4 ? batch : 4;
   const int nch = (batch + CF - 1) / CF;
-  std::vector<cudaEvent_t> ev_in(nch), ev_c(nch);
-  for (int i = 0; i < nch; ++i) {
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_c[i], cudaEventDisableTiming));
-  }
-  cudaEvent_t ev0;
-  CUDA_TRY(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventRecord(ev0, st));               // the copies follow earlier work on the caller's stream
-  CUDA_TRY(cudaStreamWaitEvent(net->st_in, ev0, 0));
+  std::vector<cudaEvent_t> ev_in(nch, nullptr), ev_c(nch, nullptr);
+  cudaEvent_t ev0 = nullptr;
   int rc = GLASSNET_OK;
+  cudaError_t ce = cudaSuccess;
+  auto ck = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && ce == cudaSuccess) { ce = e; rc = gn_fail(GLASSNET_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e)); }
+    return ce == cudaSuccess;
+  };
+  for (int i = 0; i < nch && ce == cudaSuccess; ++i) {
+    ck(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_c[i], cudaEventDisableTiming), "event");
+  }
+  if (ck(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming), "event") &&
+      ck(cudaEventRecord(ev0, st), "event record"))   // the copies follow earlier work on the caller's stream
+    ck(cudaStreamWaitEvent(net->st_in, ev0, 0), "stream wait");
   for (int i = 0; i < nch && rc == GLASSNET_OK; ++i) {
     const size_t f0 = (size_t)i * CF, nf = (size_t)((i + 1) * CF <= batch ? CF : batch - i * CF);
     const char* hg = (const char*)gbuf + f0 * P * 12 * es;
@@ -565,22 +577,26 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
     char* dt = (char*)net->st_t + f0 * P * d.k_slots * 11 * es;
     uint8_t* dn = (uint8_t*)net->st_n + f0 * P;
     float* dout = net->st_o + f0 * P * 3;
-    CUDA_TRY(cudaMemcpyAsync(dg, hg, nf * P * 12 * es, cudaMemcpyHostToDevice, net->st_in));
-    CUDA_TRY(cudaMemcpyAsync(dd, hd, nf * P * 3 * es, cudaMemcpyHostToDevice, net->st_in));
-    CUDA_TRY(cudaMemcpyAsync(dt, ht, nf * P * d.k_slots * 11 * es, cudaMemcpyHostToDevice, net->st_in));
-    CUDA_TRY(cudaMemcpyAsync(dn, tcount + f0 * P, nf * P, cudaMemcpyHostToDevice, net->st_in));
-    CUDA_TRY(cudaEventRecord(ev_in[i], net->st_in));
-    CUDA_TRY(cudaStreamWaitEvent(st, ev_in[i], 0));
+    if (!(ck(cudaMemcpyAsync(dg, hg, nf * P * 12 * es, cudaMemcpyHostToDevice, net->st_in), "H2D") &&
+          ck(cudaMemcpyAsync(dd, hd, nf * P * 3 * es, cudaMemcpyHostToDevice, net->st_in), "H2D") &&
+          ck(cudaMemcpyAsync(dt, ht, nf * P * d.k_slots * 11 * es, cudaMemcpyHostToDevice, net->st_in), "H2D") &&
+          ck(cudaMemcpyAsync(dn, tcount + f0 * P, nf * P, cudaMemcpyHostToDevice, net->st_in), "H2D") &&
+          ck(cudaEventRecord(ev_in[i], net->st_in), "event record") && ck(cudaStreamWaitEvent(st, ev_in[i], 0), "wait")))
+      break;
     rc = glassnet_forward(net, dg, dd, dt, dn, dout, (int32_t)nf, stream);
     if (rc) break;
-    CUDA_TRY(cudaEventRecord(ev_c[i], st));
-    CUDA_TRY(cudaStreamWaitEvent(net->st_out, ev_c[i], 0));
-    CUDA_TRY(cudaMemcpyAsync(out + f0 * P * 3, dout, nf * P * 3 * sizeof(float), cudaMemcpyDeviceToHost, net->st_out));
+    if (!(ck(cudaEventRecord(ev_c[i], st), "event record") && ck(cudaStreamWaitEvent(net->st_out, ev_c[i], 0), "wait") &&
+          ck(cudaMemcpyAsync(out + f0 * P * 3, dout, nf * P * 3 * sizeof(float), cudaMemcpyDeviceToHost, net->st_out),
+             "D2H")))
+      break;
   }
   const cudaError_t e1 = cudaStreamSynchronize(net->st_in), e2 = cudaStreamSynchronize(net->st_out),
                     e3 = cudaStreamSynchronize(st);
-  for (int i = 0; i < nch; ++i) { cudaEventDestroy(ev_in[i]); cudaEventDestroy(ev_c[i]); }
-  cudaEventDestroy(ev0);
+  for (int i = 0; i < nch; ++i) {
+    if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+    if (ev_c[i]) cudaEventDestroy(ev_c[i]);
+  }
+  if (ev0) cudaEventDestroy(ev0);
   if (rc) return rc;
   CUDA_TRY(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3);
   return GLASSNET_OK;
