@@ -431,10 +431,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::fence_after_sync();
         const uint32_t d2 = tmem + S::T_ACC2 + b * H, a2 = tmem + S::T_ACC1 + a3 * H;
         TBP_NOW(l2a);
+#ifndef GN_ABL_L2
 #pragma unroll
         for (int q = 0; q < H / 16; ++q)
           tc::mma_f16_ts(d2, a2 + (q / (H / 32)) * (H / 2) + (q % (H / 32)) * 8,   // A2 half h at column h H/2
                          tc::smem_desc(sW2 + 2 * q * H * 16, H * 16, 128), ID_T, q > 0);
+#endif
         tc::mma_commit(done2 + (i & 3));
         TBP_ADD(21, l2a);
       }
@@ -699,14 +701,23 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           if (s == Kt - 1 && lane == 0) tc::mbar_arrive(a1Free + t % NA);   // the tile's layer-1 MMAs are done
           const uint32_t ta = tmem + lane_off + S::T_ACC1 + a3 * H + h * HC;
           uint32_t u[HC], o[HC / 2];
+#ifdef GN_ABL_TMEM
+#pragma unroll
+          for (int k = 0; k < HC; ++k) u[k] = (uint32_t)(lane + k);
+#else
           if constexpr (HC == 32) tc::tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(u));
           else tc::tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(u));
           tc::tmem_ld_wait();
+#endif
   #pragma unroll
           for (int k = 0; k < HC / 2; ++k) o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
+#ifndef GN_ABL_TMEM
           if constexpr (HC == 32) tc::tmem_st16(ta, o);
           else tc::tmem_st8(ta, o);
           tc::tmem_st_wait();
+#else
+          if (o[0] == 0x12345678u && lane == 99) psi[0] = 0.f;
+#endif
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(rdyA + a3);
@@ -758,9 +769,14 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           tc::fence_after_sync();
           uint32_t u[HC];
           const uint32_t ta = tmem + lane_off + S::T_ACC2 + b * H + h * HC;
+#ifdef GN_ABL_TMEM
+#pragma unroll
+          for (int k = 0; k < HC; ++k) u[k] = (uint32_t)(lane + k + ta);
+#else
 #pragma unroll
           for (int c = 0; c < HC / 16; ++c) tc::tmem_ld16(ta + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(u + 16 * c));
           tc::tmem_ld_wait();
+#endif
           TBP_ADD(24, w1);
           tc::fence_before_sync();
           __syncwarp();
