@@ -1,7 +1,7 @@
 # Round profile capture (run on the GPU box from the repo root): bench line, ncu launch list,
 # ncu --set full raw CSV exports of the T, conv and elementwise kernels (reports deleted on the box).
 set -x
-B="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline"
+B="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-extra"
 timeout 300 python bench.py > gpurun_out/bench_full_${SUF:-r1d}.log 2>&1
 tail -1 gpurun_out/bench_full_${SUF:-r1d}.log > gpurun_out/bench_line_${SUF:-r1d}.json
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_${SUF:-r1d}.csv $B > /dev/null 2>&1
