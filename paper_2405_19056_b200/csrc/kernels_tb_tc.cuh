@@ -26,22 +26,23 @@
 //   pool += bits(1 + v) - bits(1)   (v + 1 has ulp 2^-23, i.e. 2^-12 in a2 units)
 // -- integer adds, so any order of the valid slots gives the same bits.
 //
-// Warp roles (one CTA per SM, 22 warps):
+// Warp roles (one CTA per SM, 24 warps):
 //   w0        issuer A (one thread): layer 1 of every item (+ its commit), B of every tile
 //   w1        issuer B (one thread): layer 2 of every item (+ its commit).  One thread issues a
 //             tcgen05.mma only every ~50 cycles; two reach the N=64 pipe rate (ubench_multi2)
-//   w2..w5    loader: claims tiles, reads the count-sorted perm, the valid records (16-byte
-//             loads of the valid prefix only), e0 and L_d; repacks the records into the K=16
-//             slot windows (A1 ring), e0 into its operand (E0 ring), per-tile meta
-//   w6..w13   E1: two warps per TMEM lane quadrant, H/2 channels each: A2 = bf16(ReLU(acc1))
-//             written back INTO acc1 (layer 2 reads its A operand from TMEM); phi / psi -> HBM
-//   w14..w21  E2: two warps per quadrant, H/2 channels each: the fixed-point pool, tau -> f16 ->
+//   w2..w3    loader (two pixel rows per thread): claims tiles, reads the count-sorted perm,
+//             copies the valid records into their K=16 slot windows (A1 ring) and e0 into its
+//             operand (E0 ring) by cp.async one tile ahead, writes the per-tile meta
+//   w4..w7    psi: one warp per TMEM lane quadrant: phi = ReLU(accB + b_B + w_Bn n), psi -> HBM
+//   w8..w15   E1: two warps per quadrant, H/2 channels each: A2 = bf16(ReLU(acc1)) written back
+//             INTO acc1 (layer 2 reads its A operand from TMEM)
+//   w16..w23  E2: two warps per quadrant, H/2 channels each: the fixed-point pool, tau -> f16 ->
 //             TMEM (the B MMA's A operand)
 // Software pipeline: acc1 is a 3-deep ring (issuer A runs up to 2 items ahead of issuer B),
 // acc2 2-deep; the tensor pipe orders nothing across the two issuers, so A writes acc1[j % 3]
 // only after layer 2 of item j-3 (its previous reader) has completed.  B of tile u is issued
-// by A before layer 1 of item last(u) + 4 and phi / psi by E1 right after that item (B's MMAs
-// precede it in A's issue order, so they have completed).
+// by A before layer 1 of item last(u) + 4 (E2 has pooled the tile by then); the psi warps only
+// consume (doneB), so they never hold up the item pipeline.
 // Hand-offs are mbarriers; each waiter is provably at most one phase behind.
 #pragma once
 #include <cuda_bf16.h>
@@ -184,8 +185,8 @@ struct TbLayout {
   static constexpr int WIMG_B = W1_B + W2_B + WBE_B + WBT_B + W1E_B;
   static constexpr int OFF_W1 = 0, OFF_W2 = OFF_W1 + W1_B, OFF_WBE = OFF_W2 + W2_B, OFF_WBT = OFF_WBE + WBE_B;
   static constexpr int OFF_W1E = OFF_WBT + WBT_B;
-  // per-tile meta: pixel ids, counts, L_d (E2's psi needs them one tile late), Kt
-  static constexpr int M_PIX = 0, M_LD = 128 * 8, M_CNT = M_LD + 128 * 12, M_KT = M_CNT + 128, META_B = M_KT + 16;
+  // per-tile meta: pixel ids, counts, Kt (the psi warps need them until B(u) has completed)
+  static constexpr int M_PIX = 0, M_CNT = 128 * 8, M_KT = M_CNT + 128, META_B = M_KT + 16;
   // CP (K even, so every row's records start 4-byte aligned): each record is copied by 4-byte
   // cp.asyncs straight into its slot window, one tile ahead; otherwise halfword loads + stores
   static constexpr bool CP = K % 2 == 0;
@@ -199,9 +200,8 @@ struct TbLayout {
   static constexpr int NBAR = 40;
   static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch, blend queue
-  static constexpr int OFF_PSX = OFF_MISC + 128;      // psi partials of the h = 1 E1 warps [2][4][32][3] f32
-  static constexpr int SMEM = OFF_PSX + 2 * 4 * 32 * 3 * 4;
-  static constexpr int NWARP = 22, THREADS = 32 * NWARP;   // 2 MMA issuers, 4 loader, 8 E1, 8 E2
+  static constexpr int SMEM = OFF_MISC + 128;
+  static constexpr int NWARP = 24, THREADS = 32 * NWARP;   // 2 MMA issuers, 2 loader, 4 psi, 8 E1, 8 E2
   // TMEM columns: acc1 ring of 3 (A2 written over its first H/2 columns), acc2 ring of 2,
   // accB x 2, tau x 4 (f16 pairs; E2 writes tau(u) once B(u-4) has completed)
   static constexpr int T_ACC1 = 0, T_ACC2 = 3 * H, T_ACCB = 5 * H, T_TAU = 5 * H + 2 * C0;
@@ -252,9 +252,12 @@ struct TbPh {
   __device__ __forceinline__ void flip(int i) { v ^= 1u << i; }
 };
 
-// 22 warps: the busiest SM sub-partitions hold 6 of them, so 16,384 / (6 x 32) registers
+#ifndef GN_TB_MAXNREG
+#define GN_TB_MAXNREG 80
+#endif
+// 24 warps, 6 per SM sub-partition: 80 registers x 32 x 24 = 61,440 of 65,536
 template <int K, int H, int C0, int POOL>
-__global__ void __maxnreg__(80)
+__global__ void __maxnreg__(GN_TB_MAXNREG)
 k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, const uint16_t* __restrict__ direct,
         const uint8_t* __restrict__ wimg, const __grid_constant__ TbParams prm, const uint32_t* __restrict__ perm,
         float* __restrict__ psi, long P, int* __restrict__ sched) {
@@ -262,20 +265,20 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t PL = S::PL;
   constexpr int NO = C0 + 3, NE = S::NE, NA = S::NA;
-  constexpr int LAGI = 4;   // B of tile u: issued by A before layer 1 of item last(u) + LAGI, psi by E1 after it
+  constexpr int LAGI = 4;   // B of tile u: issued by A before layer 1 of item last(u) + LAGI
   static_assert(C0 <= 32 && (H == 32 || H == 64), "TbParams sizes / epilogue chunks");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
-  uint64_t* tileReady = bars + 0;   // [NE] loader -> all (4 warp arrivals)
-  uint64_t* metaFree = bars + 6;    // [NE] E1 (8, psi) + E2 (8, counts read) -> loader
+  uint64_t* tileReady = bars + 0;   // [NE] loader -> all (2 warp arrivals)
+  uint64_t* metaFree = bars + 6;    // [NE] psi (4) + E2 (8, counts read) -> loader
   uint64_t* a1Free = bars + 12;     // [NA] E1 (8): the tile's last layer-1 MMA has completed -> loader
   uint64_t* done1 = bars + 15;      // [3] issuer A's commit of layer 1 of item i -> E1
   uint64_t* rdyA = bars + 18;       // [3] E1 (8) -> issuer B: A2 of item i in acc1[i % 3]
   uint64_t* done2 = bars + 21;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
   uint64_t* free2 = bars + 25;      // [2] E2 (8) -> issuer B: acc2[i % 2] read
   uint64_t* tauRdy = bars + 27;     // [4] E2 (8) -> issuer A: tau of tile u in TMEM tau[u % 4]
-  uint64_t* doneB = bars + 31;      // [4] issuer A's commit of B(u) -> E1 (psi), E2 (tau[u % 4] reuse)
-  uint64_t* accBfree = bars + 35;   // [2] E1 (8, psi) -> issuer A: accB read
+  uint64_t* doneB = bars + 31;      // [4] issuer A's commit of B(u) -> psi, E2 (tau[u % 4] reuse)
+  uint64_t* accBfree = bars + 35;   // [2] psi (4) -> issuer A: accB read
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_MISC);
   volatile int* lred = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 16);   // [2][4] warp max counts
   volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 64);    // [8] claimed tile ids
@@ -292,11 +295,11 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           make_uint2(0x3F803F80u, 0x00003F80u);
     }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, 4); tc::mbar_init(metaFree + i, 16); }
+    for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, 2); tc::mbar_init(metaFree + i, 12); }
     for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 8);
     for (int i = 0; i < 3; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 8); }
     for (int i = 0; i < 4; ++i) tc::mbar_init(done2 + i, 1);
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(free2 + i, 8); tc::mbar_init(accBfree + i, 8); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(free2 + i, 8); tc::mbar_init(accBfree + i, 4); }
     for (int i = 0; i < 4; ++i) { tc::mbar_init(tauRdy + i, 8); tc::mbar_init(doneB + i, 1); }
     *total = 0x7FFFFFFF;
     tc::fence_mbar_init();
@@ -443,30 +446,31 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       TBP_ADD(22, tot0);
       TBP_FLUSH_IF(true);
     }
-  } else if (warp <= 5) {
+  } else if (warp <= 3) {
     // ---------------------------------------------------------------- loader
-    const int r = (warp - 2) * 32 + lane;
+    // 64 threads, pixel rows r0 and r0 + 64 of every tile
+    const int r0 = (warp - 2) * 32 + lane;
     const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
     TbPh mfph, afph;
     int claim = 0;
     // tile ids are claimed three ahead by thread 0 (ids ring of 8), perm entries read one tile
     // ahead of the tile whose copies are issued
-    if (r == 0) {
+    if (r0 == 0) {
       ids[0] = atomicAdd(sched, 1); ids[1] = atomicAdd(sched, 1); ids[2] = atomicAdd(sched, 1);
       claim = atomicAdd(sched, 1);
     }
-    tc::bar_sync(1, 128);
-    auto perm_of = [&](long tl) -> uint32_t { return tl < ntiles ? __ldg(perm + tl * 128 + r) : 0u; };
+    tc::bar_sync(1, 64);
+    auto perm_of = [&](long tl, int r) -> uint32_t { return tl < ntiles ? __ldg(perm + tl * 128 + r) : 0u; };
     auto decode = [&](long tl, uint32_t pe, long& p, int& m) {
       p = tl / TB_SBT * TB_SBP + (pe & 0xFFFF);
       m = (tl < ntiles && p < P) ? (int)(pe >> 16) : 0;
       if (!(tl < ntiles && p < P)) p = -1;
     };
-    // CP: issue tile tl's copies into A1 buffer ab and E0 slot es: each valid record by six 4-byte
-    // cp.asyncs into its window (columns 0..11; even slots start at the record and zero-fill the
-    // column after it, odd slots start one halfword early), e0 by 16-byte cp.asyncs into its
-    // K-major planes; returns L_d
-    auto issue = [&](long tl, uint32_t pe, int ab, int es, float (&ldv)[3]) {
+    // CP: issue row r of tile tl's copies into A1 buffer ab and E0 slot es: each valid record by
+    // six 4-byte cp.asyncs into its window (columns 0..11; even slots start at the record and
+    // zero-fill the column after it, odd slots start one halfword early), e0 by 16-byte cp.asyncs
+    // into its K-major planes
+    auto issue = [&](long tl, uint32_t pe, int r, int ab, int es) {
       long p; int m;
       decode(tl, pe, p, m);
       const char* src = reinterpret_cast<const char*>(tbuf + (p >= 0 ? p : 0) * (K * 11));
@@ -482,18 +486,15 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
 #pragma unroll
       for (int j = 0; j < C0 / 8; ++j)
         cp_async16z(sE0 + (uint32_t)es * S::E0_B + j * PL + r * 16, es_src + 8 * j, p >= 0 ? 16u : 0u);
-      ldv[0] = ldv[1] = ldv[2] = 0.f;
-      if (p >= 0)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ldv[c] = __uint_as_float((uint32_t)__ldg(direct + p * 3 + c) << 16);
     };
-    long tile = ids[0];
-    uint32_t pe = perm_of(tile);
-    long ntile = ids[1];
-    uint32_t npe = perm_of(ntile);
-    float ldc[3] = {0.f, 0.f, 0.f};
+    long tile = ids[0], ntile = ids[1];
+    uint32_t pe[2], npe[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) { pe[h] = perm_of(tile, r0 + 64 * h); npe[h] = perm_of(ntile, r0 + 64 * h); }
     if constexpr (S::CP) {   // tile 0's copies (its operand slots are fresh: they count as waited)
-      if (tile < ntiles) issue(tile, pe, 0, 0, ldc);
+      if (tile < ntiles)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) issue(tile, pe[h], r0 + 64 * h, 0, 0);
       cp_async_commit();
       mfph.flip(0);
       afph.flip(0);
@@ -504,174 +505,188 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       uint8_t* M = meta(t);
       if (tile >= ntiles) {   // end marker (CP: this slot was waited for one iteration ago)
         if constexpr (!S::CP) tc::mbar_wait(metaFree + e, mfph[e] ^ 1);
-        if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = -1;
+        if (r0 == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = -1;
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tileReady + e);
         if constexpr (S::CP) cp_async_wait_all();
         TBP_ADD(7, tot0);
-        TBP_FLUSH_IF(r == 0);
+        TBP_FLUSH_IF(r0 == 0);
         break;
       }
       TBP_NOW(ld0);
-      long p; int m;
-      decode(tile, pe, p, m);
-      const bool pv = p >= 0;
-      float ldv[3] = {0.f, 0.f, 0.f};
-      uint4 ev[C0 / 8];
+      long p[2]; int m[2];
+      uint4 ev[2][C0 / 8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) decode(tile, pe[h], p[h], m[h]);
       if constexpr (S::CP) {
         // the next tile's copies first (its E0 / meta slot: tile t+1-NE's consumers are done; its A1
         // buffer: tile t+1-NA's layer-1 MMAs are done), then this tile's (issued one iteration ago)
-        float ldn[3] = {0.f, 0.f, 0.f};
         TBP_NOW(w0);
         tc::mbar_wait(metaFree + (t + 1) % NE, mfph[(t + 1) % NE] ^ 1); mfph.flip((t + 1) % NE);
         TBP_ADD(5, w0);
         TBP_NOW(w1);
         tc::mbar_wait(a1Free + (t + 1) % NA, afph[(t + 1) % NA] ^ 1); afph.flip((t + 1) % NA);
         TBP_ADD(6, w1);
-        if (ntile < ntiles) issue(ntile, npe, (t + 1) % NA, (t + 1) % NE, ldn);
-        cp_async_commit();
-        cp_async_wait_1();
+        TBP_NOW(is0);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) { ldv[c] = ldc[c]; ldc[c] = ldn[c]; }
+        for (int h = 0; h < 2; ++h) {
+          if (ntile < ntiles) issue(ntile, npe[h], r0 + 64 * h, (t + 1) % NA, (t + 1) % NE);
+        }
+        cp_async_commit();
+        TBP_ADD(30, is0);
+        TBP_NOW(cw0);
+        cp_async_wait_1();
+        TBP_ADD(25, cw0);
       } else {
 #pragma unroll
-        for (int j = 0; j < C0 / 8; ++j) ev[j] = pv ? tb_ld_nc4(e0 + p * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
-        if (pv)
+        for (int h = 0; h < 2; ++h) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) ldv[c] = __uint_as_float((uint32_t)__ldg(direct + p * 3 + c) << 16);
+          for (int j = 0; j < C0 / 8; ++j)
+            ev[h][j] = p[h] >= 0 ? tb_ld_nc4(e0 + p[h] * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
+        }
         TBP_NOW(w0);
         tc::mbar_wait(metaFree + e, mfph[e] ^ 1); mfph.flip(e);   // meta / E0 of tile t-NE
         TBP_ADD(5, w0);
       }
       const long nntile = ids[(t + 2) & 7];   // written before the last bar.sync
-      const uint32_t nnpe = perm_of(nntile);
-      reinterpret_cast<long long*>(M + S::M_PIX)[r] = pv ? (long long)p : -1ll;
-      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 0] = ldv[0];
-      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 1] = ldv[1];
-      reinterpret_cast<float*>(M + S::M_LD)[3 * r + 2] = ldv[2];
-      M[S::M_CNT + r] = (uint8_t)m;
-      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)m);
+      uint32_t nnpe[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + 64 * h;
+        nnpe[h] = perm_of(nntile, r);
+        reinterpret_cast<long long*>(M + S::M_PIX)[r] = p[h] >= 0 ? (long long)p[h] : -1ll;
+        M[S::M_CNT + r] = (uint8_t)m[h];
+      }
+      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)max(m[0], m[1]));
       if (lane == 0) lred[(t & 1) * 4 + warp - 2] = wm;
-      if (r == 0) { ids[(t + 3) & 7] = claim; claim = atomicAdd(sched, 1); }
+      if (r0 == 0) { ids[(t + 3) & 7] = claim; claim = atomicAdd(sched, 1); }
       TBP_NOW(w2);
-      tc::bar_sync(1, 128);
+      tc::bar_sync(1, 64);
       TBP_ADD(8, w2);
       // Kt >= 1 even for a tile of empty pixels (one item of zero records, pooled by nobody): every
       // tile then advances the item pipeline, which bounds how far a blocked consumer can lag
       // (deadlock freedom of the rings)
-      int Kt;
-      {
-        const int* L = const_cast<const int*>(lred) + (t & 1) * 4;
-        Kt = max(1, max(max(L[0], L[1]), max(L[2], L[3])));
-      }
-      TBP_NOW(st0);
-      const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + r * 16;
+      const int Kt = max(1, max(lred[(t & 1) * 4 + 0], lred[(t & 1) * 4 + 1]));
       if constexpr (S::CP) {
         // masked slots the tile's items reach: zero columns 0..11 (the constant columns stay)
-        for (int k = m; k < Kt; ++k) {
-          tc::sts128(a1 + (uint32_t)(2 * k) * PL, 0u, 0u, 0u, 0u);
-          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a1 + (uint32_t)(2 * k + 1) * PL), "r"(0u), "r"(0u)
-                       : "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + (r0 + 64 * h) * 16;
+          for (int k = m[h]; k < Kt; ++k) {
+            tc::sts128(a1 + (uint32_t)(2 * k) * PL, 0u, 0u, 0u, 0u);
+            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a1 + (uint32_t)(2 * k + 1) * PL), "r"(0u), "r"(0u)
+                         : "memory");
+          }
         }
-      } else {   // halfword loads (K odd: rows not 4-byte aligned); even-slot window layout for all slots
+      } else {
+        // halfword loads (K odd: rows not 4-byte aligned); even-slot window layout for all slots
         TBP_NOW(w1);
         tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);     // A1 of tile t-NA
         TBP_ADD(6, w1);
-        const uint16_t* src = tbuf + (pv ? p : 0) * (K * 11);
-        for (int k = 0; k < Kt; ++k) {
-          uint32_t w[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) w[i] = 0;
-          if (k < m) {
-            uint32_t hv[12];
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + 64 * h;
+          const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + r * 16;
+          const uint16_t* src = tbuf + (p[h] >= 0 ? p[h] : 0) * (K * 11);
+          for (int k = 0; k < Kt; ++k) {
+            uint32_t w[8];
 #pragma unroll
-            for (int i = 0; i < 11; ++i) hv[i] = __ldg(src + 11 * k + i);
-            hv[11] = 0;
+            for (int i = 0; i < 8; ++i) w[i] = 0;
+            if (k < m[h]) {
+              uint32_t hv[12];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) w[i] = hv[2 * i] | (hv[2 * i + 1] << 16);
+              for (int i = 0; i < 11; ++i) hv[i] = __ldg(src + 11 * k + i);
+              hv[11] = 0;
+#pragma unroll
+              for (int i = 0; i < 6; ++i) w[i] = hv[2 * i] | (hv[2 * i + 1] << 16);
+            }
+            w[6] = 0x3F803F80u;   // columns 12, 13 = 1
+            w[7] = 0x00003F80u;   // column 14 = 1, column 15 = 0
+            tc::sts128(a1 + (uint32_t)(2 * k) * PL, w[0], w[1], w[2], w[3]);
+            tc::sts128(a1 + (uint32_t)(2 * k + 1) * PL, w[4], w[5], w[6], w[7]);
           }
-          w[6] = 0x3F803F80u;   // columns 12, 13 = 1
-          w[7] = 0x00003F80u;   // column 14 = 1, column 15 = 0
-          tc::sts128(a1 + (uint32_t)(2 * k) * PL, w[0], w[1], w[2], w[3]);
-          tc::sts128(a1 + (uint32_t)(2 * k + 1) * PL, w[4], w[5], w[6], w[7]);
-        }
 #pragma unroll
-        for (int j = 0; j < C0 / 8; ++j)
-          tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[j].x, ev[j].y, ev[j].z, ev[j].w);
+          for (int j = 0; j < C0 / 8; ++j)
+            tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[h][j].x, ev[h][j].y, ev[h][j].z, ev[h][j].w);
+        }
       }
-      TBP_ADD(25, st0);
-      if (r == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = Kt;
+      if (r0 == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = Kt;
       tc::fence_proxy_async();   // this thread's operand writes (and its waited cp.asyncs) -> async proxy
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tileReady + e);
       TBP_ADD(26, ld0);
-      tile = ntile; pe = npe;
-      ntile = nntile; npe = nnpe;
+      tile = ntile; ntile = nntile;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) { pe[h] = npe[h]; npe[h] = nnpe[h]; }
     }
-  } else if (warp <= 13) {
-    // ---------------------------------------------------------------- E1: A2 = bf16(ReLU(acc1)) -> TMEM; psi
+  } else if (warp <= 7) {
+    // ---------------------------------------------------------------- psi
+    // one warp per TMEM lane quadrant, all C0 channels of accB: phi = ReLU(accB + b_B + w_Bn n),
+    // psi = W_O,d0 phi + W_O,L L_d + b_O (reading R15).  Only consumes: waits for B(u)'s commit,
+    // frees accB[u % 2] and the tile's meta slot.
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    TbPh trph, dbph;
+    TBP_NOW(tot0);
+    for (int u = 0;; ++u) {
+      const int e = u % NE, ab = u & 1;
+      TBP_NOW(w0);
+      tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
+      TBP_ADD(29, w0);
+      const uint8_t* M = meta(u);
+      if (*reinterpret_cast<const volatile int*>(M + S::M_KT) < 0) break;
+      // L_d of the pixel, loaded before the wait for B(u) (its latency hides behind the wait)
+      const long long p = reinterpret_cast<const long long*>(M + S::M_PIX)[r];
+      uint32_t ldr[3] = {0u, 0u, 0u};
+      if (p >= 0)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ldr[c] = __ldg(direct + p * 3 + c);
+      TBP_NOW(w1);
+      // one warp polls (sleeping between tries: psi is off the critical path), the four follow
+      if (warp == 4) tc::mbar_wait_sleep(doneB + (u & 3), dbph[u & 3], 256);
+      dbph.flip(u & 3);
+      tc::bar_sync(2, 128);
+      TBP_ADD(28, w1);
+      tc::fence_after_sync();
+      uint32_t v[C0];
+      if constexpr (C0 == 32) tc::tmem_ld32(tmem + lane_off + S::T_ACCB + ab * C0, *reinterpret_cast<uint32_t(*)[32]>(v));
+      else tc::tmem_ld16(tmem + lane_off + S::T_ACCB + ab * C0, *reinterpret_cast<uint32_t(*)[16]>(v));
+      tc::tmem_ld_wait();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(accBfree + ab);
+      const float fm = (float)M[S::M_CNT + r];
+      const float* WO = prm.WO;
+      const float ld0 = __uint_as_float(ldr[0] << 16), ld1 = __uint_as_float(ldr[1] << 16), ld2 = __uint_as_float(ldr[2] << 16);
+      float o0 = prm.bO[0], o1 = prm.bO[1], o2 = prm.bO[2];
+#pragma unroll
+      for (int o = 0; o < C0; ++o) {
+        const float phi = relu(__uint_as_float(v[o]) + prm.bB[o] + prm.wBn[o] * fm);
+        o0 = fmaf(WO[0 * NO + o], phi, o0);
+        o1 = fmaf(WO[1 * NO + o], phi, o1);
+        o2 = fmaf(WO[2 * NO + o], phi, o2);
+      }
+      o0 = fmaf(WO[0 * NO + C0 + 0], ld0, o0); o0 = fmaf(WO[0 * NO + C0 + 1], ld1, o0); o0 = fmaf(WO[0 * NO + C0 + 2], ld2, o0);
+      o1 = fmaf(WO[1 * NO + C0 + 0], ld0, o1); o1 = fmaf(WO[1 * NO + C0 + 1], ld1, o1); o1 = fmaf(WO[1 * NO + C0 + 2], ld2, o1);
+      o2 = fmaf(WO[2 * NO + C0 + 0], ld0, o2); o2 = fmaf(WO[2 * NO + C0 + 1], ld1, o2); o2 = fmaf(WO[2 * NO + C0 + 2], ld2, o2);
+      if (p >= 0) { psi[p * 3 + 0] = o0; psi[p * 3 + 1] = o1; psi[p * 3 + 2] = o2; }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(metaFree + e);
+    }
+    TBP_ADD(27, tot0);
+    TBP_FLUSH_IF(warp == 4 && lane == 0);
+  } else if (warp <= 15) {
+    // ---------------------------------------------------------------- E1: A2 = bf16(ReLU(acc1)) -> TMEM
     // two warps per TMEM lane quadrant, H/2 channels each; half h writes its A2 (H/4 packed
     // columns) over the first columns it has itself read: columns [h H/2, h H/2 + H/4).
-    // psi of tile u right after item last(u) + LAGI: issuer A issued B of tile u before layer 1
-    // of that item, in order, so its doneB has completed by then (no wait on the item chain);
-    // the pair (h = 0, 1) splits accB's columns and adds the halves through shared memory.
+    constexpr int HC = H / 2;
+    const int q = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    // the half h as a compile-time constant (register-indexed TMEM column offsets)
     auto e1 = [&](auto hc) {
       constexpr int h = decltype(hc)::value;
-      constexpr int HC = H / 2, CH = C0 / 2;
-      const int q = warp & 3, r = q * 32 + lane;
-      const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-      float* psx = reinterpret_cast<float*>(smem + S::OFF_PSX);
-      TbPh trph, d1ph, dbph;
+      TbPh trph, d1ph;
       int i = 0;
-      int pqt[6] = {0, 0, 0, 0, 0, 0}, pqd[6] = {0, 0, 0, 0, 0, 0}, pqn = 0;   // pending psi: (tile, due item)
-      auto psi_tile = [&]() {
-        const int u = pqt[0];
-  #pragma unroll
-        for (int k = 0; k < 5; ++k) { pqt[k] = pqt[k + 1]; pqd[k] = pqd[k + 1]; }
-        --pqn;
-        const int ab = u & 1;
-        const uint8_t* M = meta(u);
-        TBP_NOW(w0);
-        tc::mbar_wait(doneB + (u & 3), dbph[u & 3]); dbph.flip(u & 3);
-        TBP_ADD(28, w0);
-        tc::fence_after_sync();
-        uint32_t v[CH];
-        if constexpr (CH == 16) tc::tmem_ld16(tmem + lane_off + S::T_ACCB + ab * C0 + h * CH, *reinterpret_cast<uint32_t(*)[16]>(v));
-        else tc::tmem_ld8(tmem + lane_off + S::T_ACCB + ab * C0 + h * CH, *reinterpret_cast<uint32_t(*)[8]>(v));
-        tc::tmem_ld_wait();
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(accBfree + ab);
-#ifdef GN_ABL_PSI
-        if (u >= 0) { __syncwarp(); if (lane == 0) tc::mbar_arrive(metaFree + u % NE); return; }
-#endif
-        const float fm = (float)M[S::M_CNT + r];
-        const float* WO = prm.WO;
-        float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f;
-  #pragma unroll
-        for (int k = 0; k < CH; ++k) {
-          const int o = h * CH + k;
-          const float phi = relu(__uint_as_float(v[k]) + prm.bB[o] + prm.wBn[o] * fm);
-          ps0 = fmaf(WO[0 * NO + o], phi, ps0);
-          ps1 = fmaf(WO[1 * NO + o], phi, ps1);
-          ps2 = fmaf(WO[2 * NO + o], phi, ps2);
-        }
-        float* px = psx + ((u & 1) * 4 + q) * 96 + 3 * lane;
-        if (h == 1) { px[0] = ps0; px[1] = ps1; px[2] = ps2; }
-        tc::bar_sync(2 + q, 64);
-        if (h == 0) {
-          const long long p = reinterpret_cast<const long long*>(M + S::M_PIX)[r];
-          const float* ld = reinterpret_cast<const float*>(M + S::M_LD) + 3 * r;
-          const float ld0 = ld[0], ld1 = ld[1], ld2 = ld[2];
-          float o0 = prm.bO[0] + ps0 + px[0], o1 = prm.bO[1] + ps1 + px[1], o2 = prm.bO[2] + ps2 + px[2];
-          o0 = fmaf(WO[0 * NO + C0 + 0], ld0, o0); o0 = fmaf(WO[0 * NO + C0 + 1], ld1, o0); o0 = fmaf(WO[0 * NO + C0 + 2], ld2, o0);
-          o1 = fmaf(WO[1 * NO + C0 + 0], ld0, o1); o1 = fmaf(WO[1 * NO + C0 + 1], ld1, o1); o1 = fmaf(WO[1 * NO + C0 + 2], ld2, o1);
-          o2 = fmaf(WO[2 * NO + C0 + 0], ld0, o2); o2 = fmaf(WO[2 * NO + C0 + 1], ld1, o2); o2 = fmaf(WO[2 * NO + C0 + 2], ld2, o2);
-          if (p >= 0) { psi[p * 3 + 0] = o0; psi[p * 3 + 1] = o1; psi[p * 3 + 2] = o2; }
-        }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(metaFree + u % NE);
-      };
       TBP_NOW(tot0);
       for (int t = 0;; ++t) {
         const int e = t % NE;
@@ -680,19 +695,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         TBP_ADD(10, w9);
         const int Kt = *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
         if (Kt < 0) break;
-        {   // queue this tile's psi: LAGI items after its last item
-          const int d = i + Kt - 1 + LAGI;
-  #pragma unroll
-          for (int k = 0; k < 6; ++k)
-            if (k == pqn) { pqt[k] = t; pqd[k] = d; }
-          ++pqn;
-        }
-  #pragma unroll 1
+#pragma unroll 1
         for (int s = 0; s < Kt; ++s) {
           const int a3 = i % 3;
           TBP_NOW(w0);
           // one warp polls the barrier, the group of 8 E1 warps is released by a named barrier
-          if (warp == 6) tc::mbar_wait(done1 + a3, d1ph[a3]);
+          if (warp == 8) tc::mbar_wait(done1 + a3, d1ph[a3]);
           d1ph.flip(a3);
           tc::bar_sync(6, 256);
           TBP_ADD(9, w0);
@@ -709,8 +717,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           else tc::tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(u));
           tc::tmem_ld_wait();
 #endif
-  #pragma unroll
-          for (int k = 0; k < HC / 2; ++k) o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
+#pragma unroll
+          for (int k = 0; k < HC / 2; ++k)
+            o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
 #ifndef GN_ABL_TMEM
           if constexpr (HC == 32) tc::tmem_st16(ta, o);
           else tc::tmem_st8(ta, o);
@@ -722,18 +731,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(rdyA + a3);
           TBP_ADD(16, w1);
-          TBP_NOW(w2);
-          while (pqn > 0 && pqd[0] <= i) psi_tile();
-          TBP_ADD(27, w2);
           ++i;
         }
       }
-      while (pqn > 0) psi_tile();
       TBP_ADD(12, tot0);
-
     };
-    // the half h as a compile-time constant: psi's weights are then constant-bank operands
-    if (warp < 10) e1(TbInt<0>{});
+    if (warp < 12) e1(TbInt<0>{});
     else e1(TbInt<1>{});
     TBP_FLUSH_IF(warp == 8 && lane == 0);
   } else {
@@ -749,7 +752,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       int i = 0;
       TBP_NOW(tot0);
       for (int t = 0;; ++t) {
-        const int e = t % NE, ab = t & 1;
+        const int e = t % NE;
         tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
         const int Kt = *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
         if (Kt < 0) break;
@@ -761,7 +764,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         for (int s = 0; s < Kt; ++s) {
           const int b = i & 1;
           TBP_NOW(w0);
-          if (warp == 14) tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // one warp polls, the
+          if (warp == 16) tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // one warp polls, the
           d2ph.flip(i & 3);                                               // group of 8 follows
           tc::bar_sync(7, 256);
           TBP_ADD(13, w0);
@@ -821,7 +824,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       TBP_ADD(15, tot0);
       TBP_FLUSH_IF(warp == 16 && lane == 0);
     };
-    if (warp < 18) e2(TbInt<0>{});
+    if (warp < 20) e2(TbInt<0>{});
     else e2(TbInt<1>{});
   }
   tc::fence_before_sync();

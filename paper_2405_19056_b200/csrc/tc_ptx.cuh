@@ -213,6 +213,16 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
                : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
   return ok != 0;
 }
+// polling with a sleep between tries: for waiters off the critical path (their spinning would take
+// issue slots from the working warps of their SM sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
+#ifdef GN_MBAR_WATCHDOG
+  (void)ns;
+  mbar_wait(bar, phase);
+#else
+  while (!mbar_test(bar, phase)) __nanosleep(ns);
+#endif
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -36,9 +36,9 @@ names = {0: "A wait tileReady", 2: "A wait done2 (acc1 slot)", 3: "A blend waits
          23: "A blend issue", 31: "A due blends (all)", 4: "A total",
          1: "B wait rdyA", 11: "B wait free2", 21: "B layer2 issue+commit", 22: "B total",
          5: "loader wait metaFree", 6: "loader wait a1Free", 7: "loader total", 8: "loader bar.sync",
-         25: "loader store phase", 26: "loader tile (all)",
+         30: "loader issue next tile", 25: "loader cp.async wait", 26: "loader tile (all)",
          9: "E1 wait done1", 10: "E1 wait tileReady", 12: "E1 total", 16: "E1 item work",
-         27: "E1 psi (all)", 28: "E1 psi wait doneB",
+         27: "psi total", 28: "psi wait doneB", 29: "psi wait tileReady",
          13: "E2 wait done2", 14: "E2 wait doneB (tau reuse)", 15: "E2 total", 17: "E2 item work", 24: "E2 tmem ld+wait"}
 print(f"tiles {tiles} items {items} ({items / max(tiles, 1):.2f} items/tile); per CTA: {tiles / ctas:.0f} tiles")
 for i, nm in names.items():
