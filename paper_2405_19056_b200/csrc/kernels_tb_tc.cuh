@@ -194,10 +194,11 @@ struct TbLayout {
   static constexpr int OFF_A1 = (WIMG_B + 1023) / 1024 * 1024;
   static constexpr int REST = NE * E0_B + NE * META_B + 64 * 8 + 128 + 3072;
   static constexpr int LIMIT = 232448 - 1024;
-  static constexpr int NA = OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;   // A1 ring
+  // A1 ring: as deep as shared memory allows (the loader runs further ahead over short tiles)
+  static constexpr int NA = OFF_A1 + 4 * A1_B + REST <= LIMIT ? 4 : OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;
   static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
   static constexpr int OFF_META = OFF_E0 + NE * E0_B;
-  static constexpr int NBAR = 40;
+  static constexpr int NBAR = 44;
   static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch, blend queue
   static constexpr int SMEM = OFF_MISC + 128;
@@ -271,7 +272,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
   uint64_t* tileReady = bars + 0;   // [NE] loader -> all (2 warp arrivals)
   uint64_t* metaFree = bars + 6;    // [NE] psi (4) + E2 (8, counts read) -> loader
-  uint64_t* a1Free = bars + 12;     // [NA] E1 (8): the tile's last layer-1 MMA has completed -> loader
+  uint64_t* a1Free = bars + 40;     // [NA <= 4] E1 (8): the tile's last layer-1 MMA has completed -> loader
   uint64_t* done1 = bars + 15;      // [3] issuer A's commit of layer 1 of item i -> E1
   uint64_t* rdyA = bars + 18;       // [3] E1 (8) -> issuer B: A2 of item i in acc1[i % 3]
   uint64_t* done2 = bars + 21;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
