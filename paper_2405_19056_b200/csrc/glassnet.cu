@@ -674,11 +674,11 @@ extern "C" int glassnet_tile_rows(const glassnet_dims* dims, int32_t nranks, int
 }
 
 #ifdef GN_TB_PROF
-extern "C" int glassnet_debug_tb_prof(unsigned long long* out32, int reset) {
+extern "C" int glassnet_debug_tb_prof(unsigned long long* out40, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out32, gn::gn_tb_prof, 32 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out40, gn::gn_tb_prof, 40 * sizeof(unsigned long long));
   if (reset) {
-    unsigned long long z[32] = {};
+    unsigned long long z[40] = {};
     cudaMemcpyToSymbol(gn::gn_tb_prof, z, sizeof z);
   }
   return 0;

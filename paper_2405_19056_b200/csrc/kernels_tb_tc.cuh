@@ -26,23 +26,24 @@
 //   pool += bits(1 + v) - bits(1)   (v + 1 has ulp 2^-23, i.e. 2^-12 in a2 units)
 // -- integer adds, so any order of the valid slots gives the same bits.
 //
-// Warp roles (one CTA per SM, 24 warps):
-//   w0        issuer A (one thread): layer 1 of every item (+ its commit), B of every tile
+// Warp roles (one CTA per SM, 21 warps; the TMEM roles take warp % 4 = their lane quadrant):
+//   w0        issuer A (one thread): layer 1 of every item (+ its commit)
 //   w1        issuer B (one thread): layer 2 of every item (+ its commit).  One thread issues a
 //             tcgen05.mma only every ~50 cycles; two reach the N=64 pipe rate (ubench_multi2)
-//   w2..w3    loader (two pixel rows per thread): claims tiles, reads the count-sorted perm,
+//   w2        issuer C (one thread): B of every tile, as soon as E2 has written the tile's tau
+//   w3..w4    loader (two pixel rows per thread): claims tiles, reads the count-sorted perm,
 //             copies the valid records into their K=16 slot windows (A1 ring) and e0 into its
 //             operand (E0 ring) by cp.async one tile ahead, writes the per-tile meta
-//   w4..w7    psi: one warp per TMEM lane quadrant: phi = ReLU(accB + b_B + w_Bn n), psi -> HBM
-//   w8..w15   E1: two warps per quadrant, H/2 channels each: A2 = bf16(ReLU(acc1)) written back
+//   w5..w8    psi: one warp per quadrant: phi = ReLU(accB + b_B + w_Bn n), psi -> HBM
+//   w9..w12   E1: one warp per quadrant, both channel halves: A2 = bf16(ReLU(acc1)) written back
 //             INTO acc1 (layer 2 reads its A operand from TMEM)
-//   w16..w23  E2: two warps per quadrant, H/2 channels each: the fixed-point pool, tau -> f16 ->
+//   w13..w20  E2: two warps per quadrant, H/2 channels each: the fixed-point pool, tau -> f16 ->
 //             TMEM (the B MMA's A operand)
 // Software pipeline: acc1 is a 3-deep ring (issuer A runs up to 2 items ahead of issuer B),
 // acc2 2-deep; the tensor pipe orders nothing across the two issuers, so A writes acc1[j % 3]
 // only after layer 2 of item j-3 (its previous reader) has completed.  B of tile u is issued
-// by A before layer 1 of item last(u) + 4 (E2 has pooled the tile by then); the psi warps only
-// consume (doneB), so they never hold up the item pipeline.
+// by C once E2 has pooled the tile; the psi warps and C only consume, so they never hold up the
+// item pipeline.
 // Hand-offs are mbarriers; each waiter is provably at most one phase behind.
 #pragma once
 #include <cuda_bf16.h>
@@ -57,14 +58,14 @@ namespace gn {
 // Diagnostic build only (-DGN_TB_PROF): 32-bit clock() intervals accumulated in registers
 // (constant indices, so the array is scalarised), flushed once per role by one thread at the
 // role's end; summed over CTAs (glassnet_debug_tb_prof).  Indices: tools/tb_breakdown.py.
-__device__ unsigned long long gn_tb_prof[32];
-#define TBP_DECL() uint32_t tbp_acc[32] = {}
+__device__ unsigned long long gn_tb_prof[40];
+#define TBP_DECL() uint32_t tbp_acc[40] = {}
 #define TBP_NOW(v) const uint32_t v = (uint32_t)clock()
 #define TBP_ADD(i, a) (tbp_acc[i] += (uint32_t)clock() - (a))
 #define TBP_CNT(i, n) (tbp_acc[i] += (uint32_t)(n))
 #define TBP_FLUSH_IF(c)                                                              \
   if (c) {                                                                           \
-    _Pragma("unroll") for (int i_ = 0; i_ < 32; ++i_)                                \
+    _Pragma("unroll") for (int i_ = 0; i_ < 40; ++i_)                                \
       if (tbp_acc[i_]) atomicAdd(&gn_tb_prof[i_], (unsigned long long)tbp_acc[i_]); \
   }
 #else
@@ -190,19 +191,37 @@ struct TbLayout {
   // CP (K even, so every row's records start 4-byte aligned): each record is copied by 4-byte
   // cp.asyncs straight into its slot window, one tile ahead; otherwise halfword loads + stores
   static constexpr bool CP = K % 2 == 0;
-  static constexpr int NE = CP ? 6 : 5;               // E0 / meta ring (tiles the loader may run ahead)
+#ifndef GN_TB_NE
+#define GN_TB_NE 6
+#endif
+  static constexpr int NE = CP ? GN_TB_NE : 5;        // E0 / meta ring (tiles the loader may run ahead)
   static constexpr int OFF_A1 = (WIMG_B + 1023) / 1024 * 1024;
   static constexpr int REST = NE * E0_B + NE * META_B + 64 * 8 + 128 + 3072;
   static constexpr int LIMIT = 232448 - 1024;
   // A1 ring: as deep as shared memory allows (the loader runs further ahead over short tiles)
-  static constexpr int NA = OFF_A1 + 4 * A1_B + REST <= LIMIT ? 4 : OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;
+#ifndef GN_TB_NAMAX
+#define GN_TB_NAMAX 4
+#endif
+  static constexpr int NA = GN_TB_NAMAX >= 4 && OFF_A1 + 4 * A1_B + REST <= LIMIT ? 4 : OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;
   static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
   static constexpr int OFF_META = OFF_E0 + NE * E0_B;
   static constexpr int NBAR = 44;
   static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch, blend queue
   static constexpr int SMEM = OFF_MISC + 128;
-  static constexpr int NWARP = 24, THREADS = 32 * NWARP;   // 2 MMA issuers, 2 loader, 4 psi, 8 E1, 8 E2
+#ifndef GN_TB_LW
+#define GN_TB_LW 2
+#endif
+  // warps: 3 MMA issuers, LW loader, 4 psi, 4 E1, 8 E2 (the TMEM roles: warp % 4 = lane quadrant)
+#ifndef GN_TB_WA
+#define GN_TB_WA 0
+#define GN_TB_WB 1
+#define GN_TB_WC 2
+#endif
+  static constexpr int W_A = GN_TB_WA, W_B = GN_TB_WB, W_C = GN_TB_WC;   // warps 0..2, sub-partitions 0..2
+  static constexpr int LW = GN_TB_LW, W_LD = 3, W_PSI = W_LD + LW, W_E1 = W_PSI + 4, W_E2 = W_E1 + 4;
+  static constexpr int NWARP = W_E2 + 8, THREADS = 32 * NWARP;
+  static_assert(LW == 1 || LW == 2 || LW == 4, "loader warps");
   // TMEM columns: acc1 ring of 3 (A2 written over its first H/2 columns), acc2 ring of 2,
   // accB x 2, tau x 4 (f16 pairs; E2 writes tau(u) once B(u-4) has completed)
   static constexpr int T_ACC1 = 0, T_ACC2 = 3 * H, T_ACCB = 5 * H, T_TAU = 5 * H + 2 * C0;
@@ -247,6 +266,18 @@ __device__ __forceinline__ float fadd_sat(float a, float c) {
 // array in local memory)
 template <int V> struct TbInt { static constexpr int value = V; };
 
+// diagnostic builds only (-DGN_SENS=role, tools/tb_sens.sh): a busy wait of GN_SENS_CYC cycles in
+// one role's per-item (per-tile) path, to see which role the kernel's time is sensitive to
+#ifdef GN_SENS
+#ifndef GN_SENS_CYC
+#define GN_SENS_CYC 300
+#endif
+#define TB_SENS(role) \
+  if (GN_SENS == (role)) { const long long s0_ = clock64(); while (clock64() - s0_ < GN_SENS_CYC) { } }
+#else
+#define TB_SENS(role)
+#endif
+
 struct TbPh {
   uint32_t v = 0;
   __device__ __forceinline__ uint32_t operator[](int i) const { return (v >> i) & 1u; }
@@ -256,7 +287,7 @@ struct TbPh {
 #ifndef GN_TB_MAXNREG
 #define GN_TB_MAXNREG 80
 #endif
-// 24 warps, 6 per SM sub-partition: 80 registers x 32 x 24 = 61,440 of 65,536
+// 21 warps, at most 6 per SM sub-partition: 6 x 32 x 80 registers <= 16,384
 template <int K, int H, int C0, int POOL>
 __global__ void __maxnreg__(GN_TB_MAXNREG)
 k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, const uint16_t* __restrict__ direct,
@@ -266,20 +297,20 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t PL = S::PL;
   constexpr int NO = C0 + 3, NE = S::NE, NA = S::NA;
-  constexpr int LAGI = 4;   // B of tile u: issued by A before layer 1 of item last(u) + LAGI
   static_assert(C0 <= 32 && (H == 32 || H == 64), "TbParams sizes / epilogue chunks");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
-  uint64_t* tileReady = bars + 0;   // [NE] loader -> all (2 warp arrivals)
-  uint64_t* metaFree = bars + 6;    // [NE] psi (4) + E2 (8, counts read) -> loader
-  uint64_t* a1Free = bars + 40;     // [NA <= 4] E1 (8): the tile's last layer-1 MMA has completed -> loader
-  uint64_t* done1 = bars + 15;      // [3] issuer A's commit of layer 1 of item i -> E1
-  uint64_t* rdyA = bars + 18;       // [3] E1 (8) -> issuer B: A2 of item i in acc1[i % 3]
-  uint64_t* done2 = bars + 21;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
-  uint64_t* free2 = bars + 25;      // [2] E2 (8) -> issuer B: acc2[i % 2] read
-  uint64_t* tauRdy = bars + 27;     // [4] E2 (8) -> issuer A: tau of tile u in TMEM tau[u % 4]
-  uint64_t* doneB = bars + 31;      // [4] issuer A's commit of B(u) -> psi, E2 (tau[u % 4] reuse)
-  uint64_t* accBfree = bars + 35;   // [2] psi (4) -> issuer A: accB read
+  uint64_t* tileReady = bars + 0;   // [NE <= 8] loader -> all (2 warp arrivals)
+  uint64_t* metaFree = bars + 8;    // [NE] psi (4) + E2 (8, counts read) -> loader
+  uint64_t* done1 = bars + 16;      // [3] issuer A's commit of layer 1 of item i -> E1
+  uint64_t* rdyA = bars + 19;       // [3] E1 (4) -> issuer B: A2 of item i in acc1[i % 3]
+  uint64_t* done2 = bars + 22;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
+  uint64_t* free2 = bars + 26;      // [2] E2 (8) -> issuer B: acc2[i % 2] read
+  uint64_t* tauRdy = bars + 28;     // [4] E2 (8) -> issuer C: tau of tile u in TMEM tau[u % 4]
+  uint64_t* doneB = bars + 32;      // [4] issuer C's commit of B(u) -> psi, E2 (tau[u % 4] reuse)
+  uint64_t* accBfree = bars + 36;   // [2] psi (4) -> issuer C: accB read
+  uint64_t* a1Free = bars + 38;     // [NA <= 4] E1 (4): the tile's last layer-1 MMA has completed -> loader
+  static_assert(NE <= 8 && NA <= 4 && 42 <= S::NBAR, "barrier layout");
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_MISC);
   volatile int* lred = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 16);   // [2][4] warp max counts
   volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 64);    // [8] claimed tile ids
@@ -296,9 +327,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           make_uint2(0x3F803F80u, 0x00003F80u);
     }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, 2); tc::mbar_init(metaFree + i, 12); }
-    for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 8);
-    for (int i = 0; i < 3; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 8); }
+    for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, S::LW); tc::mbar_init(metaFree + i, 12); }
+    for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 4);
+    for (int i = 0; i < 3; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 4); }
     for (int i = 0; i < 4; ++i) tc::mbar_init(done2 + i, 1);
     for (int i = 0; i < 2; ++i) { tc::mbar_init(free2 + i, 8); tc::mbar_init(accBfree + i, 4); }
     for (int i = 0; i < 4; ++i) { tc::mbar_init(tauRdy + i, 8); tc::mbar_init(doneB + i, 1); }
@@ -313,7 +344,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   const uint32_t tmem = *tptr;
   const long ntiles = (P + TB_SBP - 1) / TB_SBP * TB_SBT;
 
-  if (warp <= 1) {
+  if (warp <= 2) {
     // ---------------------------------------------------------------- MMA issuers (one thread each):
     // A = layer 1 + B, B = layer 2.  One thread can issue a tcgen05.mma only every ~50 cycles;
     // two reach the N=64 pipe rate (tools/ubench_multi2.cu).  Across the two threads the
@@ -326,15 +357,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     constexpr uint32_t ID_T = tc::idesc_f16(128, H, 1, 1);
     constexpr uint32_t ID_BE = tc::idesc_f16(128, C0, 1, 1);
     constexpr uint32_t ID_BT = tc::idesc_f16(128, C0, 0, 0);
-    if (warp == 0 && lane == 0) {
-      // ------------------------------------------------ issuer A: layer 1 of every item, B of every tile
+    if (warp == S::W_A && lane == 0) {
+      // ------------------------------------------------ issuer A: layer 1 of every item
       const uint64_t dW1 = tc::smem_desc(sW1, H * 16, 128), dW1o = tc::smem_desc(sW1 + 2 * H * 16, H * 16, 128);
-      TbPh trph, d2ph, tph, bfph;
+      TbPh trph, d2ph;
       TBP_NOW(tot0);
       int ct = 0, cs = 0, cK = 0, nL1 = 0;
-      // blend queue (tile, due item): at most LAGI + 1 tiles pending (every tile has >= 1 item),
-      // registers with constant indices
-      int bqt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bqd[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bqn = 0;
       auto peek = [&](int t) -> int {   // wait for tile t's operands, return its Kt (-1: end)
         TBP_NOW(w0);
         tc::mbar_wait(tileReady + t % NE, trph[t % NE]); trph.flip(t % NE);
@@ -342,51 +370,13 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         TBP_CNT(19, 1);
         return *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
       };
-      auto blend = [&]() {   // B of the queue's front tile u: accB = e0 W_B,e0^T + tau W_B,tau^T
-        const int u = bqt[0];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) { bqt[k] = bqt[k + 1]; bqd[k] = bqd[k + 1]; }
-        --bqn;
-        const int ab = u & 1;
-        TBP_NOW(w0);
-        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);   // E2 read tile u-2's accB
-        tc::mbar_wait(tauRdy + (u & 3), tph[u & 3]); tph.flip(u & 3);   // E2 wrote tau(u)
-        TBP_ADD(3, w0);
-        tc::fence_after_sync();
-        TBP_NOW(bl0);
-        const uint32_t dB = tmem + S::T_ACCB + ab * C0;
-#pragma unroll
-        for (int q = 0; q < C0 / 16; ++q)
-          tc::mma_f16_ss(dB, tc::smem_desc(sE0 + (uint32_t)(u % NE) * S::E0_B + 2 * q * PL, PL, 128),
-                         tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
-#pragma unroll
-        for (int q = 0; q < H / 16; ++q)
-          tc::mma_f16_ts(dB, tmem + S::T_TAU + (u & 3) * (H / 2) + 8 * q,
-                         tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
-        tc::mma_commit(doneB + (u & 3));
-        TBP_ADD(23, bl0);
-      };
-      auto push_tile = [&](int t, int Kt) {   // due: LAGI items after the tile's last item
-        const int d = nL1 + Kt - 1 + LAGI;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k == bqn) { bqt[k] = t; bqd[k] = d; }
-        ++bqn;
-      };
       cK = peek(0);
-      if (cK >= 0) push_tile(0, cK);
       while (cK >= 0) {
-        // B of the tiles due now, BEFORE a possible wait for the loader (which may wait for these
-        // tiles' psi to free a meta slot)
-        TBP_NOW(bq0);
-        while (bqn > 0 && bqd[0] <= nL1) blend();
-        TBP_ADD(31, bq0);
         if (cs >= cK) {   // next tile (every tile has >= 1 item: Kt = max(1, max n))
           ++ct;
           cK = peek(ct);
           cs = 0;
           if (cK < 0) break;
-          push_tile(ct, cK);
         }
         if (nL1 >= 3) {   // acc1[nL1 % 3]'s previous reader, layer 2 of item nL1-3, has completed
           const int pb = (nL1 - 3) & 3;
@@ -395,6 +385,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           TBP_ADD(2, w1);
           tc::fence_after_sync();
         }
+        TB_SENS(1);
         TBP_NOW(l0);
         const uint32_t a = sA1 + (uint32_t)(ct % NA) * S::A1_B + (uint32_t)(2 * cs) * PL;
         tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H, tc::smem_desc(a, PL, 128),
@@ -415,11 +406,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       // extra arrival, or it would over-arrive an open phase
       for (int k = (nL1 >= 3 ? nL1 - 3 : 0); k < nL1; ++k) { tc::mbar_wait(done2 + (k & 3), d2ph[k & 3]); d2ph.flip(k & 3); }
       *total = nL1;
-      tc::mbar_arrive_cnt(rdyA + nL1 % 3, 8);
-      while (bqn > 0) blend();
+      tc::mbar_arrive_cnt(rdyA + nL1 % 3, 4);
       TBP_ADD(4, tot0);
       TBP_FLUSH_IF(true);
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == S::W_B && lane == 0) {
       // ------------------------------------------------ issuer B: layer 2 of every item
       TbPh aph, f2ph;
       TBP_NOW(tot0);
@@ -433,6 +423,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::mbar_wait(free2 + b, f2ph[b] ^ 1); f2ph.flip(b);         // E2 read acc2[b] (item i-2)
         TBP_ADD(11, w1);
         tc::fence_after_sync();
+        TB_SENS(2);
         const uint32_t d2 = tmem + S::T_ACC2 + b * H, a2 = tmem + S::T_ACC1 + a3 * H;
         TBP_NOW(l2a);
 #ifndef GN_ABL_L2
@@ -446,11 +437,42 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       }
       TBP_ADD(22, tot0);
       TBP_FLUSH_IF(true);
+    } else if (warp == S::W_C && lane == 0) {
+      // ------------------------------------------------ issuer C: B of every tile, as soon as E2 has
+      // written its tau: accB = e0 W_B,e0^T + tau W_B,tau^T.  Only the psi warps (accB) and E2 (the
+      // tau buffer, after B(u-4)) wait for it, so it never holds up the item chain.
+      TbPh trph, tph, bfph;
+      TBP_NOW(tot0);
+      for (int u = 0;; ++u) {
+        TBP_NOW(w0);
+        tc::mbar_wait(tileReady + u % NE, trph[u % NE]); trph.flip(u % NE);
+        if (*reinterpret_cast<volatile int*>(meta(u) + S::M_KT) < 0) break;
+        const int ab = u & 1;
+        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);      // psi read tile u-2's accB
+        tc::mbar_wait(tauRdy + (u & 3), tph[u & 3]); tph.flip(u & 3);   // E2 wrote tau(u)
+        TBP_ADD(3, w0);
+        tc::fence_after_sync();
+        TBP_NOW(bl0);
+        const uint32_t dB = tmem + S::T_ACCB + ab * C0;
+#pragma unroll
+        for (int q = 0; q < C0 / 16; ++q)
+          tc::mma_f16_ss(dB, tc::smem_desc(sE0 + (uint32_t)(u % NE) * S::E0_B + 2 * q * PL, PL, 128),
+                         tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
+#pragma unroll
+        for (int q = 0; q < H / 16; ++q)
+          tc::mma_f16_ts(dB, tmem + S::T_TAU + (u & 3) * (H / 2) + 8 * q,
+                         tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
+        tc::mma_commit(doneB + (u & 3));
+        TBP_ADD(23, bl0);
+      }
+      TBP_ADD(31, tot0);
+      TBP_FLUSH_IF(true);
     }
-  } else if (warp <= 3) {
+  } else if (warp < S::W_PSI) {
     // ---------------------------------------------------------------- loader
-    // 64 threads, pixel rows r0 and r0 + 64 of every tile
-    const int r0 = (warp - 2) * 32 + lane;
+    // LW warps, LR = 4 / LW pixel rows per thread: rows r0 + RS h of every tile
+    constexpr int LR = 4 / S::LW, RS = 32 * S::LW;
+    const int r0 = (warp - S::W_LD) * 32 + lane;
     const uint32_t sA1 = tc::smem_u32(smem + S::OFF_A1), sE0 = tc::smem_u32(smem + S::OFF_E0);
     TbPh mfph, afph;
     int claim = 0;
@@ -460,7 +482,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       ids[0] = atomicAdd(sched, 1); ids[1] = atomicAdd(sched, 1); ids[2] = atomicAdd(sched, 1);
       claim = atomicAdd(sched, 1);
     }
-    tc::bar_sync(1, 64);
+    tc::bar_sync(1, RS);
     auto perm_of = [&](long tl, int r) -> uint32_t { return tl < ntiles ? __ldg(perm + tl * 128 + r) : 0u; };
     auto decode = [&](long tl, uint32_t pe, long& p, int& m) {
       p = tl / TB_SBT * TB_SBP + (pe & 0xFFFF);
@@ -489,13 +511,13 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         cp_async16z(sE0 + (uint32_t)es * S::E0_B + j * PL + r * 16, es_src + 8 * j, p >= 0 ? 16u : 0u);
     };
     long tile = ids[0], ntile = ids[1];
-    uint32_t pe[2], npe[2];
+    uint32_t pe[LR], npe[LR];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) { pe[h] = perm_of(tile, r0 + 64 * h); npe[h] = perm_of(ntile, r0 + 64 * h); }
+    for (int h = 0; h < LR; ++h) { pe[h] = perm_of(tile, r0 + RS * h); npe[h] = perm_of(ntile, r0 + RS * h); }
     if constexpr (S::CP) {   // tile 0's copies (its operand slots are fresh: they count as waited)
       if (tile < ntiles)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) issue(tile, pe[h], r0 + 64 * h, 0, 0);
+        for (int h = 0; h < LR; ++h) issue(tile, pe[h], r0 + RS * h, 0, 0);
       cp_async_commit();
       mfph.flip(0);
       afph.flip(0);
@@ -515,10 +537,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         break;
       }
       TBP_NOW(ld0);
-      long p[2]; int m[2];
-      uint4 ev[2][C0 / 8];
+      long p[LR]; int m[LR];
+      uint4 ev[LR][C0 / 8];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) decode(tile, pe[h], p[h], m[h]);
+      for (int h = 0; h < LR; ++h) decode(tile, pe[h], p[h], m[h]);
       if constexpr (S::CP) {
         // the next tile's copies first (its E0 / meta slot: tile t+1-NE's consumers are done; its A1
         // buffer: tile t+1-NA's layer-1 MMAs are done), then this tile's (issued one iteration ago)
@@ -530,8 +552,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         TBP_ADD(6, w1);
         TBP_NOW(is0);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (ntile < ntiles) issue(ntile, npe[h], r0 + 64 * h, (t + 1) % NA, (t + 1) % NE);
+        for (int h = 0; h < LR; ++h) {
+          if (ntile < ntiles) issue(ntile, npe[h], r0 + RS * h, (t + 1) % NA, (t + 1) % NE);
         }
         cp_async_commit();
         TBP_ADD(30, is0);
@@ -540,7 +562,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         TBP_ADD(25, cw0);
       } else {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < LR; ++h) {
 #pragma unroll
           for (int j = 0; j < C0 / 8; ++j)
             ev[h][j] = p[h] >= 0 ? tb_ld_nc4(e0 + p[h] * C0 + 8 * j) : make_uint4(0, 0, 0, 0);
@@ -549,30 +571,38 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::mbar_wait(metaFree + e, mfph[e] ^ 1); mfph.flip(e);   // meta / E0 of tile t-NE
         TBP_ADD(5, w0);
       }
+      TBP_NOW(mt0);
       const long nntile = ids[(t + 2) & 7];   // written before the last bar.sync
-      uint32_t nnpe[2];
+      uint32_t nnpe[LR];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = r0 + 64 * h;
+      for (int h = 0; h < LR; ++h) {
+        const int r = r0 + RS * h;
         nnpe[h] = perm_of(nntile, r);
         reinterpret_cast<long long*>(M + S::M_PIX)[r] = p[h] >= 0 ? (long long)p[h] : -1ll;
         M[S::M_CNT + r] = (uint8_t)m[h];
       }
-      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)max(m[0], m[1]));
-      if (lane == 0) lred[(t & 1) * 4 + warp - 2] = wm;
+      int mm = m[0];
+#pragma unroll
+      for (int h = 1; h < LR; ++h) mm = max(mm, m[h]);
+      const int wm = __reduce_max_sync(0xFFFFFFFFu, (unsigned)mm);
+      if (lane == 0) lred[(t & 1) * 4 + warp - S::W_LD] = wm;
       if (r0 == 0) { ids[(t + 3) & 7] = claim; claim = atomicAdd(sched, 1); }
+      TBP_ADD(32, mt0);
       TBP_NOW(w2);
-      tc::bar_sync(1, 64);
+      tc::bar_sync(1, RS);
       TBP_ADD(8, w2);
+      TBP_NOW(zf0);
       // Kt >= 1 even for a tile of empty pixels (one item of zero records, pooled by nobody): every
       // tile then advances the item pipeline, which bounds how far a blocked consumer can lag
       // (deadlock freedom of the rings)
-      const int Kt = max(1, max(lred[(t & 1) * 4 + 0], lred[(t & 1) * 4 + 1]));
+      int Kt = 1;
+#pragma unroll
+      for (int w = 0; w < S::LW; ++w) Kt = max(Kt, (int)lred[(t & 1) * 4 + w]);
       if constexpr (S::CP) {
         // masked slots the tile's items reach: zero columns 0..11 (the constant columns stay)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + (r0 + 64 * h) * 16;
+        for (int h = 0; h < LR; ++h) {
+          const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + (r0 + RS * h) * 16;
           for (int k = m[h]; k < Kt; ++k) {
             tc::sts128(a1 + (uint32_t)(2 * k) * PL, 0u, 0u, 0u, 0u);
             asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a1 + (uint32_t)(2 * k + 1) * PL), "r"(0u), "r"(0u)
@@ -585,8 +615,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         tc::mbar_wait(a1Free + a, afph[a] ^ 1); afph.flip(a);     // A1 of tile t-NA
         TBP_ADD(6, w1);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = r0 + 64 * h;
+        for (int h = 0; h < LR; ++h) {
+          const int r = r0 + RS * h;
           const uint32_t a1 = sA1 + (uint32_t)a * S::A1_B + r * 16;
           const uint16_t* src = tbuf + (p[h] >= 0 ? p[h] : 0) * (K * 11);
           for (int k = 0; k < Kt; ++k) {
@@ -611,16 +641,20 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
             tc::sts128(sE0 + (uint32_t)e * S::E0_B + j * PL + r * 16, ev[h][j].x, ev[h][j].y, ev[h][j].z, ev[h][j].w);
         }
       }
+      TBP_ADD(33, zf0);
+      TBP_NOW(fe0);
       if (r0 == 0) *reinterpret_cast<volatile int*>(M + S::M_KT) = Kt;
+      TB_SENS(5);
       tc::fence_proxy_async();   // this thread's operand writes (and its waited cp.asyncs) -> async proxy
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tileReady + e);
+      TBP_ADD(34, fe0);
       TBP_ADD(26, ld0);
       tile = ntile; ntile = nntile;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) { pe[h] = npe[h]; npe[h] = nnpe[h]; }
+      for (int h = 0; h < LR; ++h) { pe[h] = npe[h]; npe[h] = nnpe[h]; }
     }
-  } else if (warp <= 7) {
+  } else if (warp < S::W_E1) {
     // ---------------------------------------------------------------- psi
     // one warp per TMEM lane quadrant, all C0 channels of accB: phi = ReLU(accB + b_B + w_Bn n),
     // psi = W_O,d0 phi + W_O,L L_d + b_O (reading R15).  Only consumes: waits for B(u)'s commit,
@@ -644,7 +678,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         for (int c = 0; c < 3; ++c) ldr[c] = __ldg(direct + p * 3 + c);
       TBP_NOW(w1);
       // one warp polls (sleeping between tries: psi is off the critical path), the four follow
-      if (warp == 4) tc::mbar_wait_sleep(doneB + (u & 3), dbph[u & 3], 256);
+      if (warp == S::W_PSI) tc::mbar_wait_sleep(doneB + (u & 3), dbph[u & 3], 256);
       dbph.flip(u & 3);
       tc::bar_sync(2, 128);
       TBP_ADD(28, w1);
@@ -670,76 +704,66 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       o0 = fmaf(WO[0 * NO + C0 + 0], ld0, o0); o0 = fmaf(WO[0 * NO + C0 + 1], ld1, o0); o0 = fmaf(WO[0 * NO + C0 + 2], ld2, o0);
       o1 = fmaf(WO[1 * NO + C0 + 0], ld0, o1); o1 = fmaf(WO[1 * NO + C0 + 1], ld1, o1); o1 = fmaf(WO[1 * NO + C0 + 2], ld2, o1);
       o2 = fmaf(WO[2 * NO + C0 + 0], ld0, o2); o2 = fmaf(WO[2 * NO + C0 + 1], ld1, o2); o2 = fmaf(WO[2 * NO + C0 + 2], ld2, o2);
+      TB_SENS(6);
       if (p >= 0) { psi[p * 3 + 0] = o0; psi[p * 3 + 1] = o1; psi[p * 3 + 2] = o2; }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(metaFree + e);
     }
     TBP_ADD(27, tot0);
-    TBP_FLUSH_IF(warp == 4 && lane == 0);
-  } else if (warp <= 15) {
+    TBP_FLUSH_IF(warp == S::W_PSI && lane == 0);
+  } else if (warp < S::W_E2) {
     // ---------------------------------------------------------------- E1: A2 = bf16(ReLU(acc1)) -> TMEM
-    // two warps per TMEM lane quadrant, H/2 channels each; half h writes its A2 (H/4 packed
-    // columns) over the first columns it has itself read: columns [h H/2, h H/2 + H/4).
+    // one warp per TMEM lane quadrant, the two channel halves in turn; half h writes its A2 (H/4
+    // packed columns) over the first columns it has itself read: columns [h H/2, h H/2 + H/4).
     constexpr int HC = H / 2;
     const int q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    // the half h as a compile-time constant (register-indexed TMEM column offsets)
-    auto e1 = [&](auto hc) {
-      constexpr int h = decltype(hc)::value;
-      TbPh trph, d1ph;
-      int i = 0;
-      TBP_NOW(tot0);
-      for (int t = 0;; ++t) {
-        const int e = t % NE;
-        TBP_NOW(w9);
-        tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
-        TBP_ADD(10, w9);
-        const int Kt = *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
-        if (Kt < 0) break;
+    TbPh trph, d1ph;
+    int i = 0;
+    TBP_NOW(tot0);
+    for (int t = 0;; ++t) {
+      const int e = t % NE;
+      TBP_NOW(w9);
+      tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
+      TBP_ADD(10, w9);
+      const int Kt = *reinterpret_cast<volatile int*>(meta(t) + S::M_KT);
+      if (Kt < 0) break;
 #pragma unroll 1
-        for (int s = 0; s < Kt; ++s) {
-          const int a3 = i % 3;
-          TBP_NOW(w0);
-          // one warp polls the barrier, the group of 8 E1 warps is released by a named barrier
-          if (warp == 8) tc::mbar_wait(done1 + a3, d1ph[a3]);
-          d1ph.flip(a3);
-          tc::bar_sync(6, 256);
-          TBP_ADD(9, w0);
-          TBP_NOW(w1);
-          tc::fence_after_sync();
-          if (s == Kt - 1 && lane == 0) tc::mbar_arrive(a1Free + t % NA);   // the tile's layer-1 MMAs are done
+      for (int s = 0; s < Kt; ++s) {
+        const int a3 = i % 3;
+        TBP_NOW(w0);
+        // one warp polls the barrier, the group of 4 E1 warps is released by a named barrier
+        if (warp == S::W_E1) tc::mbar_wait(done1 + a3, d1ph[a3]);
+        d1ph.flip(a3);
+        tc::bar_sync(6, 128);
+        TBP_ADD(9, w0);
+        TBP_NOW(w1);
+        tc::fence_after_sync();
+        if (s == Kt - 1 && lane == 0) tc::mbar_arrive(a1Free + t % NA);   // the tile's layer-1 MMAs are done
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
           const uint32_t ta = tmem + lane_off + S::T_ACC1 + a3 * H + h * HC;
           uint32_t u[HC], o[HC / 2];
-#ifdef GN_ABL_TMEM
-#pragma unroll
-          for (int k = 0; k < HC; ++k) u[k] = (uint32_t)(lane + k);
-#else
           if constexpr (HC == 32) tc::tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(u));
           else tc::tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(u));
           tc::tmem_ld_wait();
-#endif
 #pragma unroll
           for (int k = 0; k < HC / 2; ++k)
             o[k] = tc::cvt_relu_bf16x2(__uint_as_float(u[2 * k]), __uint_as_float(u[2 * k + 1]));
-#ifndef GN_ABL_TMEM
           if constexpr (HC == 32) tc::tmem_st16(ta, o);
           else tc::tmem_st8(ta, o);
-          tc::tmem_st_wait();
-#else
-          if (o[0] == 0x12345678u && lane == 99) psi[0] = 0.f;
-#endif
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(rdyA + a3);
-          TBP_ADD(16, w1);
-          ++i;
         }
+        tc::tmem_st_wait();
+        tc::fence_before_sync();
+        __syncwarp();
+        TB_SENS(3);
+        if (lane == 0) tc::mbar_arrive(rdyA + a3);
+        TBP_ADD(16, w1);
+        ++i;
       }
-      TBP_ADD(12, tot0);
-    };
-    if (warp < 12) e1(TbInt<0>{});
-    else e1(TbInt<1>{});
-    TBP_FLUSH_IF(warp == 8 && lane == 0);
+    }
+    TBP_ADD(12, tot0);
+    TBP_FLUSH_IF(warp == S::W_E1 && lane == 0);
   } else {
     // ---------------------------------------------------------------- E2: the pool, tau
     constexpr int HC = H / 2;   // channels per warp
@@ -765,7 +789,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         for (int s = 0; s < Kt; ++s) {
           const int b = i & 1;
           TBP_NOW(w0);
-          if (warp == 16) tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // one warp polls, the
+          if (warp == S::W_E2) tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // one warp polls, the
           d2ph.flip(i & 3);                                               // group of 8 follows
           tc::bar_sync(7, 256);
           TBP_ADD(13, w0);
@@ -799,6 +823,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
               pool[j + 1] += __float_as_uint(w.y);
             }
           }
+          TB_SENS(4);
           ++i;
           TBP_ADD(17, w1);
         }
@@ -823,9 +848,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         }
       }
       TBP_ADD(15, tot0);
-      TBP_FLUSH_IF(warp == 16 && lane == 0);
+      TBP_FLUSH_IF(warp == S::W_E2 && lane == 0);
     };
-    if (warp < 20) e2(TbInt<0>{});
+    if (warp < S::W_E2 + 4) e2(TbInt<0>{});
     else e2(TbInt<1>{});
   }
   tc::fence_before_sync();

@@ -23,7 +23,7 @@ net = GlassNet(w, make_dims(cfg.height, cfg.width, cfg.k_slots, cfg.widths, cfg.
 g, d, t, n = device.alloc_and_fill(cfg)
 L = gb.lib()
 L.glassnet_debug_tb_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 32)()
+buf = (ctypes.c_ulonglong * 40)()
 net.forward(g, d, t, n)
 L.glassnet_debug_tb_prof(buf, 1)
 net.forward(g, d, t, n)
@@ -32,11 +32,12 @@ L.glassnet_debug_tb_prof(buf, 1)
 v = list(buf)
 ctas = 148
 tiles, items = v[19], v[18]
-names = {0: "A wait tileReady", 2: "A wait done2 (acc1 slot)", 3: "A blend waits", 20: "A layer1 issue+commit",
-         23: "A blend issue", 31: "A due blends (all)", 4: "A total",
+names = {0: "A wait tileReady", 2: "A wait done2 (acc1 slot)", 20: "A layer1 issue+commit", 4: "A total",
+         3: "C waits (tile, accB, tau)", 23: "C B issue", 31: "C total",
          1: "B wait rdyA", 11: "B wait free2", 21: "B layer2 issue+commit", 22: "B total",
          5: "loader wait metaFree", 6: "loader wait a1Free", 7: "loader total", 8: "loader bar.sync",
-         30: "loader issue next tile", 25: "loader cp.async wait", 26: "loader tile (all)",
+         30: "loader issue next tile", 25: "loader cp.async wait", 32: "loader meta + decode",
+         33: "loader zero-fill", 34: "loader fence + hand-over", 26: "loader tile (all)",
          9: "E1 wait done1", 10: "E1 wait tileReady", 12: "E1 total", 16: "E1 item work",
          27: "psi total", 28: "psi wait doneB", 29: "psi wait tileReady",
          13: "E2 wait done2", 14: "E2 wait doneB (tau reuse)", 15: "E2 total", 17: "E2 item work", 24: "E2 tmem ld+wait"}
