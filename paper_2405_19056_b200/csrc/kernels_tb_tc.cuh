@@ -205,7 +205,7 @@ struct TbLayout {
   static constexpr int NA = GN_TB_NAMAX >= 4 && OFF_A1 + 4 * A1_B + REST <= LIMIT ? 4 : OFF_A1 + 3 * A1_B + REST <= LIMIT ? 3 : 2;
   static constexpr int OFF_E0 = OFF_A1 + NA * A1_B;
   static constexpr int OFF_META = OFF_E0 + NE * E0_B;
-  static constexpr int NBAR = 44;
+  static constexpr int NBAR = 46;
   static constexpr int OFF_BAR = (OFF_META + NE * META_B + 15) / 16 * 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;   // tmem ptr, loader scratch, blend queue
   static constexpr int SMEM = OFF_MISC + 128;
@@ -224,8 +224,14 @@ struct TbLayout {
   static_assert(LW == 1 || LW == 2 || LW == 4, "loader warps");
   // TMEM columns: acc1 ring of 3 (A2 written over its first H/2 columns), acc2 ring of 2,
   // accB x 2, tau x 4 (f16 pairs; E2 writes tau(u) once B(u-4) has completed)
-  static constexpr int T_ACC1 = 0, T_ACC2 = 3 * H, T_ACCB = 5 * H, T_TAU = 5 * H + 2 * C0;
-  static_assert(T_TAU + 4 * (H / 2) <= 512, "TMEM");
+#ifndef GN_TB_NACC2
+#define GN_TB_NACC2 2
+#define GN_TB_NACCB 2
+#define GN_TB_NTAU 4
+#endif
+  static constexpr int NACC2 = GN_TB_NACC2, NACCB = GN_TB_NACCB, NTAU = GN_TB_NTAU;
+  static constexpr int T_ACC1 = 0, T_ACC2 = 3 * H, T_ACCB = T_ACC2 + NACC2 * H, T_TAU = T_ACCB + NACCB * C0;
+  static_assert(T_TAU + NTAU * (H / 2) <= 512 && NACC2 <= 4 && NACCB <= 2 && NTAU <= 4, "TMEM");
   static_assert(SMEM <= LIMIT, "shared memory");
 };
 
@@ -305,12 +311,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   uint64_t* done1 = bars + 16;      // [3] issuer A's commit of layer 1 of item i -> E1
   uint64_t* rdyA = bars + 19;       // [3] E1 (4) -> issuer B: A2 of item i in acc1[i % 3]
   uint64_t* done2 = bars + 22;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
-  uint64_t* free2 = bars + 26;      // [2] E2 (8) -> issuer B: acc2[i % 2] read
+  uint64_t* free2 = bars + 42;      // [NACC2 <= 4] E2 (8) -> issuer B: acc2[i % NACC2] read
   uint64_t* tauRdy = bars + 28;     // [4] E2 (8) -> issuer C: tau of tile u in TMEM tau[u % 4]
   uint64_t* doneB = bars + 32;      // [4] issuer C's commit of B(u) -> psi, E2 (tau[u % 4] reuse)
   uint64_t* accBfree = bars + 36;   // [2] psi (4) -> issuer C: accB read
   uint64_t* a1Free = bars + 38;     // [NA <= 4] E1 (4): the tile's last layer-1 MMA has completed -> loader
-  static_assert(NE <= 8 && NA <= 4 && 42 <= S::NBAR, "barrier layout");
+  static_assert(NE <= 8 && NA <= 4 && 46 <= S::NBAR, "barrier layout");
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_MISC);
   volatile int* lred = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 16);   // [2][4] warp max counts
   volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 64);    // [8] claimed tile ids
@@ -331,7 +337,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 4);
     for (int i = 0; i < 3; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 4); }
     for (int i = 0; i < 4; ++i) tc::mbar_init(done2 + i, 1);
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(free2 + i, 8); tc::mbar_init(accBfree + i, 4); }
+    for (int i = 0; i < S::NACC2; ++i) tc::mbar_init(free2 + i, 8);
+    for (int i = 0; i < S::NACCB; ++i) tc::mbar_init(accBfree + i, 4);
     for (int i = 0; i < 4; ++i) { tc::mbar_init(tauRdy + i, 8); tc::mbar_init(doneB + i, 1); }
     *total = 0x7FFFFFFF;
     tc::fence_mbar_init();
@@ -414,7 +421,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       TbPh aph, f2ph;
       TBP_NOW(tot0);
       for (int i = 0;; ++i) {
-        const int a3 = i % 3, b = i & 1;
+        const int a3 = i % 3, b = i % S::NACC2;
         TBP_NOW(w0);
         tc::mbar_wait(rdyA + a3, aph[a3]); aph.flip(a3);             // A2 of item i in acc1[i % 3]
         TBP_ADD(1, w0);
@@ -447,11 +454,12 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         TBP_NOW(w0);
         tc::mbar_wait(tileReady + u % NE, trph[u % NE]); trph.flip(u % NE);
         if (*reinterpret_cast<volatile int*>(meta(u) + S::M_KT) < 0) break;
-        const int ab = u & 1;
-        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);      // psi read tile u-2's accB
+        const int ab = u % S::NACCB;
+        tc::mbar_wait(accBfree + ab, bfph[ab] ^ 1); bfph.flip(ab);      // psi read tile u-NACCB's accB
         tc::mbar_wait(tauRdy + (u & 3), tph[u & 3]); tph.flip(u & 3);   // E2 wrote tau(u)
         TBP_ADD(3, w0);
         tc::fence_after_sync();
+        TB_SENS(7);
         TBP_NOW(bl0);
         const uint32_t dB = tmem + S::T_ACCB + ab * C0;
 #pragma unroll
@@ -460,7 +468,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
                          tc::smem_desc(sWBE + 2 * q * C0 * 16, C0 * 16, 128), ID_BE, q > 0);
 #pragma unroll
         for (int q = 0; q < H / 16; ++q)
-          tc::mma_f16_ts(dB, tmem + S::T_TAU + (u & 3) * (H / 2) + 8 * q,
+          tc::mma_f16_ts(dB, tmem + S::T_TAU + (u % S::NTAU) * (H / 2) + 8 * q,
                          tc::smem_desc(sWBT + 2 * q * C0 * 16, C0 * 16, 128), ID_BT, 1);
         tc::mma_commit(doneB + (u & 3));
         TBP_ADD(23, bl0);
@@ -664,7 +672,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
     TbPh trph, dbph;
     TBP_NOW(tot0);
     for (int u = 0;; ++u) {
-      const int e = u % NE, ab = u & 1;
+      const int e = u % NE, ab = u % S::NACCB;
       TBP_NOW(w0);
       tc::mbar_wait(tileReady + e, trph[e]); trph.flip(e);
       TBP_ADD(29, w0);
@@ -787,11 +795,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         for (int j = 0; j < HC; ++j) pool[j] = 0;
 #pragma unroll 1
         for (int s = 0; s < Kt; ++s) {
-          const int b = i & 1;
+          const int b = i % S::NACC2;
           TBP_NOW(w0);
-          if (warp == S::W_E2) tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // one warp polls, the
-          d2ph.flip(i & 3);                                               // group of 8 follows
-          tc::bar_sync(7, 256);
+          tc::mbar_wait(done2 + (i & 3), d2ph[i & 3]);   // every E2 warp polls (no named-barrier hop)
+          d2ph.flip(i & 3);
           TBP_ADD(13, w0);
           TBP_NOW(w1);
           tc::fence_after_sync();
@@ -801,6 +808,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
 #pragma unroll
           for (int k = 0; k < HC; ++k) u[k] = (uint32_t)(lane + k + ta);
 #else
+          if constexpr (HC == 32) tc::tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(u));
+          else
 #pragma unroll
           for (int c = 0; c < HC / 16; ++c) tc::tmem_ld16(ta + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(u + 16 * c));
           tc::tmem_ld_wait();
@@ -829,7 +838,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         }
         // tau(t) -> TMEM, once B of tile t-4 (the last reader of this tau buffer) has completed
         TBP_NOW(w5);
-        if (t >= 4) { tc::mbar_wait(doneB + (t & 3), dbph[t & 3]); dbph.flip(t & 3); }
+        if (t >= S::NTAU) {   // the last reader of this tau buffer, B(t - NTAU), has completed
+          const int uo = (t - S::NTAU) & 3;
+          tc::mbar_wait(doneB + uo, dbph[uo]); dbph.flip(uo);
+        }
         TBP_ADD(14, w5);
         {
           const uint32_t off = (uint32_t)m * TB_ONE_BITS;
@@ -838,7 +850,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
 #pragma unroll
           for (int j = 0; j < HC / 2; ++j)
             o[j] = tc::cvt_relu_f16x2((float)(pool[2 * j] - off) * sc, (float)(pool[2 * j + 1] - off) * sc);
-          const uint32_t tt = tmem + lane_off + S::T_TAU + (t & 3) * (H / 2) + h * (HC / 2);
+          const uint32_t tt = tmem + lane_off + S::T_TAU + (t % S::NTAU) * (H / 2) + h * (HC / 2);
           if constexpr (HC / 2 == 16) tc::tmem_st16(tt, o);
           else tc::tmem_st8(tt, o);
           tc::tmem_st_wait();
