@@ -39,9 +39,9 @@
 //             INTO acc1 (layer 2 reads its A operand from TMEM)
 //   w13..w20  E2: two warps per quadrant, H/2 channels each: the fixed-point pool, tau -> f16 ->
 //             TMEM (the B MMA's A operand)
-// Software pipeline: acc1 is a 3-deep ring (issuer A runs up to 2 items ahead of issuer B),
-// acc2 2-deep; the tensor pipe orders nothing across the two issuers, so A writes acc1[j % 3]
-// only after layer 2 of item j-3 (its previous reader) has completed.  B of tile u is issued
+// Software pipeline: acc1 is a NACC1-deep ring (issuer A runs up to NACC1 - 1 items ahead of
+// issuer B), acc2 NACC2-deep; the tensor pipe orders nothing across the issuers, so A writes
+// acc1[j % NACC1] only after layer 2 of item j - NACC1 (its previous reader) has completed.  B of tile u is issued
 // by C once E2 has pooled the tile; the psi warps and C only consume, so they never hold up the
 // item pipeline.
 // Hand-offs are mbarriers; each waiter is provably at most one phase behind.
@@ -222,16 +222,17 @@ struct TbLayout {
   static constexpr int LW = GN_TB_LW, W_LD = 3, W_PSI = W_LD + LW, W_E1 = W_PSI + 4, W_E2 = W_E1 + 4;
   static constexpr int NWARP = W_E2 + 8, THREADS = 32 * NWARP;
   static_assert(LW == 1 || LW == 2 || LW == 4, "loader warps");
-  // TMEM columns: acc1 ring of 3 (A2 written over its first H/2 columns), acc2 ring of 2,
-  // accB x 2, tau x 4 (f16 pairs; E2 writes tau(u) once B(u-4) has completed)
-#ifndef GN_TB_NACC2
+  // TMEM columns: acc1 ring of 4 (A2 written over its first H/2 columns), acc2 ring of 2,
+  // accB x 1, tau x 3 (f16 pairs; E2 writes tau(u) once B(u-3) has completed)
+#ifndef GN_TB_NACC1   // (diagnostic builds may override the ring sizes; the TMEM budget is checked below)
+#define GN_TB_NACC1 4
 #define GN_TB_NACC2 2
-#define GN_TB_NACCB 2
-#define GN_TB_NTAU 4
+#define GN_TB_NACCB 1
+#define GN_TB_NTAU 3
 #endif
-  static constexpr int NACC2 = GN_TB_NACC2, NACCB = GN_TB_NACCB, NTAU = GN_TB_NTAU;
-  static constexpr int T_ACC1 = 0, T_ACC2 = 3 * H, T_ACCB = T_ACC2 + NACC2 * H, T_TAU = T_ACCB + NACCB * C0;
-  static_assert(T_TAU + NTAU * (H / 2) <= 512 && NACC2 <= 4 && NACCB <= 2 && NTAU <= 4, "TMEM");
+  static constexpr int NACC1 = GN_TB_NACC1, NACC2 = GN_TB_NACC2, NACCB = GN_TB_NACCB, NTAU = GN_TB_NTAU;
+  static constexpr int T_ACC1 = 0, T_ACC2 = NACC1 * H, T_ACCB = T_ACC2 + NACC2 * H, T_TAU = T_ACCB + NACCB * C0;
+  static_assert(T_TAU + NTAU * (H / 2) <= 512 && NACC1 <= 4 && NACC2 <= 4 && NACCB <= 2 && NTAU <= 4, "TMEM");
   static_assert(SMEM <= LIMIT, "shared memory");
 };
 
@@ -308,15 +309,16 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
   uint64_t* tileReady = bars + 0;   // [NE <= 8] loader -> all (2 warp arrivals)
   uint64_t* metaFree = bars + 8;    // [NE] psi (4) + E2 (8, counts read) -> loader
-  uint64_t* done1 = bars + 16;      // [3] issuer A's commit of layer 1 of item i -> E1
-  uint64_t* rdyA = bars + 19;       // [3] E1 (4) -> issuer B: A2 of item i in acc1[i % 3]
-  uint64_t* done2 = bars + 22;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
-  uint64_t* free2 = bars + 42;      // [NACC2 <= 4] E2 (8) -> issuer B: acc2[i % NACC2] read
-  uint64_t* tauRdy = bars + 28;     // [4] E2 (8) -> issuer C: tau of tile u in TMEM tau[u % 4]
-  uint64_t* doneB = bars + 32;      // [4] issuer C's commit of B(u) -> psi, E2 (tau[u % 4] reuse)
-  uint64_t* accBfree = bars + 36;   // [2] psi (4) -> issuer C: accB read
+  uint64_t* done1 = bars + 16;      // [NACC1] issuer A's commit of layer 1 of item i -> E1
+  uint64_t* rdyA = bars + 20;       // [NACC1] E1 (4) -> issuer B: A2 of item i in acc1[i % NACC1]
+  uint64_t* done2 = bars + 24;      // [4] issuer B's commit of layer 2 of item i -> E2, issuer A
+  uint64_t* tauRdy = bars + 28;     // [4] E2 (8) -> issuer C: tau of tile u in TMEM tau[u % NTAU]
+  uint64_t* doneB = bars + 32;      // [4] issuer C's commit of B(u) -> psi, E2 (tau[u % NTAU] reuse)
+  uint64_t* accBfree = bars + 36;   // [NACCB] psi (4) -> issuer C: accB[u % NACCB] read
   uint64_t* a1Free = bars + 38;     // [NA <= 4] E1 (4): the tile's last layer-1 MMA has completed -> loader
+  uint64_t* free2 = bars + 42;      // [NACC2 <= 4] E2 (8) -> issuer B: acc2[i % NACC2] read
   static_assert(NE <= 8 && NA <= 4 && 46 <= S::NBAR, "barrier layout");
+  constexpr int NACC1 = S::NACC1;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + S::OFF_MISC);
   volatile int* lred = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 16);   // [2][4] warp max counts
   volatile int* ids = reinterpret_cast<volatile int*>(smem + S::OFF_MISC + 64);    // [8] claimed tile ids
@@ -335,7 +337,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
   if (threadIdx.x == 0) {
     for (int i = 0; i < NE; ++i) { tc::mbar_init(tileReady + i, S::LW); tc::mbar_init(metaFree + i, 12); }
     for (int i = 0; i < NA; ++i) tc::mbar_init(a1Free + i, 4);
-    for (int i = 0; i < 3; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 4); }
+    for (int i = 0; i < NACC1; ++i) { tc::mbar_init(done1 + i, 1); tc::mbar_init(rdyA + i, 4); }
     for (int i = 0; i < 4; ++i) tc::mbar_init(done2 + i, 1);
     for (int i = 0; i < S::NACC2; ++i) tc::mbar_init(free2 + i, 8);
     for (int i = 0; i < S::NACCB; ++i) tc::mbar_init(accBfree + i, 4);
@@ -353,10 +355,10 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
 
   if (warp <= 2) {
     // ---------------------------------------------------------------- MMA issuers (one thread each):
-    // A = layer 1 + B, B = layer 2.  One thread can issue a tcgen05.mma only every ~50 cycles;
-    // two reach the N=64 pipe rate (tools/ubench_multi2.cu).  Across the two threads the
-    // tensor pipe gives no ordering, so A issues layer 1 of item j into acc1[j % 3] only after
-    // layer 2 of item j-3 (its previous reader) has COMPLETED (done2 commit).
+    // A = layer 1, B = layer 2, C = the tile-level B.  One thread can issue a tcgen05.mma only
+    // every ~50 cycles; two reach the N=64 pipe rate (tools/ubench_multi2.cu).  Across the threads
+    // the tensor pipe gives no ordering, so A issues layer 1 of item j into acc1[j % NACC1] only
+    // after layer 2 of item j - NACC1 (its previous reader) has COMPLETED (done2 commit).
     const uint32_t sW1 = tc::smem_u32(smem + S::OFF_W1), sW2 = tc::smem_u32(smem + S::OFF_W2);
     const uint32_t sWBE = tc::smem_u32(smem + S::OFF_WBE), sWBT = tc::smem_u32(smem + S::OFF_WBT);
     const uint32_t sW1E = tc::smem_u32(smem + S::OFF_W1E);
@@ -385,8 +387,8 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
           cs = 0;
           if (cK < 0) break;
         }
-        if (nL1 >= 3) {   // acc1[nL1 % 3]'s previous reader, layer 2 of item nL1-3, has completed
-          const int pb = (nL1 - 3) & 3;
+        if (nL1 >= NACC1) {   // acc1[nL1 % NACC1]'s previous reader, layer 2 of item nL1-NACC1, has completed
+          const int pb = (nL1 - NACC1) & 3;
           TBP_NOW(w1);
           tc::mbar_wait(done2 + pb, d2ph[pb]); d2ph.flip(pb);
           TBP_ADD(2, w1);
@@ -395,15 +397,15 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
         TB_SENS(1);
         TBP_NOW(l0);
         const uint32_t a = sA1 + (uint32_t)(ct % NA) * S::A1_B + (uint32_t)(2 * cs) * PL;
-        tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H, tc::smem_desc(a, PL, 128),
+        tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % NACC1) * H, tc::smem_desc(a, PL, 128),
                        (S::CP && (cs & 1)) ? dW1o : dW1, ID_T, 0);
         if (prm.sigma)   // N1: + e0 W1,sigma^T, the same two MMAs for every slot of the pixel
 #pragma unroll
           for (int q = 0; q < C0 / 16; ++q)
-            tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % 3) * H,
+            tc::mma_f16_ss(tmem + S::T_ACC1 + (nL1 % NACC1) * H,
                            tc::smem_desc(sE0 + (uint32_t)(ct % NE) * S::E0_B + 2 * q * PL, PL, 128),
                            tc::smem_desc(sW1E + 2 * q * H * 16, H * 16, 128), ID_T, 1);
-        tc::mma_commit(done1 + nL1 % 3);
+        tc::mma_commit(done1 + nL1 % NACC1);
         TBP_ADD(20, l0);
         TBP_CNT(18, 1);
         ++nL1; ++cs;
@@ -411,9 +413,9 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       // wake issuer B, which waits for rdyA of item nL1 (it does not exist): first let layer 2 of
       // the last items complete -- their rdyA phases must be fully arrived by E1 before this
       // extra arrival, or it would over-arrive an open phase
-      for (int k = (nL1 >= 3 ? nL1 - 3 : 0); k < nL1; ++k) { tc::mbar_wait(done2 + (k & 3), d2ph[k & 3]); d2ph.flip(k & 3); }
+      for (int k = (nL1 >= NACC1 ? nL1 - NACC1 : 0); k < nL1; ++k) { tc::mbar_wait(done2 + (k & 3), d2ph[k & 3]); d2ph.flip(k & 3); }
       *total = nL1;
-      tc::mbar_arrive_cnt(rdyA + nL1 % 3, 4);
+      tc::mbar_arrive_cnt(rdyA + nL1 % NACC1, 4);
       TBP_ADD(4, tot0);
       TBP_FLUSH_IF(true);
     } else if (warp == S::W_B && lane == 0) {
@@ -421,7 +423,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       TbPh aph, f2ph;
       TBP_NOW(tot0);
       for (int i = 0;; ++i) {
-        const int a3 = i % 3, b = i % S::NACC2;
+        const int a3 = i % NACC1, b = i % S::NACC2;
         TBP_NOW(w0);
         tc::mbar_wait(rdyA + a3, aph[a3]); aph.flip(a3);             // A2 of item i in acc1[i % 3]
         TBP_ADD(1, w0);
@@ -738,7 +740,7 @@ k_tb_tc(const uint16_t* __restrict__ tbuf, const uint16_t* __restrict__ e0, cons
       if (Kt < 0) break;
 #pragma unroll 1
       for (int s = 0; s < Kt; ++s) {
-        const int a3 = i % 3;
+        const int a3 = i % NACC1;
         TBP_NOW(w0);
         // one warp polls the barrier, the group of 4 E1 warps is released by a named barrier
         if (warp == S::W_E1) tc::mbar_wait(done1 + a3, d1ph[a3]);
