@@ -12,6 +12,9 @@ Parity status per function:
               weights = the unconditioned network, bitwise) and P16 (records with zero weights:
               every fragment is h(sigma), n = 2 gives exactly 2 h(sigma)) and P10 (torch-fp64)
   og_forward  pinned (P10 torch-fp64 composition, P11 homogeneity, P13 tiles, P14 shift)
+  og_supersample (N3) pinned (PS1 identity residual = nearest up-sampling, PS2 constant residual
+              = clamp(u + beta), PS3 torch-fp64 composition (interpolate nearest + conv2d),
+              PS4 receptive field: a coarse pixel reaches only hi-res pixels within 2 of its block)
 """
 from __future__ import annotations
 
@@ -60,6 +63,9 @@ def lib():
         _lib.og_conv3x3.restype = None
         _lib.og_up2.restype = None
         _lib.og_T_pixel.restype = None
+        _lib.og_ss_weight_count.restype = ctypes.c_size_t
+        _lib.og_ss_weight_count.argtypes = [ctypes.c_int]
+        _lib.og_supersample.restype = ctypes.c_int
     return _lib
 
 
@@ -191,5 +197,38 @@ def split_weights(d: Dims, weights):
         take(f"R{l}.W", (c[l - 1], 3, 3, c[l])); take(f"R{l}.b", (c[l - 1],))
     nO = c[0] + (3 if d.r_takes_ld else 0)
     take("O.W", (3, nO)); take("O.b", (3,))
+    assert p == w.size
+    return out
+
+
+def ss_weight_count(s: int) -> int:
+    return int(lib().og_ss_weight_count(int(s)))
+
+
+def supersample(s, weights_ss, img, gbuf_hi, input_norm=True):
+    """N3 super-sampler S of one frame (or a batch): img [H][W][3], gbuf_hi [2H][2W][12] ->
+    out [2H][2W][3] fp64 (glassnet_oracle.c og_supersample; reading N3)."""
+    img = np.asarray(img)
+    if img.ndim == 4:
+        return np.stack([supersample(s, weights_ss, img[b], gbuf_hi[b], input_norm) for b in range(img.shape[0])])
+    H, W, _ = img.shape
+    w, im, g = _c64(weights_ss), _c64(img), _c64(gbuf_hi)
+    assert w.size == ss_weight_count(s), (w.size, ss_weight_count(s))
+    assert im.shape == (H, W, 3) and g.shape == (2 * H, 2 * W, 12)
+    out = np.zeros((2 * H, 2 * W, 3))
+    rc = lib().og_supersample(H, W, int(s), int(bool(input_norm)), _ptr(w), _ptr(im), _ptr(g), _ptr(out))
+    if rc != 0:
+        raise RuntimeError(f"og_supersample failed rc={rc}")
+    return out
+
+
+def split_ss_weights(s, weights_ss):
+    w = _c64(weights_ss)
+    out, p = {}, 0
+    for name, shape in (("S1.W", (s, 3, 3, 15)), ("S1.b", (s,)), ("S2.W", (s, 3, 3, s)), ("S2.b", (s,)),
+                        ("S3.W", (3, s)), ("S3.b", (3,))):
+        n = int(np.prod(shape))
+        out[name] = w[p:p + n].reshape(shape)
+        p += n
     assert p == w.size
     return out

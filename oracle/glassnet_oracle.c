@@ -265,3 +265,57 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
   for (int l = 0; l < 4; ++l) { free(dbuf[l]); free(ybuf[l]); }
   return 0;
 }
+
+/* ---- N3: the x2 super-sampling network S (§3.4 P:384-389 "a
+ * multi-layer CNN is used as a super-sampling network that super-samples the result at x2
+ * the original resolution", P:387-389 high-resolution G-buffers are cheap to rasterise;
+ * the architecture is unspecified, so SPEC.md's form: the nearest-upsampled
+ * image concatenated with the hi-res G-buffer channels -> a shallow CNN -> a residual added
+ * to the upsampled image).  DESIGN.md reading N3:
+ *   u   = up_nearest(img)                    u[Y][X] = img[Y/2][X/2]          (2H x 2W x 3)
+ *   x   = [G'_hi, u]                         G' normalised as in step 1 (R9)  (15 ch)
+ *   s1  = ReLU(conv3x3_s1(x;  S1))           15 -> s
+ *   s2  = ReLU(conv3x3_s1(s1; S2))           s  -> s
+ *   r   = S3.W s2 + S3.b                     1x1, s -> 3
+ *   out = clamp(u + r, 0, 1)                 the display image in GlassNet's [0,1] range
+ * Weights (fp64, blob order): S1.W[s][3][3][15] S1.b[s] S2.W[s][3][3][s] S2.b[s] S3.W[3][s] S3.b[3].
+ * img [H][W][3], gbuf_hi [2H][2W][12], out [2H][2W][3].  Returns 0 on success. */
+size_t og_ss_weight_count(int s) { return (size_t)s * 9 * 15 + s + (size_t)s * 9 * s + s + (size_t)3 * s + 3; }
+
+int og_supersample(int H, int W, int s, int input_norm, const double* wts, const double* img,
+                   const double* gbuf_hi, double* out) {
+  if (H < 1 || W < 1 || s < 1) return 1;
+  const int H2 = 2 * H, W2 = 2 * W;
+  const size_t P2 = (size_t)H2 * W2;
+  const double* p = wts;
+  const double* S1W = p; p += (size_t)s * 9 * 15; const double* S1b = p; p += s;
+  const double* S2W = p; p += (size_t)s * 9 * s;  const double* S2b = p; p += s;
+  const double* S3W = p; p += (size_t)3 * s;      const double* S3b = p;
+  double* x = (double*)malloc(sizeof(double) * P2 * 15);
+  double* u = (double*)malloc(sizeof(double) * P2 * 3);
+  double* s1 = (double*)malloc(sizeof(double) * P2 * s);
+  double* s2 = (double*)malloc(sizeof(double) * P2 * s);
+  for (int Y = 0; Y < H2; ++Y)
+    for (int X = 0; X < W2; ++X) {
+      const size_t q = (size_t)Y * W2 + X;
+      const size_t qc = (size_t)(Y / 2) * W + (X / 2);       /* nearest: the covering coarse pixel */
+      for (int i = 0; i < 3; ++i) u[q * 3 + i] = img[qc * 3 + i];
+      for (int i = 0; i < 12; ++i) x[q * 15 + i] = gbuf_hi[q * 12 + i];
+      if (input_norm) {
+        for (int i = 0; i < 3; ++i) x[q * 15 + i] = x[q * 15 + i] * 0x1p-3;
+        x[q * 15 + 11] = x[q * 15 + 11] * 0x1p-7;
+      }
+      for (int i = 0; i < 3; ++i) x[q * 15 + 12 + i] = u[q * 3 + i];
+    }
+  og_conv3x3(x, H2, W2, 15, S1W, S1b, s, 1, 1, s1);
+  og_conv3x3(s1, H2, W2, s, S2W, S2b, s, 1, 1, s2);
+  for (size_t q = 0; q < P2; ++q)
+    for (int o = 0; o < 3; ++o) {
+      double r = S3b[o];
+      for (int i = 0; i < s; ++i) r += S3W[(size_t)o * s + i] * s2[q * s + i];
+      double v = u[q * 3 + o] + r;
+      out[q * 3 + o] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    }
+  free(x); free(u); free(s1); free(s2);
+  return 0;
+}

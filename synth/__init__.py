@@ -210,6 +210,51 @@ def make_weights(widths, levels, t_hidden, seed=0, r_takes_ld=True, bf16_weights
     return np.concatenate(parts).astype("<f4")
 
 
+def ss_layer_shapes(s):
+    """N3 super-sampler S (reading N3): (name, W shape, fan_in) in blob order."""
+    return [("S1", (s, 3, 3, 15), 9 * 15), ("S2", (s, 3, 3, s), 9 * s), ("S3", (3, s), s)]
+
+
+SS_RESIDUAL_SCALE = 0.1   # S3 (the residual head) drawn He-normal x 0.1: a near-identity init
+
+
+def make_ss_weights(s, seed=0, bf16_weights=False):
+    """Flat fp32 blob of S (S1.W S1.b S2.W S2.b S3.W S3.b); same generator as make_weights
+    with layer keys 2000+li; the residual head scaled by SS_RESIDUAL_SCALE."""
+    parts = []
+    for li, (name, shp, fan_in) in enumerate(ss_layer_shapes(s)):
+        key = splitmix64_int((seed * 4096 + 2000 + li) & MASK64)
+        nW = int(np.prod(shp))
+        idx = np.arange(nW, dtype=np.uint64)
+        h1 = splitmix64(np.uint64(key) ^ (idx * np.uint64(2)))
+        h2 = splitmix64(np.uint64(key) ^ (idx * np.uint64(2) + np.uint64(1)))
+        u1 = ((h1 >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0 ** -53
+        u2 = (h2 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+        z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * u2)
+        sc = SS_RESIDUAL_SCALE if name == "S3" else 1.0
+        W = (z * math.sqrt(2.0 / fan_in) * sc).astype(np.float32)
+        if bf16_weights:
+            W = round_to_bf16(W)
+        hb = splitmix64(np.uint64(key) ^ (np.arange(shp[0], dtype=np.uint64) + np.uint64(1 << 40)))
+        bound = sc / math.sqrt(fan_in)
+        b = (-bound + 2.0 * bound * u24(hb)).astype(np.float32)
+        parts += [W.reshape(-1), b]
+    return np.concatenate(parts).astype("<f4")
+
+
+def gen_image(seed, nframes, H, W):
+    """A [0,1] RGB image batch standing in for GlassNet's output (S's input in isolation)."""
+    key = stream_key(seed, 6)
+    b = _bases(0, nframes, H, W, 0, H, 0, W)
+    return np.stack([u24(_hash(key, b, c)) for c in range(3)], axis=-1).astype(np.float32)
+
+
+def gen_gbuf_hi(seed, nframes, H2, W2, precision):
+    """The hi-res G-buffer S reads: the G-buffer recipe on the 2H x 2W grid (seed distinct from
+    the low-res frame's), stored in `precision`."""
+    return store(gen_gbuf64(seed, 0, nframes, H2, W2, 0, H2, 0, W2), precision)
+
+
 # --------------------------------------------------------------------------- inputs
 def _bases(frame0, nframes, H, W, y0, y1, x0, x1):
     f = np.arange(frame0, frame0 + nframes, dtype=np.uint64)[:, None, None]
