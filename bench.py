@@ -242,7 +242,49 @@ def run_extras(net, cfg, g, d, t, n, args):
                      "l2": "inputs (>= 190 MB) larger than L2; back-to-back forwards"}
         net2.close()
         del g2, d2, t2, n2, o2
+    res["n3_supersample_c3"] = run_supersample(cfg, out, args)
     return res
+
+
+def run_supersample(cfg, img, args, nf=8):
+    """N3: the x2 super-sampler S on c3 geometry -- nf of this run's 1080p
+    GlassNet outputs to 3840x2160 with a seeded hi-res G-buffer, tensor-core family; per-stage
+    times with the algorithmic bytes / FLOPs of DESIGN.md §6.5."""
+    import torch
+    from paper_2405_19056_b200 import GlassNet, make_dims
+    from synth import device as sdev
+    H, W, c0 = cfg.height, cfg.width, cfg.widths[0]
+    w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True)
+    wss = synth.make_ss_weights(c0, seed=0, bf16_weights=True)
+    net = GlassNet(np.concatenate([w, wss]), make_dims(H, W, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels,
+                                                       max_batch=nf, supersample=True))
+    hi = synth.Config("hi", 2 * H, 2 * W, nf, 1, cfg.levels, cfg.widths, cfg.t_hidden, "bf16")
+    gh, dh, th, nh = sdev.alloc_and_fill(hi, nframes=nf, seed=6)
+    del dh, th, nh
+    im = img[:nf].contiguous()
+    o = torch.empty((nf, 2 * H, 2 * W, 3), dtype=torch.float32, device="cuda")
+    steps = max(5, args.steps)
+    ms = _time_forward(lambda: net.supersample(im, gh, o), steps, 3)
+    net.profile_begin(3 * steps + 2)
+    for _ in range(steps):
+        net.supersample(im, gh, o)
+    st = net.profile_end()
+    torch.cuda.synchronize()
+    P2 = 4 * H * W
+    alg = {"ss_S1": (P2 * (24 + 3 + 2 * c0), 2 * 9 * 15 * c0 * P2),           # G_hi + img in, s1 out
+           "ss_S2": (P2 * (2 * c0 + 3 + 12), (2 * 9 * c0 * c0 + 2 * 3 * c0) * P2)}   # s1 + img in, out
+    stages = {}
+    for k, (tot, cnt) in st.items():
+        per = tot / cnt
+        by, fl = alg.get(k, (0, 0))
+        stages[k] = {"ms_per_launch": per, "ms_per_frame": per / nf,
+                     "alg_GBps": by * nf / (per / 1000.0) / 1e9, "alg_TFLOPs": fl * nf / (per / 1000.0) / 1e12}
+    net.close()
+    del gh, o
+    return {"workload": f"S: {nf} frames {W}x{H} -> {2 * W}x{2 * H}, hidden {c0}, bf16 tensor cores",
+            "ms_per_call": ms, "ms_per_frame": ms / nf, "frames_per_s": nf * 1000.0 / ms,
+            "hbm_floor_ms_per_frame": sum(v[0] for v in alg.values()) / 6556.8e9 * 1000.0,
+            "stages": stages, "l2": "inputs (>= 1.6 GB) larger than L2; back-to-back calls"}
 
 
 def run_ours(args):

@@ -39,6 +39,8 @@
  *   B.W[c0][c0+h+1] B.b[c0]                 concat order [e0, tau_sum, n]
  *   R_{L-1}.W[c_{L-2}][3][3][c_{L-1}] R_{L-1}.b ... R_1.W[c0][3][3][c1] R_1.b
  *   O.W[3][c0+3] O.b[3]                     concat order [d0, L_d]
+ *   (GLASSNET_FLAG_SUPERSAMPLE only, s = c0:)
+ *   S1.W[s][3][3][15] S1.b[s] S2.W[s][3][3][s] S2.b[s] S3.W[3][s] S3.b[3]   (glassnet_supersample)
  * In GLASSNET_BF16 mode the W tensors are rounded RNE to bf16; biases stay fp32.
  *
  * Errors: every function returns GLASSNET_OK (0) or an error code; the message
@@ -64,7 +66,8 @@ enum { GLASSNET_BF16 = 0, GLASSNET_FP32 = 1 };          /* storage + math mode  
 enum { GLASSNET_POOL_SUM = 0, GLASSNET_POOL_MEAN = 1 };  /* g of Eq. eq:SymmetricNN     */
 enum { GLASSNET_FLAG_R_TAKES_LD = 1u << 0,               /* reading R15, default on     */
        GLASSNET_FLAG_INPUT_NORM = 1u << 1,               /* reading R9, default on      */
-       GLASSNET_FLAG_SIGMA_COND = 1u << 2 };             /* N1, default off: h(b, sigma) */
+       GLASSNET_FLAG_SIGMA_COND = 1u << 2,               /* N1, default off: h(b, sigma) */
+       GLASSNET_FLAG_SUPERSAMPLE = 1u << 3 };            /* N3, default off: the x2 super-sampler S */
 
 typedef struct glassnet* glassnet_t;
 typedef struct glassnet_comm* glassnet_comm_t;
@@ -136,6 +139,23 @@ int glassnet_profile_end(glassnet_t net, int32_t max_stages, char* names, double
  * device buffer `dst`.  Bitwise checks of T (slot permutation invariance, Eq.
  * eq:SymmetricNN P:303-318, table:OrderLoss P:666-679) compare it across forwards. */
 int glassnet_debug_psi(glassnet_t net, float* dst, int32_t batch, glassnet_stream_t stream);
+
+/* N3 -- the x2 super-sampling network S (§3.4: "A
+ * multi-layer CNN is used as a super-sampling network that super-samples the result at x2 the
+ * original resolution", fed with the cheaply rasterised high-resolution G-buffer; the
+ * architecture is unstated, so SPEC.md S:434-439's form, reading N3):
+ *   u = up_nearest(img);  x = [G'_hi, u] (15 ch, G' normalised as above when INPUT_NORM)
+ *   s1 = ReLU(conv3x3_s1(x; S1));  s2 = ReLU(conv3x3_s1(s1; S2));  r = S3.W s2 + S3.b
+ *   out_hi = clamp(u + r, 0, 1)
+ * Needs a handle created with GLASSNET_FLAG_SUPERSAMPLE (the blob then ends with S's weights,
+ * hidden width s = widths[0]; the workspace adds the hi-res activations for max_batch frames).
+ *   img     [B][H][W][3]        fp32 device (e.g. glassnet_forward's out)
+ *   gbuf_hi [B][2H][2W][12]     device, element type = dims.precision, layout as gbuf
+ *   out_hi  [B][2H][2W][3]      fp32 device, may not alias img
+ * Enqueued on `stream`; no host sync, no allocation.  Errors as above (UNSUPPORTED without
+ * the flag). */
+int glassnet_supersample(glassnet_t net, const float* img, const void* gbuf_hi, float* out_hi, int32_t batch,
+                         glassnet_stream_t stream);
 
 /* ---- row-tile sharding (one process per GPU, NCCL point-to-point halos) ---- */
 

@@ -81,6 +81,10 @@ extern "C" size_t glassnet_weight_count(const glassnet_dims* d) {
   for (int l = L - 1; l >= 1; --l) n += (size_t)c[l - 1] * 9 * c[l] + c[l - 1];
   const int nO = c[0] + ((d->flags & GLASSNET_FLAG_R_TAKES_LD) ? 3 : 0);
   n += (size_t)3 * nO + 3;
+  if (d->flags & GLASSNET_FLAG_SUPERSAMPLE) {   // N3: S1, S2, S3 with s = c0
+    const size_t sw = (size_t)c[0];
+    n += sw * 9 * 15 + sw + sw * 9 * sw + sw + 3 * sw + 3;
+  }
   return n;
 }
 
@@ -142,7 +146,14 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   const float* BW = p; p += (size_t)c[0] * NB; const float* Bb = p; p += c[0];
   for (int l = L - 1; l >= 1; --l) { RW[l] = p; p += (size_t)c[l - 1] * 9 * c[l]; Rb[l] = p; p += c[l - 1]; }
   const int NO = c[0] + (ld ? 3 : 0);
-  const float* OW = p; p += (size_t)3 * NO; const float* Ob = p;
+  const float* OW = p; p += (size_t)3 * NO; const float* Ob = p; p += 3;
+  const bool ss = (d.flags & GLASSNET_FLAG_SUPERSAMPLE) != 0;
+  const float *S1W = nullptr, *S1b = nullptr, *S2W = nullptr, *S2b = nullptr, *S3W = nullptr, *S3b = nullptr;
+  if (ss) {   // N3 (blob tail): S1.W[s][3][3][15] S1.b S2.W[s][3][3][s] S2.b S3.W[3][s] S3.b, s = c0
+    S1W = p; p += (size_t)c[0] * 9 * 15; S1b = p; p += c[0];
+    S2W = p; p += (size_t)c[0] * 9 * c[0]; S2b = p; p += c[0];
+    S3W = p; p += (size_t)3 * c[0]; S3b = p;
+  }
 
   // ---- SIMT packs ----
   std::vector<float> tb;
@@ -182,6 +193,17 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   for (int o = 0; o < 3; ++o)
     for (int i = 0; i < c[0]; ++i) wz[(size_t)o * c[0] + i] = W(OW[(size_t)o * NO + i]);
   if ((rc = dev_upload(&net->wz, wz, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+  if (ss) {
+    pack_conv(S1W, c[0], 15, 16, tmp);
+    if ((rc = dev_upload(&net->ssW[0], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    pack_conv(S2W, c[0], c[0], c[0], tmp);
+    if ((rc = dev_upload(&net->ssW[1], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    std::vector<float> b1(S1b, S1b + c[0]), b2(S2b, S2b + c[0]), w3((size_t)3 * c[0]);
+    for (size_t i = 0; i < w3.size(); ++i) w3[i] = W(S3W[i]);
+    if ((rc = dev_upload(&net->ssB[0], b1, &net->w_bytes)) || (rc = dev_upload(&net->ssB[1], b2, &net->w_bytes)) ||
+        (rc = dev_upload(&net->ss_wz, w3, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    for (int i = 0; i < 3; ++i) net->ss_b3[i] = S3b[i];
+  }
 
   // ---- workspace (independent of K: the T stage streams fragments) ----
   const size_t es = bf ? 2 : 4;
@@ -202,6 +224,9 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   for (int l = 1; l < L && !rc; ++l) rc = alloc(&net->y[l], B * Hl[l] * Wl[l] * c[l - 1] * es);
   for (int l = 1; l < L - 1 && !rc; ++l) rc = alloc(&net->dd[l], B * Hl[l] * Wl[l] * c[l] * es);
   if (!rc) rc = alloc((void**)&net->z, B * Hl[1] * Wl[1] * 3 * sizeof(float));
+  if (ss && !rc) rc = alloc(&net->ss_s1, B * 4 * P0 * c[0] * es);
+  if (ss && !rc) rc = alloc(&net->ss_x, B * 4 * P0 * 16 * es);      // SIMT family only: x and r stored
+  if (ss && !rc) rc = alloc((void**)&net->ss_r, B * 4 * P0 * 3 * sizeof(float));
   if (rc) { glassnet_destroy(net); return rc; }
   net->ws_bytes = ws;
   // ---- tensor-core packs (bf16 mode) ----
@@ -209,6 +234,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
     rc = gn::tc_pack_weights(net, T1W, T1b, T2W, T2b, FW, Fb, BW, Bb, RW, Rb, OW, Ob);
     if (!rc) rc = gn::tc_setup_convs(net, FW, RW);
     if (!rc) rc = gn::tc_setup_full_geom(net);
+    if (!rc && ss) rc = gn::tc_setup_ss(net, S1W, S2W);
     if (rc) { glassnet_destroy(net); return rc; }
   }
   net->tc = bf && gn::tc_supported(d);
@@ -220,7 +246,8 @@ extern "C" void glassnet_destroy(glassnet_t net) {
   if (!net) return;
   cudaSetDevice(net->dev);
   void* ptrs[] = {net->w_tb, net->wz, net->x16, net->psi, net->z, net->st_g, net->st_d, net->st_t,
-                  net->st_n, net->st_o};
+                  net->st_n, net->st_o, net->ssW[0], net->ssW[1], net->ssB[0], net->ssB[1], net->ss_wz,
+                  net->ss_s1, net->ss_x, net->ss_r};
   for (void* q : ptrs) if (q) cudaFree(q);
   if (net->st_in) cudaStreamDestroy(net->st_in);
   if (net->st_out) cudaStreamDestroy(net->st_out);
@@ -600,6 +627,62 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
   if (rc) return rc;
   CUDA_TRY(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3);
   return GLASSNET_OK;
+}
+
+// ------------------------------------------------------------------------ N3 super-sampler
+template <typename T>
+static int supersample_simt(glassnet* net, const float* img, const T* gbuf_hi, float* out_hi, int B, cudaStream_t st) {
+  const glassnet_dims& d = net->d;
+  const int H2 = 2 * d.height, W2 = 2 * d.width, c0 = d.widths[0];
+  const long P2 = (long)B * H2 * W2;
+  T* x = (T*)net->ss_x;
+  T* s1 = (T*)net->ss_s1;
+  net->prof.mark(nullptr, st);
+  gn::k_prep_ss<T><<<nblk(P2, 256), 256, 0, st>>>(gbuf_hi, img, x, W2, H2, P2, (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
+  net->prof.mark("ss_prep", st);
+  const dim3 g1(nblk(P2, 128), c0 / 16), g2(nblk(P2, 128), 1);
+  gn::k_conv3x3_simt<T, 16, 0><<<g1, 128, 0, st>>>(x, H2, W2, 16, net->ssW[0], net->ssB[0], c0, 1, s1, H2, W2, P2,
+                                                  nullptr, nullptr);
+  net->prof.mark("ss_S1", st);
+  if (c0 == 32)
+    gn::k_conv3x3_simt<T, 32, 1><<<g2, 128, 0, st>>>(s1, H2, W2, c0, net->ssW[1], net->ssB[1], c0, 1, nullptr, H2, W2,
+                                                    P2, net->ss_wz, net->ss_r);
+  else
+    gn::k_conv3x3_simt<T, 16, 1><<<g2, 128, 0, st>>>(s1, H2, W2, c0, net->ssW[1], net->ssB[1], c0, 1, nullptr, H2, W2,
+                                                    P2, net->ss_wz, net->ss_r);
+  net->prof.mark("ss_S2", st);
+  gn::k_ss_out<<<nblk(P2, 256), 256, 0, st>>>(img, net->ss_r, net->ss_b3[0], net->ss_b3[1], net->ss_b3[2], out_hi, W2,
+                                             H2, P2);
+  net->prof.mark("ss_out", st);
+  CUDA_TRY(cudaGetLastError());
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_supersample(glassnet_t net, const float* img, const void* gbuf_hi, float* out_hi, int32_t batch,
+                                    glassnet_stream_t stream) {
+  if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
+  if (!(net->d.flags & GLASSNET_FLAG_SUPERSAMPLE))
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "the handle was created without GLASSNET_FLAG_SUPERSAMPLE");
+  int rc;
+  if ((rc = check_ptr(img, "img")) || (rc = check_ptr(gbuf_hi, "gbuf_hi")) || (rc = check_ptr(out_hi, "out_hi")))
+    return rc;
+  if (batch < 1 || batch > net->d.max_batch)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "batch=%d outside [1, max_batch=%d]", batch, net->d.max_batch);
+  const size_t P = (size_t)batch * net->d.height * net->d.width;
+  if ((const char*)out_hi < (const char*)(img + 3 * P) && (const char*)img < (const char*)(out_hi + 12 * P))
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "out_hi overlaps img");
+  CUDA_TRY(cudaSetDevice(net->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (net->d.precision == GLASSNET_FP32)
+    return supersample_simt<float>(net, img, (const float*)gbuf_hi, out_hi, batch, st);
+  if (net->tc) {
+    net->prof.mark(nullptr, st);
+    rc = gn::tc_supersample(net, img, gbuf_hi, out_hi, batch, st);
+    if (rc) return rc;
+    CUDA_TRY(cudaGetLastError());
+    return GLASSNET_OK;
+  }
+  return supersample_simt<__nv_bfloat16>(net, img, (const __nv_bfloat16*)gbuf_hi, out_hi, batch, st);
 }
 
 extern "C" int glassnet_debug_psi(glassnet_t net, float* dst, int32_t batch, glassnet_stream_t stream) {

@@ -78,7 +78,10 @@ struct ConvArgs {
   int out_rows_buf;      // output buffer rows per frame
   const uint16_t* gbuf;  // GB = 1 (F0 on the full frame): [B][H][W][12] bf16, read directly
   const uint16_t* direct;   //                                  [B][H][W][3]
-  int Wi;                // input width (GB = 1)
+  int Wi;                // input width (GB = 1, 2)
+  // N3 super-sampler S (GB = 2 / EPI = 2, full frame): the low-res image [B][Ho/2][Wo/2][3] fp32
+  const float* img;      // GB = 2: channels 12..14 of the halo = bf16(img at the covering coarse pixel)
+  float b3[3];           // EPI = 2: out = clamp(img(coarse) + S3.W s2 + b3, 0, 1) -> zout
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
@@ -97,6 +100,10 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 // GB = 1 (F0 only, full frame): the producer warp builds the halo itself from the G-buffer
 // and L_d (one pixel row = [G(12), L_d(3), 0], the input normalisation folded into F0's
 // weights, exactly) in the same SWIZZLE_32B layout TMA writes, so x16 is never stored.
+// GB = 2 (S1 of the N3 super-sampler): the same producer with L_d replaced by the nearest-
+// upsampled low-res image (fp32, read at the covering coarse pixel, rounded to bf16).
+// EPI = 2 (S2 of N3): the z projection of EPI 1 plus S3's bias and the residual onto the
+// nearest-upsampled image, clamped to [0,1], written as the fp32 hi-res output.
 constexpr int GB_PRODUCERS = 7;   // GB = 1: warps 0 and 6..11 build the halo
 template <int S, int NS, int EPI, int WS = 0, int OST = 0, int RR = 1, int GB = 0>
 __global__ void __launch_bounds__(GB ? 32 * (5 + GB_PRODUCERS) : 192, GB ? 2 : 1)
@@ -132,7 +139,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
   }
   for (int i = tid; i < NS; i += blockDim.x) sBias[i] = a.bias[split * NS + i];
-  if (EPI == 1)   // the z projection's weights (EPI 1 runs unsplit: NS = Cout)
+  if (EPI >= 1)   // the z projection's weights (EPI 1, 2 run unsplit: NS = Cout)
     for (int i = tid; i < 3 * NS; i += blockDim.x) sBias[NS + i] = a.wz[i];
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, GB ? GB_PRODUCERS : 1); tc::mbar_init(empty + i, 1); }
@@ -180,10 +187,17 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const long p = ((long)b * a.in_rows_buf + gy) * a.Wi + gx;
           const uint2* g = reinterpret_cast<const uint2*>(a.gbuf + p * 12);
           const uint2 g0 = __ldg(g), g1 = __ldg(g + 1), g2 = __ldg(g + 2);
-          const uint16_t* dl = a.direct + p * 3;
           w[k][0] = g0.x; w[k][1] = g0.y; w[k][2] = g1.x; w[k][3] = g1.y; w[k][4] = g2.x; w[k][5] = g2.y;
-          w[k][6] = (uint32_t)__ldg(dl) | ((uint32_t)__ldg(dl + 1) << 16);
-          w[k][7] = (uint32_t)__ldg(dl + 2);
+          if (GB == 1) {
+            const uint16_t* dl = a.direct + p * 3;
+            w[k][6] = (uint32_t)__ldg(dl) | ((uint32_t)__ldg(dl + 1) << 16);
+            w[k][7] = (uint32_t)__ldg(dl + 2);
+          } else {   // nearest up-sampling: the coarse pixel covering (gy, gx)
+            const long pc = ((long)b * (a.in_rows_buf >> 1) + (gy >> 1)) * (a.Wi >> 1) + (gx >> 1);
+            const float* im = a.img + pc * 3;
+            w[k][6] = tc::cvt_bf16x2(__ldg(im), __ldg(im + 1));
+            w[k][7] = tc::cvt_bf16x2(__ldg(im + 2), 0.f);
+          }
         }
       }
 #pragma unroll
@@ -338,6 +352,13 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         if (EPI == 1 && valid) {
           a.zout[opix * 3 + 0] = z0; a.zout[opix * 3 + 1] = z1; a.zout[opix * 3 + 2] = z2;
+        }
+        if (EPI == 2 && valid) {   // N3: residual onto the nearest-upsampled image, clamped
+          const long pc = ((long)b * (a.out_rows_buf >> 1) + ((oy + a.out_row_off) >> 1)) * (a.Wo >> 1) + (px >> 1);
+          const float* im = a.img + pc * 3;
+          a.zout[opix * 3 + 0] = fminf(fmaxf(__ldg(im) + (z0 + a.b3[0]), 0.f), 1.f);
+          a.zout[opix * 3 + 1] = fminf(fmaxf(__ldg(im + 1) + (z1 + a.b3[1]), 0.f), 1.f);
+          a.zout[opix * 3 + 2] = fminf(fmaxf(__ldg(im + 2) + (z2 + a.b3[2]), 0.f), 1.f);
         }
         if (OST) {   // the warp's 32 pixels of this row are contiguous in NHWC: one bulk copy
           tc::fence_proxy_async();

@@ -52,6 +52,47 @@ __global__ void k_prep_x(const T* __restrict__ gbuf, const T* __restrict__ direc
   store8(x + p * 16 + 8, v + 8);
 }
 
+// N3 super-sampler S, SIMT family: x[p] = [G'_hi(12), img(coarse)(3), 0] at the hi-res pixel p
+// (nearest up-sampling: the coarse pixel covering it), G' as k_prep_x.  One thread per pixel.
+template <typename T>
+__global__ void k_prep_ss(const T* __restrict__ gbuf, const float* __restrict__ img, T* __restrict__ x,
+                          int W2, int H2, long P2, int norm) {
+  long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P2) return;
+  const int X = (int)(p % W2);
+  const long t = p / W2;
+  const int Y = (int)(t % H2);
+  const long b = t / H2;
+  const long pc = (b * (H2 >> 1) + (Y >> 1)) * (W2 >> 1) + (X >> 1);
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) v[i] = to_f(gbuf[p * 12 + i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) v[12 + i] = to_f(T(img[pc * 3 + i]));   // stored in T like any x
+  v[15] = 0.f;
+  if (norm) {
+    v[0] *= 0.125f; v[1] *= 0.125f; v[2] *= 0.125f;
+    v[11] *= 0.0078125f;
+  }
+  store8(x + p * 16, v);
+  store8(x + p * 16 + 8, v + 8);
+}
+
+// N3: out = clamp(img(coarse) + r + b3, 0, 1), r = S3.W s2 from k_conv3x3_simt<..., EPI 1>.
+__global__ void k_ss_out(const float* __restrict__ img, const float* __restrict__ r, float b30, float b31, float b32,
+                         float* __restrict__ out, int W2, int H2, long P2) {
+  long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P2) return;
+  const int X = (int)(p % W2);
+  const long t = p / W2;
+  const int Y = (int)(t % H2);
+  const long b = t / H2;
+  const long pc = (b * (H2 >> 1) + (Y >> 1)) * (W2 >> 1) + (X >> 1);
+  const float bb[3] = {b30, b31, b32};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[p * 3 + c] = fminf(fmaxf(img[pc * 3 + c] + (r[p * 3 + c] + bb[c]), 0.f), 1.f);
+}
+
 // conv3x3 (cross-correlation, zero pad 1), NHWC.  w: [9][Cin][Cout] fp32.  One thread =
 // one output pixel x NJ output channels.  EPI 0: bias + ReLU -> T.  EPI 1 (R_1 only):
 // bias + ReLU -> z = Wz y (3 fp32), the projection of reading R15.

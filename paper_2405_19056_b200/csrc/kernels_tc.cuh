@@ -26,6 +26,7 @@ struct TcConv {
   int ctas_per_sm = 1;
   uint8_t* wimg = nullptr;
   const float* bias = nullptr;
+  const float* wz = nullptr;     // EPI 1/2 projection weights [3][Cout] (nullptr: the handle's R15 wz)
 };
 
 // One conv layer in one execution geometry (buffers, row offsets, tensor maps).
@@ -61,6 +62,8 @@ struct TcState {
   TcConv conv[8];               // [l] = F_l, [4+l] = R_l
   Geom full;                    // the handle's own workspace
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
+  TcConv ssconv[2];             // N3 super-sampler: S1 (GB = 2), S2 (EPI = 2)
+  ConvGeom ssg[2];
   int* sched = nullptr;         // T kernel's dynamic tile counter
   uint32_t* perm = nullptr;     // T kernel's count-sorted pixel order (k_tb_sort), one entry per pixel
   long perm_cap = 0;
@@ -241,7 +244,7 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
           !getenv("GN_CONV_NO_STREAM")) ? 1 : 0;
   if (!L.ws)
     while (NS > 16 && conv_smem(S, Cin, NS, 2, 0, 0, 1, epi) > LIMIT) NS /= 2;
-  if (conv_smem(S, Cin, NS, 2, L.ws, 0, 1, epi) > LIMIT || (epi == 1 && NS != Cout))
+  if (conv_smem(S, Cin, NS, 2, L.ws, 0, 1, epi) > LIMIT || (epi >= 1 && NS != Cout))
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv %d->%d does not fit shared memory", Cin, Cout);
   L.NS = NS;
   L.nsplit = Cout / NS;
@@ -353,6 +356,33 @@ inline int tc_setup_full_geom(glassnet* net) {
   return geom_convs(net, G);
 }
 
+// N3 super-sampler S on the tensor cores: S1 = k_conv_tc<..., GB = 2> (its producers build the
+// [G'_hi, bf16(up_nearest(img)), 0] halo), S2 = k_conv_tc<..., EPI = 2> (projection, residual,
+// clamp in the epilogue): the hi-res input x and the residual r never reach HBM, only s1 does.
+inline int tc_setup_ss(glassnet* net, const float* S1W, const float* S2W) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  const glassnet_dims& d = net->d;
+  const int c0 = d.widths[0];
+  float sc0[16];
+  for (int i = 0; i < 16; ++i) sc0[i] = 1.f;
+  if (d.flags & GLASSNET_FLAG_INPUT_NORM) { sc0[0] = sc0[1] = sc0[2] = 0.125f; sc0[11] = 0.0078125f; }
+  int rc = setup_conv(net, s->ssconv[0], 1, S1W, net->ssB[0], 15, 16, c0, 0, sc0);
+  if (!rc) rc = setup_conv(net, s->ssconv[1], 1, S2W, net->ssB[1], c0, c0, c0, 2);
+  if (rc) return rc;
+  s->ssconv[1].wz = net->ss_wz;
+  for (int i = 0; i < 2 && !rc; ++i) {
+    ConvGeom& g = s->ssg[i];
+    g.Hi_buf = 2 * d.height; g.Wi = 2 * d.width; g.Ho = 2 * d.height; g.Wo = 2 * d.width;
+    g.in_row_off = 0; g.out_row_off = 0; g.out_rows_buf = 2 * d.height;
+    g.out = i == 0 ? reinterpret_cast<uint16_t*>(net->ss_s1) : nullptr;
+    g.zout = nullptr;   // S2: the caller's out_hi, set per call
+    // S1's producers build the halo themselves (the map, over s1, is valid but unused); S2 reads s1
+    rc = make_halo_maps(1, g, net->ss_s1, d.max_batch, c0, s->ssconv[i].rr);
+  }
+  return rc;
+}
+
+
 // Row-tile geometry for rank `rank` of `nranks` (one frame, halo rows, own buffers).
 inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int rows0) {
   TcState* s = reinterpret_cast<TcState*>(net->tc_state);
@@ -395,11 +425,18 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
 
 template <int S, int NS, int EPI, int WS, int OST, int RR, int GB = 0>
 static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
-                          const void* gbuf = nullptr, const void* direct = nullptr) {
+                          const void* gbuf = nullptr, const void* direct = nullptr, const float* img = nullptr,
+                          const float* b3 = nullptr) {
   auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST, RR, GB>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+  static int smem_set = -1;   // the attribute is set once per instantiation and size (not per launch)
+  if (smem_set < (int)L.smem) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    smem_set = (int)L.smem;
+  }
   conv::ConvArgs a;
-  a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = net->wz; a.zout = G.zout;
+  a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = L.wz ? L.wz : net->wz; a.zout = G.zout;
+  a.img = img;
+  for (int i = 0; i < 3; ++i) a.b3[i] = b3 ? b3[i] : 0.f;
   a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
   a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
   a.in_rows_buf = G.Hi_buf;
@@ -412,7 +449,29 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
 }
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
-                       const void* gbuf = nullptr, const void* direct = nullptr) {
+                       const void* gbuf = nullptr, const void* direct = nullptr, const float* img = nullptr,
+                       const float* b3 = nullptr) {
+  if (gbuf && img) {   // N3 S1: the hi-res G-buffer + the nearest-upsampled image
+#define CONV_GB2(NS_, OST_, RR_)                                                                         \
+    if (L.S == 1 && L.NS == NS_ && L.epi == 0 && L.ws == 0 && L.ost == OST_ && L.rr == RR_) {           \
+      launch_conv_k<1, NS_, 0, 0, OST_, RR_, 2>(net, L, G, B, st, gbuf, nullptr, img);                 \
+      return 0;                                                                                         \
+    }
+    CONV_GB2(16, 0, 4) CONV_GB2(16, 1, 4) CONV_GB2(32, 0, 4) CONV_GB2(32, 1, 4)
+    CONV_GB2(16, 0, 2) CONV_GB2(16, 1, 2) CONV_GB2(32, 0, 2) CONV_GB2(32, 1, 2)
+#undef CONV_GB2
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "S1 from the G-buffer: NS=%d ost=%d rr=%d", L.NS, L.ost, L.rr);
+  }
+  if (img) {   // N3 S2: the residual epilogue
+#define CONV_E2(NS_, RR_)                                                                                \
+    if (L.S == 1 && L.NS == NS_ && L.epi == 2 && L.ws == 0 && L.ost == 0 && L.rr == RR_) {              \
+      launch_conv_k<1, NS_, 2, 0, 0, RR_>(net, L, G, B, st, nullptr, nullptr, img, b3);                 \
+      return 0;                                                                                         \
+    }
+    CONV_E2(16, 1) CONV_E2(16, 2) CONV_E2(16, 4) CONV_E2(32, 1) CONV_E2(32, 2) CONV_E2(32, 4)
+#undef CONV_E2
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "S2: NS=%d rr=%d", L.NS, L.rr);
+  }
   if (gbuf) {   // F0 straight from the G-buffer (full frame)
 #define CONV_GB(NS_, OST_, RR_)                                                                          \
     if (L.S == 1 && L.NS == NS_ && L.epi == 0 && L.ws == 0 && L.ost == OST_ && L.rr == RR_) {           \
@@ -441,6 +500,18 @@ static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B,
 #undef CONV_K
   return gn_fail(GLASSNET_ERR_UNSUPPORTED, "conv variant S=%d NS=%d epi=%d ws=%d ost=%d rr=%d", L.S, L.NS, L.epi, L.ws,
                  L.ost, L.rr);
+}
+
+inline int tc_supersample(glassnet* net, const float* img, const void* gbuf_hi, float* out_hi, int B, cudaStream_t st) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  int rc = launch_conv(net, s->ssconv[0], s->ssg[0], B, st, gbuf_hi, nullptr, img);
+  net->prof.mark("ss_S1", st);
+  if (rc) return rc;
+  ConvGeom g = s->ssg[1];
+  g.zout = out_hi;
+  rc = launch_conv(net, s->ssconv[1], g, B, st, nullptr, nullptr, img, net->ss_b3);
+  net->prof.mark("ss_S2", st);
+  return rc;
 }
 
 inline bool tc_supported(const glassnet_dims& d) {

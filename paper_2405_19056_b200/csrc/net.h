@@ -67,6 +67,14 @@ struct glassnet {
   void* y[4] = {};          // y_l at level l
   void* dd[4] = {};         // d_l (1 <= l <= L-2)
   float* z = nullptr;       // [B][H/2][W/2][3]
+  // N3 super-sampler S (GLASSNET_FLAG_SUPERSAMPLE): SIMT packs [tap][ci][co], biases, S3.W, S3.b
+  float* ssW[2] = {};
+  float* ssB[2] = {};
+  float* ss_wz = nullptr;   // [3][c0]
+  float ss_b3[3] = {};
+  void* ss_s1 = nullptr;    // [B][2H][2W][c0]
+  void* ss_x = nullptr;     // [B][2H][2W][16]  (SIMT family)
+  float* ss_r = nullptr;    // [B][2H][2W][3]   (SIMT family)
   size_t ws_bytes = 0, w_bytes = 0;
   // staging for glassnet_forward_host
   void *st_g = nullptr, *st_d = nullptr, *st_t = nullptr, *st_n = nullptr;

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("GN_LIB", os.path.join(_HERE, "libglassnet.so"))   # G
 GLASSNET_ABI_VERSION = 1
 BF16, FP32 = 0, 1
 POOL_SUM, POOL_MEAN = 0, 1
-FLAG_R_TAKES_LD, FLAG_INPUT_NORM, FLAG_SIGMA_COND = 1, 2, 4
+FLAG_R_TAKES_LD, FLAG_INPUT_NORM, FLAG_SIGMA_COND, FLAG_SUPERSAMPLE = 1, 2, 4, 8
 ERRORS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CUDA", 4: "NCCL", 5: "OUT_OF_MEMORY"}
 
 EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glassnet_forward_host",
@@ -25,7 +25,7 @@ EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glas
            "glassnet_set_kernel_family", "glassnet_get_unique_id", "glassnet_comm_create",
            "glassnet_comm_destroy", "glassnet_tile_rows", "glassnet_forward_sharded",
            "glassnet_destroy", "glassnet_last_error", "glassnet_profile_begin", "glassnet_profile_end",
-           "glassnet_forward_sharded_local", "glassnet_debug_psi"]
+           "glassnet_forward_sharded_local", "glassnet_debug_psi", "glassnet_supersample"]
 
 
 class GlassNetError(RuntimeError):
@@ -83,6 +83,8 @@ def lib():
         L.glassnet_profile_end.argtypes = [vp, i32, vp, vp, vp, vp]
         L.glassnet_forward_sharded_local.restype = ctypes.c_int
         L.glassnet_forward_sharded_local.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+        L.glassnet_supersample.restype = ctypes.c_int
+        L.glassnet_supersample.argtypes = [vp, vp, vp, vp, i32, vp]
         L.glassnet_debug_psi.restype = ctypes.c_int
         L.glassnet_debug_psi.argtypes = [vp, vp, i32, vp]
         L.glassnet_destroy.restype = None
@@ -99,11 +101,11 @@ def _check(rc):
 
 
 def make_dims(height, width, k_slots, widths, t_hidden, levels=None, precision="bf16", max_batch=1,
-              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False) -> Dims:
+              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False, supersample=False) -> Dims:
     levels = len(widths) if levels is None else levels
     w = (ctypes.c_int32 * 4)(*(list(widths)[:levels] + [0] * (4 - levels)))
     flags = ((FLAG_R_TAKES_LD if r_takes_ld else 0) | (FLAG_INPUT_NORM if input_norm else 0)
-             | (FLAG_SIGMA_COND if sigma_cond else 0))
+             | (FLAG_SIGMA_COND if sigma_cond else 0) | (FLAG_SUPERSAMPLE if supersample else 0))
     return Dims(GLASSNET_ABI_VERSION, height, width, max_batch, k_slots, levels, w, t_hidden,
                 BF16 if precision == "bf16" else FP32, POOL_MEAN if pool == "mean" else POOL_SUM, flags)
 
@@ -178,6 +180,23 @@ class GlassNet:
     def forward_sharded(self, comm, gbuf, direct, tbuf, tcount, out, stream=None):
         _check(lib().glassnet_forward_sharded(self._h, comm._h, _ptr(gbuf), _ptr(direct), _ptr(tbuf),
                                               _ptr(tcount), _ptr(out), _stream(stream)))
+        return out
+
+    def supersample(self, img, gbuf_hi, out=None, stream=None):
+        """N3: the x2 super-sampler S (include/glassnet.h glassnet_supersample): img [B][H][W][3]
+        fp32, gbuf_hi [B][2H][2W][12] (dims precision) -> out [B][2H][2W][3] fp32, all on the device."""
+        import torch
+        d = self.dims
+        B = img.shape[0]
+        dt = torch.bfloat16 if d.precision == BF16 else torch.float32
+        if out is None:
+            out = torch.empty((B, 2 * d.height, 2 * d.width, 3), dtype=torch.float32, device=img.device)
+        for name, t, shape, dtype in (("img", img, (B, d.height, d.width, 3), torch.float32),
+                                      ("gbuf_hi", gbuf_hi, (B, 2 * d.height, 2 * d.width, 12), dt),
+                                      ("out", out, (B, 2 * d.height, 2 * d.width, 3), torch.float32)):
+            if tuple(t.shape) != shape or t.dtype != dtype or not t.is_contiguous() or not t.is_cuda:
+                raise ValueError(f"{name}: want {shape} {dtype} contiguous CUDA, got {tuple(t.shape)} {t.dtype}")
+        _check(lib().glassnet_supersample(self._h, _ptr(img), _ptr(gbuf_hi), _ptr(out), B, _stream(stream)))
         return out
 
     def debug_psi(self, batch, stream=None):

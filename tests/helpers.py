@@ -116,3 +116,26 @@ def frames_from_device(g, d, t, n, precision="bf16"):
     else:
         cv = lambda x: x.cpu().numpy()
     return synth.Frames(cv(g), cv(d), cv(t), n.cpu().numpy(), precision)
+
+
+def ss_band_oracle(s, w_ss, img, gbuf_hi, band=None, threads=None, input_norm=True):
+    """Oracle S (N3) of one frame as low-res row bands, each from a crop extended by one low-res
+    row (= two hi-res rows, the receptive field of S's two 3x3 convs) in a thread pool.  Bitwise
+    equal to the whole-frame oracle (pinned in test_oracle_ss_pins.py)."""
+    import concurrent.futures as cf
+    import os
+    import oracle
+    H, W, _ = img.shape
+    threads = threads or max(1, os.cpu_count() or 1)
+    band = band or max(1, -(-H // (2 * threads)))
+    out = np.zeros((2 * H, 2 * W, 3), np.float64)
+
+    def run(r0):
+        r1 = min(H, r0 + band)
+        a, b = max(0, r0 - 1), min(H, r1 + 1)
+        o = oracle.supersample(s, w_ss, img[a:b], gbuf_hi[2 * a:2 * b], input_norm=input_norm)
+        out[2 * r0:2 * r1] = o[2 * (r0 - a):2 * (r1 - a)]
+
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, range(0, H, band)))
+    return out

@@ -93,3 +93,24 @@ def test_PS4_receptive_field():
 def test_ss_weight_count():
     for s in (16, 32):
         assert oracle.ss_weight_count(s) == synth.make_ss_weights(s).size == 9 * 15 * s + s + 9 * s * s + s + 3 * s + 3
+
+
+def test_ss_band_oracle_is_bitwise_the_full_frame():
+    """The banded S oracle the full-size GPU parity tests use (one low-res row of margin) equals
+    the whole-frame oracle bit for bit (S's receptive field is 2 hi-res pixels)."""
+    from helpers import ss_band_oracle
+    s, H, W = 16, 9, 6
+    w, img, g = _inputs(s, H, W, seed=11)
+    full = oracle.supersample(s, w, img, g)
+    for band in (1, 2, 4):
+        assert np.array_equal(ss_band_oracle(s, w, img, g, band=band, threads=2), full)
+
+
+def test_ss_blob_layout_matches_library():
+    """glassnet_weight_count with GLASSNET_FLAG_SUPERSAMPLE = the network's count + S's (s = c0)."""
+    from paper_2405_19056_b200 import glassnet as gb
+    for c in (synth.CONFIGS["c0"], synth.CONFIGS["c1"]):
+        d0 = gb.make_dims(c.height, c.width, c.k_slots, c.widths, c.t_hidden, c.levels, precision=c.precision)
+        d1 = gb.make_dims(c.height, c.width, c.k_slots, c.widths, c.t_hidden, c.levels, precision=c.precision,
+                          supersample=True)
+        assert gb.weight_count(d1) == gb.weight_count(d0) + oracle.ss_weight_count(c.widths[0])
