@@ -12,6 +12,9 @@ Parity status per function:
               weights = the unconditioned network, bitwise) and P16 (records with zero weights:
               every fragment is h(sigma), n = 2 gives exactly 2 h(sigma)) and P10 (torch-fp64)
   og_forward  pinned (P10 torch-fp64 composition, P11 homogeneity, P13 tiles, P14 shift)
+  og_posenc (N2) pinned (PE1 SPEC S:401-403 examples, PE2 channel count, PE3 torch sin/cos at
+              exact dyadic points); forward with pe_L pinned by P15pe (zero sin/cos weights = the
+              unencoded network, bitwise) and P10pe (torch-fp64 composition with torch.sin/cos PE)
   og_supersample (N3) pinned (PS1 identity residual = nearest up-sampling, PS2 constant residual
               = clamp(u + beta), PS3 torch-fp64 composition (interpolate nearest + conv2d),
               PS4 receptive field: a coarse pixel reaches only hi-res pixels within 2 of its block)
@@ -41,7 +44,8 @@ def build(force=False):
 class Dims(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("K", ctypes.c_int), ("L", ctypes.c_int),
                 ("c", ctypes.c_int * 4), ("h", ctypes.c_int), ("pool", ctypes.c_int),
-                ("r_takes_ld", ctypes.c_int), ("input_norm", ctypes.c_int), ("sigma_cond", ctypes.c_int)]
+                ("r_takes_ld", ctypes.c_int), ("input_norm", ctypes.c_int), ("sigma_cond", ctypes.c_int),
+                ("pe_L", ctypes.c_int)]
 
 
 _P = ctypes.POINTER(ctypes.c_double)
@@ -63,6 +67,7 @@ def lib():
         _lib.og_conv3x3.restype = None
         _lib.og_up2.restype = None
         _lib.og_T_pixel.restype = None
+        _lib.og_posenc.restype = None
         _lib.og_ss_weight_count.restype = ctypes.c_size_t
         _lib.og_ss_weight_count.argtypes = [ctypes.c_int]
         _lib.og_supersample.restype = ctypes.c_int
@@ -70,15 +75,16 @@ def lib():
 
 
 def make_dims(H, W, K, widths, t_hidden, levels=None, pool="sum", r_takes_ld=True,
-              input_norm=True, sigma_cond=False) -> Dims:
+              input_norm=True, sigma_cond=False, pe_L=0) -> Dims:
     levels = len(widths) if levels is None else levels
     c = (ctypes.c_int * 4)(*(list(widths) + [0] * (4 - len(widths))))
     return Dims(H, W, K, levels, c, t_hidden, 1 if pool == "mean" else 0,
-                1 if r_takes_ld else 0, 1 if input_norm else 0, 1 if sigma_cond else 0)
+                1 if r_takes_ld else 0, 1 if input_norm else 0, 1 if sigma_cond else 0, int(pe_L))
 
 
 def dims_from_cfg(cfg, H=None, W=None, **kw) -> Dims:
     kw.setdefault("sigma_cond", bool(getattr(cfg, "extra", {}).get("sigma_cond", False)))
+    kw.setdefault("pe_L", int(getattr(cfg, "extra", {}).get("pe_L", 0)))
     return make_dims(cfg.height if H is None else H, cfg.width if W is None else W,
                      cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool, **kw)
 
@@ -121,7 +127,7 @@ def forward(d: Dims, weights, gbuf, direct, tbuf, tcount, dump=False):
     arrays = {}
     if dump:
         c = list(d.c)
-        arrays["x"] = np.zeros((H, W, 15))
+        arrays["x"] = np.zeros((H, W, 15 * (2 * d.pe_L + 1)))
         arrays["e"] = [np.zeros((lvl(H, l), lvl(W, l), c[l])) for l in range(L)]
         arrays["tau"] = np.zeros((H, W, h + 1))
         arrays["phi"] = np.zeros((H, W, c[0]))
@@ -188,8 +194,9 @@ def split_weights(d: Dims, weights):
         out[name] = w[p:p + n].reshape(shape)
         p += n
 
-    take("T1.W", (h, 11 + (c[0] if d.sigma_cond else 0))); take("T1.b", (h,)); take("T2.W", (h, h)); take("T2.b", (h,))
-    cin = 15
+    pe = 2 * d.pe_L + 1
+    take("T1.W", (h, 11 * pe + (c[0] if d.sigma_cond else 0))); take("T1.b", (h,)); take("T2.W", (h, h)); take("T2.b", (h,))
+    cin = 15 * pe
     for l in range(L):
         take(f"F{l}.W", (c[l], 3, 3, cin)); take(f"F{l}.b", (c[l],)); cin = c[l]
     take("B.W", (c[0], c[0] + h + 1)); take("B.b", (c[0],))
@@ -231,4 +238,12 @@ def split_ss_weights(s, weights_ss):
         out[name] = w[p:p + n].reshape(shape)
         p += n
     assert p == w.size
+    return out
+
+
+def posenc(v, L):
+    """N2 gamma(v) per channel (og_posenc): [n] -> [n (2L + 1)] fp64."""
+    v = _c64(np.atleast_1d(v))
+    out = np.zeros(v.size * (2 * L + 1))
+    lib().og_posenc(_ptr(v), int(v.size), int(L), _ptr(out))
     return out

@@ -8,7 +8,9 @@
  * What it computes (PAPER.md = /root/reference/PAPER.md, P:n = line n):
  *   1. normalise   x = [G', D], G' = G except pos*2^-3, depth*2^-7; record depth*2^-7
  *                  (reading R9 -- the paper position-encodes all inputs, P:373-375,
- *                  which presumes bounded inputs).
+ *                  which presumes bounded inputs).  With pe_L > 0
+ *                   x and every record are then positionally encoded
+ *                  (og_posenc): F0 reads 15(2L+1) channels, h's layer 1 11(2L+1) (+ c0).
  *   2. F (scene encoder): e0 = ReLU(conv3x3_s1(x)), e_l = ReLU(conv3x3_s2(e_{l-1})).
  *   3. T (Eq. eq:SymmetricNN): tau = g(h(b_1),...,h(b_t)) = sum_i h(b_i), h a
  *      shared 2-layer ReLU MLP over each VALID fragment record (k < min(n,K)) -- or, with
@@ -41,6 +43,7 @@ typedef struct {
   int r_takes_ld;  /* 1: output 1x1 takes [d0; L_d] (reading R15) */
   int input_norm;  /* 1: power-of-two input normalisation (R9)    */
   int sigma_cond;  /* 1: h(b, sigma), sigma = e0 at the pixel (N1) */
+  int pe_L;        /* N2: positional encoding with L_pe frequencies (0 = off)              */
 } og_dims;
 
 typedef struct {        /* optional per-layer dumps (any pointer may be NULL) */
@@ -55,6 +58,24 @@ typedef struct {        /* optional per-layer dumps (any pointer may be NULL) */
 
 static double relu(double v) { return v > 0.0 ? v : 0.0; }
 
+/* N2 -- positional encoding (§3.4 P:373-375 "All the inputs use
+ * positional encoding by Mildenhall et al."; the formula as SPEC.md S:395-403 states it):
+ *   gamma(v) = (v, sin(2^0 pi v), cos(2^0 pi v), ..., sin(2^(L-1) pi v), cos(2^(L-1) pi v))
+ * per channel, channels concatenated in input order: n channels -> n (2L + 1) (DESIGN.md
+ * reading N2).  L = 0: the identity. */
+void og_posenc(const double* v, int n, int L, double* out) {
+  const double pi = 3.14159265358979323846;
+  for (int c = 0; c < n; ++c) {
+    double* o = out + (size_t)c * (2 * L + 1);
+    o[0] = v[c];
+    for (int k = 0; k < L; ++k) {
+      const double a = ldexp(1.0, k) * pi * v[c];
+      o[1 + 2 * k] = sin(a);
+      o[2 + 2 * k] = cos(a);
+    }
+  }
+}
+
 static int lvl_size(int n, int l) { /* ceil(n / 2^l) */
   for (int i = 0; i < l; ++i) n = (n + 1) / 2;
   return n;
@@ -63,9 +84,10 @@ static int lvl_size(int n, int l) { /* ceil(n / 2^l) */
 size_t og_weight_count(const og_dims* d) {
   size_t n = 0;
   int h = d->h;
-  n += (size_t)h * (11 + (d->sigma_cond ? d->c[0] : 0)) + h;   /* T1 */
+  const int pe = 2 * d->pe_L + 1;          /* N2: channels per encoded input channel */
+  n += (size_t)h * (11 * pe + (d->sigma_cond ? d->c[0] : 0)) + h;   /* T1 */
   n += (size_t)h * h + h;                  /* T2 */
-  int cin = 15;
+  int cin = 15 * pe;
   for (int l = 0; l < d->L; ++l) { n += (size_t)d->c[l] * 9 * cin + d->c[l]; cin = d->c[l]; }
   n += (size_t)d->c[0] * (d->c[0] + h + 1) + d->c[0];   /* B */
   for (int l = d->L - 1; l >= 1; --l) n += (size_t)d->c[l - 1] * 9 * d->c[l] + d->c[l - 1];
@@ -133,19 +155,21 @@ static int cmp_double(const void* a, const void* b) {
 void og_T_pixel(const og_dims* d, const double* W1, const double* b1, const double* W2,
                 const double* b2, const double* rec, int n, const double* sigma, double* tau_out) {
   int h = d->h, K = d->K;
-  const int ns = d->sigma_cond ? d->c[0] : 0, nin = 11 + ns;
+  const int pe = 2 * d->pe_L + 1, nr = 11 * pe;          /* N2: encoded record width */
+  const int ns = d->sigma_cond ? d->c[0] : 0, nin = nr + ns;
   int m = n < K ? n : K;
   double* a2 = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1) * h);
   double* a1 = (double*)malloc(sizeof(double) * (size_t)h);
   double* col = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
   for (int k = 0; k < m; ++k) {
-    double r[11];
-    for (int i = 0; i < 11; ++i) r[i] = rec[(size_t)k * 11 + i];
-    if (d->input_norm) r[7] = r[7] * 0x1p-7;            /* record depth (R9) */
-    for (int o = 0; o < h; ++o) {                        /* h layer 1 over [b ; sigma] */
+    double r0[11], r[11 * 21];
+    for (int i = 0; i < 11; ++i) r0[i] = rec[(size_t)k * 11 + i];
+    if (d->input_norm) r0[7] = r0[7] * 0x1p-7;          /* record depth (R9) */
+    og_posenc(r0, 11, d->pe_L, r);                       /* N2 (identity when pe_L = 0) */
+    for (int o = 0; o < h; ++o) {                        /* h layer 1 over [gamma(b) ; sigma] */
       double acc = b1[o];
-      for (int i = 0; i < 11; ++i) acc += W1[(size_t)o * nin + i] * r[i];
-      for (int j = 0; j < ns; ++j) acc += W1[(size_t)o * nin + 11 + j] * sigma[j];
+      for (int i = 0; i < nr; ++i) acc += W1[(size_t)o * nin + i] * r[i];
+      for (int j = 0; j < ns; ++j) acc += W1[(size_t)o * nin + nr + j] * sigma[j];
       a1[o] = relu(acc);
     }
     for (int o = 0; o < h; ++o) {                        /* h layer 2 */
@@ -173,14 +197,15 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
   const int H = d->H, W = d->W, K = d->K, L = d->L, h = d->h;
   const int* c = d->c;
   const size_t P = (size_t)H * W;
-  if (L < 2 || L > 4 || K < 1 || H < 1 || W < 1) return 1;
+  if (L < 2 || L > 4 || K < 1 || H < 1 || W < 1 || d->pe_L < 0 || d->pe_L > 10) return 1;
+  const int pe = 2 * d->pe_L + 1, nx = 15 * pe;          /* N2: encoded input width */
 
   /* ---- unpack the weight blob (SURVEY.md §8(b) order) ---- */
   const double* p = wts;
-  const double *T1W = p; p += (size_t)h * (11 + (d->sigma_cond ? c[0] : 0)); const double* T1b = p; p += h;
+  const double *T1W = p; p += (size_t)h * (11 * pe + (d->sigma_cond ? c[0] : 0)); const double* T1b = p; p += h;
   const double *T2W = p; p += (size_t)h * h;  const double* T2b = p; p += h;
   const double *FW[4], *Fb[4];
-  int cin = 15;
+  int cin = nx;
   for (int l = 0; l < L; ++l) { FW[l] = p; p += (size_t)c[l] * 9 * cin; Fb[l] = p; p += c[l]; cin = c[l]; }
   const int nB = c[0] + h + 1;
   const double* BW = p; p += (size_t)c[0] * nB; const double* Bb = p; p += c[0];
@@ -192,20 +217,22 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
   int Hl[4], Wl[4];
   for (int l = 0; l < L; ++l) { Hl[l] = lvl_size(H, l); Wl[l] = lvl_size(W, l); }
 
-  /* ---- 1. normalise ---- */
-  double* x = (double*)malloc(sizeof(double) * P * 15);
+  /* ---- 1. normalise (then N2's positional encoding, identity when pe_L = 0) ---- */
+  double* x = (double*)malloc(sizeof(double) * P * nx);
   for (size_t q = 0; q < P; ++q) {
-    for (int i = 0; i < 12; ++i) x[q * 15 + i] = gbuf[q * 12 + i];
-    for (int i = 0; i < 3; ++i) x[q * 15 + 12 + i] = direct[q * 3 + i];
+    double v[15];
+    for (int i = 0; i < 12; ++i) v[i] = gbuf[q * 12 + i];
+    for (int i = 0; i < 3; ++i) v[12 + i] = direct[q * 3 + i];
     if (d->input_norm) {
-      for (int i = 0; i < 3; ++i) x[q * 15 + i] = x[q * 15 + i] * 0x1p-3;  /* position */
-      x[q * 15 + 11] = x[q * 15 + 11] * 0x1p-7;                            /* depth */
+      for (int i = 0; i < 3; ++i) v[i] = v[i] * 0x1p-3;  /* position */
+      v[11] = v[11] * 0x1p-7;                            /* depth */
     }
+    og_posenc(v, 15, d->pe_L, x + q * nx);
   }
   /* ---- 2. F ---- */
   double* e[4];
   e[0] = (double*)malloc(sizeof(double) * P * c[0]);
-  og_conv3x3(x, H, W, 15, FW[0], Fb[0], c[0], 1, 1, e[0]);
+  og_conv3x3(x, H, W, nx, FW[0], Fb[0], c[0], 1, 1, e[0]);
   for (int l = 1; l < L; ++l) {
     e[l] = (double*)malloc(sizeof(double) * (size_t)Hl[l] * Wl[l] * c[l]);
     og_conv3x3(e[l - 1], Hl[l - 1], Wl[l - 1], c[l - 1], FW[l], Fb[l], c[l], 2, 1, e[l]);
@@ -250,7 +277,7 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
     }
 
   if (dump) {
-    if (dump->x) memcpy(dump->x, x, sizeof(double) * P * 15);
+    if (dump->x) memcpy(dump->x, x, sizeof(double) * P * nx);
     for (int l = 0; l < L; ++l)
       if (dump->e[l]) memcpy(dump->e[l], e[l], sizeof(double) * (size_t)Hl[l] * Wl[l] * c[l]);
     if (dump->tau) memcpy(dump->tau, tau, sizeof(double) * P * (h + 1));

@@ -141,6 +141,17 @@ def _frame(H, W, K, widths=(16, 32, 64), h=32, seed=1, precision="fp32"):
     return dims, wts, g[0], d[0], t[0], n[0]
 
 
+def torch_pe(x, L):
+    """N2's gamma on the last axis with torch.sin/cos: channel c -> [v, sin(2^k pi v), cos(2^k pi v)]_k."""
+    if L == 0:
+        return x
+    parts = [x[..., None]]
+    for k in range(L):
+        a = (2.0 ** k) * math.pi * x
+        parts += [torch.sin(a)[..., None], torch.cos(a)[..., None]]
+    return torch.cat(parts, -1).reshape(*x.shape[:-1], x.shape[-1] * (2 * L + 1))
+
+
 def torch_forward(dims, wts, g, dr, tb, n):
     """Independent torch-fp64 composition of the same graph (P10)."""
     wd = {k: torch.from_numpy(v) for k, v in oracle.split_weights(dims, wts).items()}
@@ -150,7 +161,7 @@ def torch_forward(dims, wts, g, dr, tb, n):
     scale = torch.ones(12, dtype=torch.float64)
     scale[0:3] = 0.125
     scale[11] = 1 / 128
-    x = torch.cat([g * scale, dr], -1).permute(2, 0, 1)[None]
+    x = torch_pe(torch.cat([g * scale, dr], -1), dims.pe_L).permute(2, 0, 1)[None]
     conv = lambda t, name, s: Fnn.relu(Fnn.conv2d(t, wd[name + ".W"].permute(0, 3, 1, 2), wd[name + ".b"],
                                                   stride=s, padding=1))
     e = [conv(x, "F0", 1)]
@@ -158,7 +169,7 @@ def torch_forward(dims, wts, g, dr, tb, n):
         e.append(conv(e[-1], f"F{l}", 2))
     rs = torch.ones(11, dtype=torch.float64)
     rs[7] = 1 / 128
-    rec = tb * rs
+    rec = torch_pe(tb * rs, dims.pe_L)
     if dims.sigma_cond:   # N1: h's input is [record ; e0 at the pixel]
         sig = e[0][0].permute(1, 2, 0)[:, :, None, :].expand(-1, -1, dims.K, -1)
         rec = torch.cat([rec, sig], -1)
