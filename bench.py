@@ -48,18 +48,22 @@ def parse():
     ap.add_argument("--no-extra", action="store_true", help="skip the c1/c2 lines and the batch sweep")
     ap.add_argument("--sigma-cond", action="store_true",
                     help="SURVEY §8(f) N1: h(b, sigma) (layer 1 over [record ; e0]); not the headline network")
+    ap.add_argument("--pe", type=int, default=0,
+                    help="SURVEY §8(f) N2: positional encoding with L_pe frequencies (6 in the paper's "
+                         "NeRF form); not the headline network")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------------------- helpers
-def alg_flops_per_frame(cfg, mean_n, sigma_cond=False):
+def alg_flops_per_frame(cfg, mean_n, sigma_cond=False, pe_L=0):
     """Algorithmic FLOPs per frame (valid fragments only, unpadded)."""
     H, W = cfg.height, cfg.width
     c, h, L = cfg.widths, cfg.t_hidden, cfg.levels
     P = H * W
+    pe = 2 * pe_L + 1
     macs = {}
-    macs["T"] = P * mean_n * ((11 + (c[0] if sigma_cond else 0)) * h + h * h)
-    macs["F0"] = P * 9 * 15 * c[0]
+    macs["T"] = P * mean_n * ((11 * pe + (c[0] if sigma_cond else 0)) * h + h * h)
+    macs["F0"] = P * 9 * 15 * pe * c[0]
     for l in range(1, L):
         macs[f"F{l}"] = (P >> (2 * l)) * 9 * c[l - 1] * c[l]
     macs["B"] = P * (c[0] + h + 1) * c[0]
@@ -313,9 +317,9 @@ def run_ours(args):
             raise SystemExit(f"{world} ranks for a {cfg.batch}-frame batch")
     H, W, K = cfg.height, cfg.width, cfg.k_slots
     w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True,
-                           sigma_cond=args.sigma_cond)
+                           sigma_cond=args.sigma_cond, pe_L=args.pe)
     dims = make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, precision=cfg.precision, max_batch=B,
-                     pool=cfg.pool, sigma_cond=args.sigma_cond)
+                     pool=cfg.pool, sigma_cond=args.sigma_cond, pe_L=args.pe)
     net = GlassNet(w, dims)
     net.set_kernel_family(args.family == "tc")
     stream = torch.cuda.current_stream()
@@ -368,7 +372,7 @@ def run_ours(args):
         run()
     stages = net.profile_end()
     torch.cuda.synchronize()
-    flops = alg_flops_per_frame(cfg, mean_n, args.sigma_cond)
+    flops = alg_flops_per_frame(cfg, mean_n, args.sigma_cond, args.pe)
     if tiles_mode:   # this rank's share of the frame
         flops = {k: v * rows / H for k, v in flops.items()}
     step_ms = sum(v[0] for v in stages.values()) / args.steps
@@ -461,7 +465,7 @@ def run_ours(args):
             cfgj = {"workload": f"{cfg.name}: {W}x{H}, K={K}, batch {frames_per_step} frames, n~U{{0..{K}}}",
                     "frames_per_gpu": B, "global_batch": frames_per_step, "parallelism": f"dp{world} (frames)",
                     "kernel_family": args.family, "l2": "inputs (13.7 GB/rank) larger than L2; no flush",
-                    "sigma_cond": args.sigma_cond,
+                    "sigma_cond": args.sigma_cond, "pe_L": args.pe,
                     "mean_valid_fragments": mean_n}
             metric = METRIC
         line = {"metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,

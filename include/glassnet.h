@@ -31,6 +31,7 @@
  *
  * Weights: one little-endian fp32 host blob, in this order (conv weights OHWI,
  * cross-correlation, tap (ky,kx) reads offset (ky-1,kx-1)):
+ *   (with GLASSNET_FLAG_POSENC(L): every "11" below is 11(2L+1) and F0's "15" is 15(2L+1))
  *   T1.W[h][11] T1.b[h] T2.W[h][h] T2.b[h]   (GLASSNET_FLAG_SIGMA_COND: T1.W[h][11 + c0] --
  *                                             the paper's h(b_i, sigma), Eq. eq:SymmetricNN
  *                                             P:308-316, layer 1 over [record ; e0 at the
@@ -68,6 +69,14 @@ enum { GLASSNET_FLAG_R_TAKES_LD = 1u << 0,               /* reading R15, default
        GLASSNET_FLAG_INPUT_NORM = 1u << 1,               /* reading R9, default on      */
        GLASSNET_FLAG_SIGMA_COND = 1u << 2,               /* N1, default off: h(b, sigma) */
        GLASSNET_FLAG_SUPERSAMPLE = 1u << 3 };            /* N3, default off: the x2 super-sampler S */
+/* N2 (default off): positional encoding with L_pe = 1..10 frequencies of every input channel
+ * (§3.4 P:373-375 "All the inputs use positional encoding by Mildenhall et al.";
+ * SPEC.md S:395-403): gamma(v) = (v, sin(2^0 pi v), cos(2^0 pi v), ..., sin(2^(L-1) pi v),
+ * cos(2^(L-1) pi v)) per channel, channels in input order, applied after the R9 normalisation
+ * to x (15 -> 15(2L+1) channels, F0's input) and to every record (11 -> 11(2L+1), h's layer-1
+ * input).  Stored in flags bits 8..11. */
+#define GLASSNET_FLAG_POSENC(L) ((uint32_t)(L) << 8)
+#define GLASSNET_POSENC_OF(flags) ((int)(((flags) >> 8) & 15u))
 
 typedef struct glassnet* glassnet_t;
 typedef struct glassnet_comm* glassnet_comm_t;

@@ -66,6 +66,9 @@ static int validate_dims(const glassnet_dims* d) {
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "widths[0] > 32 is not implemented");
   if (d->t_hidden != 16 && d->t_hidden != 32 && d->t_hidden != 64)
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "t_hidden must be 16, 32 or 64");
+  if (gn_pe_L(*d) > 10) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "positional encoding L_pe must be <= 10");
+  if (d->flags & ~(0xFu | (0xFu << 8)))
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "unknown flag bits 0x%x", d->flags & ~(0xFu | (0xFu << 8)));
   return GLASSNET_OK;
 }
 
@@ -73,9 +76,9 @@ extern "C" size_t glassnet_weight_count(const glassnet_dims* d) {
   if (validate_dims(d) != GLASSNET_OK) return 0;
   const int h = d->t_hidden, L = d->levels;
   const int* c = d->widths;
-  const int nin = 11 + ((d->flags & GLASSNET_FLAG_SIGMA_COND) ? d->widths[0] : 0);   // N1: [record ; e0]
+  const int nin = gn_rec_in(*d) + ((d->flags & GLASSNET_FLAG_SIGMA_COND) ? d->widths[0] : 0);   // N1: [record ; e0]
   size_t n = (size_t)h * nin + h + (size_t)h * h + h;
-  int cin = 15;
+  int cin = gn_x_in(*d);   // N2: 15 (2 L_pe + 1)
   for (int l = 0; l < L; ++l) { n += (size_t)c[l] * 9 * cin + c[l]; cin = c[l]; }
   n += (size_t)c[0] * (c[0] + h + 1) + c[0];
   for (int l = L - 1; l >= 1; --l) n += (size_t)c[l - 1] * 9 * c[l] + c[l - 1];
@@ -137,10 +140,11 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   const float* p = weights;
   std::vector<const float*> FW(L), Fb(L), RW(L), Rb(L);
   const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
-  const int nin = 11 + (sig ? c[0] : 0);
+  const int nin = gn_rec_in(d) + (sig ? c[0] : 0);
   const float *T1W = p; p += (size_t)h * nin; const float* T1b = p; p += h;
   const float *T2W = p; p += (size_t)h * h; const float* T2b = p; p += h;
-  int cin = 15;
+  const int XIN = gn_x_in(d), XC = gn_x_ch(d);   // N2: F0's input channels (real, stored)
+  int cin = XIN;
   for (int l = 0; l < L; ++l) { FW[l] = p; p += (size_t)c[l] * 9 * cin; Fb[l] = p; p += c[l]; cin = c[l]; }
   const int NB = c[0] + h + 1;
   const float* BW = p; p += (size_t)c[0] * NB; const float* Bb = p; p += c[0];
@@ -177,7 +181,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   };
   std::vector<float> tmp;
   for (int l = 0; l < L; ++l) {
-    const int ci = l == 0 ? 15 : c[l - 1], cip = l == 0 ? 16 : c[l - 1];
+    const int ci = l == 0 ? XIN : c[l - 1], cip = l == 0 ? XC : c[l - 1];
     pack_conv(FW[l], c[l], ci, cip, tmp);
     if ((rc = dev_upload(&net->convW[l], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
     std::vector<float> bb(Fb[l], Fb[l] + c[l]);
@@ -218,7 +222,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   size_t Hl[4], Wl[4];
   for (int l = 0; l < L; ++l) { Hl[l] = (size_t)d.height >> l; Wl[l] = (size_t)d.width >> l; }
   const size_t P0 = Hl[0] * Wl[0];
-  rc = alloc(&net->x16, B * P0 * 16 * es);
+  rc = alloc(&net->x16, B * P0 * XC * es);
   for (int l = 0; l < L && !rc; ++l) rc = alloc(&net->e[l], B * Hl[l] * Wl[l] * c[l] * es);
   if (!rc) rc = alloc((void**)&net->psi, B * P0 * 3 * sizeof(float));
   for (int l = 1; l < L && !rc; ++l) rc = alloc(&net->y[l], B * Hl[l] * Wl[l] * c[l - 1] * es);
@@ -292,20 +296,56 @@ static gn::Up2Rows full_rows(int rows_f, int rows_c) {
   return g;
 }
 
+// T + B + psi on the SIMT kernel (FFMA): the fp32 check mode, the SIMT family, and -- with N2's
+// positional encoding -- the tensor-core family's T stage (h's layer 1 over 11 (2L+1) encoded
+// features per record has no tensor-core kernel here).
+template <typename T>
+static void launch_tb_simt(glassnet* net, const T* tbuf, const uint8_t* tcount, const T* e0, const T* direct, float* psi,
+                           long P0, cudaStream_t st) {
+  const glassnet_dims& d = net->d;
+  const int K = d.k_slots, h = d.t_hidden;
+  const int* c = d.widths;
+  const bool norm = (d.flags & GLASSNET_FLAG_INPUT_NORM) != 0;
+  const bool ld = (d.flags & GLASSNET_FLAG_R_TAKES_LD) != 0;
+  const int NB = c[0] + h + 1, NO = c[0] + (ld ? 3 : 0);
+  const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
+  const size_t nw = h * (gn_rec_in(d) + (sig ? c[0] : 0)) + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3;
+  // (+ N2: a transposed copy of W1, 16-byte aligned)
+  const size_t smem = sizeof(float) * (gn_pe_L(d) ? (nw + 3) / 4 * 4 + h * (gn_rec_in(d) + (sig ? c[0] : 0)) : nw);
+  const unsigned g = nblk(P0, 128);
+#define TB_LAUNCH(HH, CC)                                                                                      \
+  {                                                                                                            \
+    auto kfn = gn::k_tb_simt<T, HH, CC>;                                                                       \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
+    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e0, direct, net->w_tb, psi, P0, K, d.pool, ld, norm, sig ? 1 : 0, \
+                              gn_pe_L(d));                                                                     \
+  }
+  if (h == 64 && c[0] == 32) TB_LAUNCH(64, 32)
+  else if (h == 64 && c[0] == 16) TB_LAUNCH(64, 16)
+  else if (h == 32 && c[0] == 32) TB_LAUNCH(32, 32)
+  else if (h == 32 && c[0] == 16) TB_LAUNCH(32, 16)
+  else if (h == 16 && c[0] == 32) TB_LAUNCH(16, 32)
+  else TB_LAUNCH(16, 16)
+#undef TB_LAUNCH
+}
+
 template <typename T>
 static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
                         float* out, int B, cudaStream_t st) {
   const glassnet_dims& d = net->d;
-  const int L = d.levels, K = d.k_slots, h = d.t_hidden;
+  const int L = d.levels;
   const int* c = d.widths;
   const bool norm = (d.flags & GLASSNET_FLAG_INPUT_NORM) != 0;
-  const bool ld = (d.flags & GLASSNET_FLAG_R_TAKES_LD) != 0;
   int Hl[4], Wl[4];
   for (int l = 0; l < L; ++l) { Hl[l] = d.height >> l; Wl[l] = d.width >> l; }
   const long P0 = (long)B * Hl[0] * Wl[0];
   T* x16 = (T*)net->x16;
+  const int XC = gn_x_ch(d);
   net->prof.mark(nullptr, st);
-  gn::k_prep_x<T><<<nblk(P0, 256), 256, 0, st>>>(gbuf, direct, x16, P0, norm);
+  if (gn_pe_L(d))   // N2: x = gamma([G', L_d])
+    gn::k_prep_pe<T><<<nblk(P0, 32), 32, 32 * XC * sizeof(T), st>>>(gbuf, direct, x16, P0, norm, gn_pe_L(d), XC);
+  else
+    gn::k_prep_x<T><<<nblk(P0, 256), 256, 0, st>>>(gbuf, direct, x16, P0, norm);
   net->prof.mark("prep_x", st);
   auto conv = [&](const T* in, int l_in, int cin, int wi, int cout, int stride, T* o, int epi) {
     const int Ho = Hl[l_in] / stride, Wo = Wl[l_in] / stride;
@@ -329,28 +369,10 @@ static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* 
   };
   T* e[4];
   for (int l = 0; l < L; ++l) e[l] = (T*)net->e[l];
-  conv(x16, 0, 16, 0, c[0], 1, e[0], 0);
+  conv(x16, 0, XC, 0, c[0], 1, e[0], 0);
   for (int l = 1; l < L; ++l) conv(e[l - 1], l - 1, c[l - 1], l, c[l], 2, e[l], 0);
-  {  // T + B + psi
-    const int NB = c[0] + h + 1, NO = c[0] + (ld ? 3 : 0);
-    const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
-    const size_t smem = sizeof(float) * (h * (11 + (sig ? c[0] : 0)) + h + h * h + h + c[0] * NB + c[0] + 3 * NO + 3);
-    const unsigned g = nblk(P0, 128);
-#define TB_LAUNCH(HH, CC)                                                                              \
-  {                                                                                                    \
-    auto kfn = gn::k_tb_simt<T, HH, CC>;                                                               \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                \
-    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e[0], direct, net->w_tb, net->psi, P0, K, d.pool, ld, norm, sig ? 1 : 0); \
-  }
-    if (h == 64 && c[0] == 32) TB_LAUNCH(64, 32)
-    else if (h == 64 && c[0] == 16) TB_LAUNCH(64, 16)
-    else if (h == 32 && c[0] == 32) TB_LAUNCH(32, 32)
-    else if (h == 32 && c[0] == 16) TB_LAUNCH(32, 16)
-    else if (h == 16 && c[0] == 32) TB_LAUNCH(16, 32)
-    else TB_LAUNCH(16, 16)
-#undef TB_LAUNCH
-    net->prof.mark("T_B_psi", st);
-  }
+  launch_tb_simt<T>(net, tbuf, tcount, e[0], direct, net->psi, P0, st);
+  net->prof.mark("T_B_psi", st);
   // R: d_{L-1} = e_{L-1}
   const T* dcur = e[L - 1];
   for (int l = L - 1; l >= 2; --l) {
@@ -411,7 +433,7 @@ int tc_tensor_rows(glassnet* net, bool tile, int tensor, char** base, size_t* ro
   int l = 0;
   size_t ch = 0, es = 2;
   void* p = nullptr;
-  if (tensor == TEN_X) { l = 0; ch = 16; p = G.x16; }
+  if (tensor == TEN_X) { l = 0; ch = gn_x_ch(net->d); p = G.x16; }
   else if (tensor >= TEN_E && tensor < TEN_E + 4) { l = tensor - TEN_E; ch = c[l]; p = G.e[l]; }
   else if (tensor >= TEN_Y && tensor < TEN_Y + 4) { l = tensor - TEN_Y; ch = c[l - 1]; p = G.y[l]; }
   else if (tensor >= TEN_D && tensor < TEN_D + 4) { l = tensor - TEN_D; ch = c[l]; p = G.dd[l]; }
@@ -434,6 +456,14 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
   typedef __nv_bfloat16 bf;
   switch (sp.kind) {
     case ST_PREP: {
+      if (gn_pe_L(d)) {   // N2: x = gamma([G', L_d]) stored (XC channels) for F0's TMA halo; T runs SIMT
+        const int XC = gn_x_ch(d);
+        bf* x = (bf*)G.x16 + (size_t)h * G.W[0] * XC;
+        k_prep_pe<bf><<<nblk(P0, 32), 32, 32 * XC * sizeof(bf), st>>>((const bf*)gbuf, (const bf*)direct, x, P0,
+                                                           (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0, gn_pe_L(d), XC);
+        net->prof.mark("prep_x", st);
+        return 0;
+      }
       {   // T's count sort, on its own stream beside the encoder (kernels_tc.cuh)
         const int rc = tc_launch_sort(net, tcount, P0, st);
         if (rc) return rc;
@@ -448,13 +478,18 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       return 0;
     }
     case ST_CONV: {
-      int rc = (!tile && sp.idx == 0) ? launch_conv(net, s->conv[0], G.cg[0], B, st, gbuf, direct)
+      int rc = (!tile && sp.idx == 0 && !gn_pe_L(d)) ? launch_conv(net, s->conv[0], G.cg[0], B, st, gbuf, direct)
                                       : launch_conv(net, s->conv[sp.idx], G.cg[sp.idx], B, st);
       net->prof.mark(kConvNames[sp.idx], st);
       return rc;
     }
     case ST_TB: {
       const bf* e0 = (const bf*)G.e[0] + (size_t)h * G.W[0] * c[0];
+      if (gn_pe_L(d)) {   // N2: T over the encoded records on the SIMT kernel (same stream order)
+        launch_tb_simt<bf>(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, st);
+        net->prof.mark("T_B_psi", st);
+        return 0;
+      }
       if (!tile) {
         int rc = tc_launch_tb(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, st);
         net->prof.mark("T_B_psi", st);
@@ -492,7 +527,7 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       g.rows_f = G.rows[0]; g.rows_f_buf = G.rows[0] + 2 * h; g.grow0_f = G.grow0[0];
       g.rows_c_buf = G.rows[1] + 2 * h; g.grow0_c = G.grow0[1]; g.Hc_full = G.Hfull[1]; g.halo = h;
       const dim3 grid((unsigned)((G.W[0] / 2 + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
-      if (tile) cudaStreamWaitEvent(st, s->ev_tb, 0);   // psi from T's stream
+      if (tile && !gn_pe_L(d)) cudaStreamWaitEvent(st, s->ev_tb, 0);   // psi from T's stream
       ew::k_output<<<grid, 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g);
       net->prof.mark("output", st);
       return 0;

@@ -52,6 +52,55 @@ __global__ void k_prep_x(const T* __restrict__ gbuf, const T* __restrict__ direc
   store8(x + p * 16 + 8, v + 8);
 }
 
+// N2 positional encoding: the features of v are
+// v, sin(2^k pi v), cos(2^k pi v) for k < L.  sincospif(v) once (exact argument reduction), then
+// the double-angle recurrence sin 2a = 2 sin a cos a, cos 2a = (cos a - sin a)(cos a + sin a):
+// the absolute error at most doubles per octave (<= 2^(L-1) x ~1 ulp, ~4e-6 at L = 6), far inside
+// bf16 storage rounding and the fp32 check mode's 1e-4.
+struct PeIter {
+  float s, c;
+  __device__ __forceinline__ explicit PeIter(float v) { sincospif(v, &s, &c); }
+  __device__ __forceinline__ void next() {
+    const float s2 = 2.f * s * c, c2 = (c - s) * (c + s);
+    s = s2; c = c2;
+  }
+};
+
+// N2: x = gamma([G', L_d]) (15 (2L+1) channels, zero-padded to XC).  A block = 32 pixels (one per
+// thread); each thread encodes its pixel into shared memory, then the block writes the 32
+// contiguous NHWC pixels with 16-byte stores.
+template <typename T>
+__global__ void __launch_bounds__(32) k_prep_pe(const T* __restrict__ gbuf, const T* __restrict__ direct,
+                                                T* __restrict__ x, long P, int norm, int L, int XC) {
+  extern __shared__ __align__(16) uint8_t pe_smem[];
+  T* st = reinterpret_cast<T*>(pe_smem);
+  const long p0 = (long)blockIdx.x * 32;
+  const long p = p0 + threadIdx.x;
+  const int pe = 2 * L + 1;
+  if (p < P) {
+    T* o = st + threadIdx.x * XC;
+    for (int c = 0; c < 15; ++c) {
+      float v = c < 12 ? to_f(gbuf[p * 12 + c]) : to_f(direct[p * 3 + c - 12]);
+      if (norm && c < 3) v *= 0.125f;
+      if (norm && c == 11) v *= 0.0078125f;
+      o[c * pe] = T(v);
+      PeIter it(v);
+      for (int k = 0; k < L; ++k) {
+        o[c * pe + 1 + 2 * k] = T(it.s);
+        o[c * pe + 2 + 2 * k] = T(it.c);
+        it.next();
+      }
+    }
+    for (int j = 15 * pe; j < XC; ++j) o[j] = T(0.f);
+  }
+  __syncwarp();
+  const long np = (P - p0) < 32 ? (P - p0) : 32;
+  const int nvec = (int)(np * XC * sizeof(T) / 16);
+  const int4* src = reinterpret_cast<const int4*>(st);
+  int4* dst = reinterpret_cast<int4*>(x + p0 * XC);
+  for (int i = threadIdx.x; i < nvec; i += 32) dst[i] = src[i];
+}
+
 // N3 super-sampler S, SIMT family: x[p] = [G'_hi(12), img(coarse)(3), 0] at the hi-res pixel p
 // (nearest up-sampling: the coarse pixel covering it), G' as k_prep_x.  One thread per pixel.
 template <typename T>
@@ -178,16 +227,23 @@ __device__ __forceinline__ bool rec_less(const T* a, const T* b) {
 //   phi = ReLU(W_B [e0; tau] + b_B)
 //   psi = W_O[:, :c0] phi + W_O[:, c0:] L_d + b_O                    (reading R15)
 // wts (fp32): W1[H][NIN] b1[H] W2[H][H] b2[H] WB[C0][C0+H+1] bB[C0] WO[3][NO] bO[3],
-// NIN = 11 (+ C0 with sigma, N1: h's layer 1 over [record ; e0 at the pixel])
+// NIN = NR (+ C0 with sigma, N1: h's layer 1 over [record ; e0 at the pixel]); NR = 11, or
+// 11 (2 pe_L + 1) with N2's positional encoding of the record (computed here, per fragment)
 template <typename T, int H, int C0>
 __global__ void __launch_bounds__(128) k_tb_simt(
     const T* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const T* __restrict__ e0,
     const T* __restrict__ direct, const float* __restrict__ wts, float* __restrict__ psi,
-    long P, int K, int pool, int r_takes_ld, int norm, int sigma) {
+    long P, int K, int pool, int r_takes_ld, int norm, int sigma, int pe_L) {
   extern __shared__ float sw[];
-  const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0), NIN = 11 + (sigma ? C0 : 0);
+  const int PE = 2 * pe_L + 1, NR = 11 * PE;
+  const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0), NIN = NR + (sigma ? C0 : 0);
   const int nw = H * NIN + H + H * H + H + C0 * NB + C0 + 3 * NO + 3;
   for (int i = threadIdx.x; i < nw; i += blockDim.x) sw[i] = wts[i];
+  if (pe_L) {   // N2: W1 transposed to [NIN][H] so layer 1 reads 4 consecutive outputs per 16-byte load
+    __syncthreads();
+    float* w1t = sw + ((nw + 3) & ~3);
+    for (int i = threadIdx.x; i < H * NIN; i += blockDim.x) w1t[(i % NIN) * H + i / NIN] = sw[i];
+  }
   __syncthreads();
   const float* W1 = sw;
   const float* b1 = W1 + H * NIN;
@@ -220,7 +276,7 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     float a = b1[o];
     if (sigma)
 #pragma unroll
-      for (int j = 0; j < C0; ++j) a = fmaf(W1[o * NIN + 11 + j], ev[j], a);
+      for (int j = 0; j < C0; ++j) a = fmaf(W1[o * NIN + NR + j], ev[j], a);
     u1[o] = a;
   }
   float s[H];
@@ -233,12 +289,47 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     for (int i = 0; i < 11; ++i) x[i] = to_f(r[i]);
     if (norm) x[7] *= 0.0078125f;
     float a1[H];
+    if (pe_L == 0) {
 #pragma unroll
-    for (int o = 0; o < H; ++o) {
-      float a = u1[o];
+      for (int o = 0; o < H; ++o) {
+        float a = u1[o];
 #pragma unroll
-      for (int i = 0; i < 11; ++i) a = fmaf(W1[o * NIN + i], x[i], a);
-      a1[o] = relu(a);
+        for (int i = 0; i < 11; ++i) a = fmaf(W1[o * NIN + i], x[i], a);
+        a1[o] = relu(a);
+      }
+    } else {   // N2: layer 1 over gamma(record), channel by channel (features in index order)
+      const float* w1t = sw + ((nw + 3) & ~3);   // [NIN][H]
+#pragma unroll
+      for (int o = 0; o < H; ++o) a1[o] = u1[o];
+#pragma unroll 1
+      for (int i = 0; i < 11; ++i) {
+        const float v = x[i];
+        const float4* w = reinterpret_cast<const float4*>(w1t + (i * PE) * H);
+#pragma unroll
+        for (int o = 0; o < H / 4; ++o) {
+          const float4 q = w[o];
+          a1[4 * o] = fmaf(q.x, v, a1[4 * o]); a1[4 * o + 1] = fmaf(q.y, v, a1[4 * o + 1]);
+          a1[4 * o + 2] = fmaf(q.z, v, a1[4 * o + 2]); a1[4 * o + 3] = fmaf(q.w, v, a1[4 * o + 3]);
+        }
+        PeIter it(v);
+#pragma unroll 1
+        for (int k = 0; k < pe_L; ++k) {
+          const float4* ws = w + (1 + 2 * k) * (H / 4);
+          const float4* wc = w + (2 + 2 * k) * (H / 4);
+          const float sn = it.s, cs = it.c;
+#pragma unroll
+          for (int o = 0; o < H / 4; ++o) {
+            const float4 q = ws[o], r = wc[o];
+            a1[4 * o] = fmaf(r.x, cs, fmaf(q.x, sn, a1[4 * o]));
+            a1[4 * o + 1] = fmaf(r.y, cs, fmaf(q.y, sn, a1[4 * o + 1]));
+            a1[4 * o + 2] = fmaf(r.z, cs, fmaf(q.z, sn, a1[4 * o + 2]));
+            a1[4 * o + 3] = fmaf(r.w, cs, fmaf(q.w, sn, a1[4 * o + 3]));
+          }
+          it.next();
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < H; ++o) a1[o] = relu(a1[o]);
     }
 #pragma unroll 4
     for (int o = 0; o < H; ++o) {

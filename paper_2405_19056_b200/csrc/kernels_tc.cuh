@@ -128,7 +128,9 @@ inline int tc_pack_weights(glassnet* net, const float* T1W, const float* T1b, co
   // (depth column x 2^-7 when normalising; bf16-exact) at columns 0..10, odd = at columns 1..11;
   // both: b1 as three exact bf16 pieces at columns 12..14 (the record window carries 1.0 there)
   const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
-  const int nin = 11 + (sig ? C0 : 0);   // N1: T1.W rows are [record weights ; sigma weights]
+  // N1: T1.W rows are [record weights ; sigma weights].  With N2 (positional encoding) T runs on
+  // the SIMT kernel and these windows are not used.
+  const int nin = gn_rec_in(d) + (sig ? C0 : 0);
   for (int v = 0; v < 2; ++v) {
     std::vector<float> w1((size_t)H * 16, 0.f);
     for (int n = 0; n < H; ++n) {
@@ -311,7 +313,9 @@ inline int tc_setup_convs(glassnet* net, const std::vector<const float*>& FW, co
   float sc0[16];
   for (int i = 0; i < 16; ++i) sc0[i] = 1.f;
   if (d.flags & GLASSNET_FLAG_INPUT_NORM) { sc0[0] = sc0[1] = sc0[2] = 0.125f; sc0[11] = 0.0078125f; }
-  int rc = setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], 0, sc0);
+  // N2: F0 reads the stored gamma(x) (normalised before the encoding: no weight scale)
+  int rc = gn_pe_L(d) ? setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], gn_x_in(d), gn_x_ch(d), c[0], 0)
+                      : setup_conv(net, s->conv[0], 1, FW[0], net->convB[0], 15, 16, c[0], 0, sc0);
   for (int l = 1; l < L && !rc; ++l) rc = setup_conv(net, s->conv[l], 2, FW[l], net->convB[l], c[l - 1], c[l - 1], c[l], 0);
   for (int l = L - 1; l >= 1 && !rc; --l)
     rc = setup_conv(net, s->conv[4 + l], 1, RW[l], net->convB[4 + l], c[l], c[l], c[l - 1], l == 1 ? 1 : 0);
@@ -332,7 +336,7 @@ static int geom_convs(glassnet* net, Geom& G) {
     g.zout = zout;
     return make_halo_maps(S, g, in, G.Bmax, cin, s->conv[idx].rr);
   };
-  int rc = set(0, 0, 1, G.x16, 16, 0, G.e[0], nullptr);
+  int rc = set(0, 0, 1, G.x16, gn_x_ch(net->d), 0, G.e[0], nullptr);
   for (int l = 1; l < L && !rc; ++l) rc = set(l, l - 1, 2, G.e[l - 1], c[l - 1], l, G.e[l], nullptr);
   for (int l = L - 1; l >= 1 && !rc; --l) {
     void* in = (l == L - 1) ? G.e[L - 1] : G.dd[l];
@@ -404,7 +408,7 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
     G->bytes += bytes;
     return q;
   };
-  bool ok = (G->x16 = alloc((size_t)(G->rows[0] + 2) * G->W[0] * 16 * 2)) != nullptr;
+  bool ok = (G->x16 = alloc((size_t)(G->rows[0] + 2) * G->W[0] * gn_x_ch(d) * 2)) != nullptr;
   for (int l = 0; l < L && ok; ++l) ok = (G->e[l] = alloc((size_t)(G->rows[l] + 2) * G->W[l] * c[l] * 2)) != nullptr;
   for (int l = 2; l < L && ok; ++l) ok = (G->y[l] = alloc((size_t)(G->rows[l] + 2) * G->W[l] * c[l - 1] * 2)) != nullptr;
   for (int l = 1; l < L - 1 && ok; ++l) ok = (G->dd[l] = alloc((size_t)(G->rows[l] + 2) * G->W[l] * c[l] * 2)) != nullptr;

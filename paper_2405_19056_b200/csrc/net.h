@@ -8,6 +8,14 @@
 
 int gn_fail(int code, const char* fmt, ...);
 
+// N2 positional encoding: L_pe, channels per encoded input channel, the encoded widths of a
+// record (h's layer-1 input) and of x (F0's input), and x's stored width (padded to 16).
+inline int gn_pe_L(const glassnet_dims& d) { return GLASSNET_POSENC_OF(d.flags); }
+inline int gn_pe(const glassnet_dims& d) { return 2 * gn_pe_L(d) + 1; }
+inline int gn_rec_in(const glassnet_dims& d) { return 11 * gn_pe(d); }
+inline int gn_x_in(const glassnet_dims& d) { return 15 * gn_pe(d); }
+inline int gn_x_ch(const glassnet_dims& d) { return (gn_x_in(d) + 15) / 16 * 16; }
+
 #include <cuda_runtime.h>
 #include <string>
 

@@ -101,11 +101,12 @@ def _check(rc):
 
 
 def make_dims(height, width, k_slots, widths, t_hidden, levels=None, precision="bf16", max_batch=1,
-              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False, supersample=False) -> Dims:
+              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False, supersample=False, pe_L=0) -> Dims:
     levels = len(widths) if levels is None else levels
     w = (ctypes.c_int32 * 4)(*(list(widths)[:levels] + [0] * (4 - levels)))
     flags = ((FLAG_R_TAKES_LD if r_takes_ld else 0) | (FLAG_INPUT_NORM if input_norm else 0)
-             | (FLAG_SIGMA_COND if sigma_cond else 0) | (FLAG_SUPERSAMPLE if supersample else 0))
+             | (FLAG_SIGMA_COND if sigma_cond else 0) | (FLAG_SUPERSAMPLE if supersample else 0)
+             | (int(pe_L) << 8))   # N2: GLASSNET_FLAG_POSENC(L)
     return Dims(GLASSNET_ABI_VERSION, height, width, max_batch, k_slots, levels, w, t_hidden,
                 BF16 if precision == "bf16" else FP32, POOL_MEAN if pool == "mean" else POOL_SUM, flags)
 

@@ -23,16 +23,20 @@ def sigma_of(cfg):
     return bool(cfg.extra.get("sigma_cond", False))
 
 
+def pe_of(cfg):
+    return int(cfg.extra.get("pe_L", 0))
+
+
 def weights_for(cfg, seed=0):
     return synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=seed,
-                              bf16_weights=(cfg.precision == "bf16"), sigma_cond=sigma_of(cfg))
+                              bf16_weights=(cfg.precision == "bf16"), sigma_cond=sigma_of(cfg), pe_L=pe_of(cfg))
 
 
 def net_for(cfg, max_batch=None, **kw):
     from paper_2405_19056_b200 import GlassNet, make_dims
     dims = make_dims(cfg.height, cfg.width, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels,
                      precision=cfg.precision, max_batch=cfg.batch if max_batch is None else max_batch,
-                     pool=cfg.pool, sigma_cond=sigma_of(cfg), **kw)
+                     pool=cfg.pool, sigma_cond=sigma_of(cfg), pe_L=pe_of(cfg), **kw)
     return GlassNet(weights_for(cfg), dims)
 
 
@@ -57,7 +61,7 @@ def window_oracle(cfg, weights, frame, rows, cols, margin=64, seed=1, mask=None)
     fr = synth.gen_frames(cfg, seed=seed, frame0=frame, nframes=1, rows=(a, b), cols=(c, e), mask=mask)
     g, d, t, n = fr.as64()
     dims = oracle.make_dims(b - a, e - c, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool,
-                            sigma_cond=sigma_of(cfg))
+                            sigma_cond=sigma_of(cfg), pe_L=pe_of(cfg))
     out = oracle.forward(dims, weights.astype(np.float64), g[0], d[0], t[0], n[0])
     return out[rows[0] - a:rows[1] - a, cols[0] - c:cols[1] - c]
 
@@ -99,7 +103,7 @@ def band_oracle(cfg, weights, fr, frame_idx=0, margin=40, threads=None, band=Non
                            fr.precision)
         g, d, t, n = sub.as64()
         dims = oracle.make_dims(b - a, W, cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool,
-                                sigma_cond=sigma_of(cfg))
+                                sigma_cond=sigma_of(cfg), pe_L=pe_of(cfg))
         o = oracle.forward(dims, w64, g[0], d[0], t[0], n[0])
         out[r0:r1] = o[r0 - a:r1 - a]
 
