@@ -15,6 +15,9 @@ Parity status per function:
   og_posenc (N2) pinned (PE1 SPEC S:401-403 examples, PE2 channel count, PE3 torch sin/cos at
               exact dyadic points); forward with pe_L pinned by P15pe (zero sin/cos weights = the
               unencoded network, bitwise) and P10pe (torch-fp64 composition with torch.sin/cos PE)
+  og_forward_objects (N4) pinned (P17 centre-tap convs = the pixel-major network on the slot
+              decomposition, bitwise; PO1 object order bitwise; PO2 garbage outside the coverage
+              bitwise; PO3 locality of an object's contribution; PO4 tau == torch-fp64 conv2d sum)
   og_supersample (N3) pinned (PS1 identity residual = nearest up-sampling, PS2 constant residual
               = clamp(u + beta), PS3 torch-fp64 composition (interpolate nearest + conv2d),
               PS4 receptive field: a coarse pixel reaches only hi-res pixels within 2 of its block)
@@ -45,7 +48,7 @@ class Dims(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("K", ctypes.c_int), ("L", ctypes.c_int),
                 ("c", ctypes.c_int * 4), ("h", ctypes.c_int), ("pool", ctypes.c_int),
                 ("r_takes_ld", ctypes.c_int), ("input_norm", ctypes.c_int), ("sigma_cond", ctypes.c_int),
-                ("pe_L", ctypes.c_int)]
+                ("pe_L", ctypes.c_int), ("objects", ctypes.c_int)]
 
 
 _P = ctypes.POINTER(ctypes.c_double)
@@ -75,16 +78,18 @@ def lib():
 
 
 def make_dims(H, W, K, widths, t_hidden, levels=None, pool="sum", r_takes_ld=True,
-              input_norm=True, sigma_cond=False, pe_L=0) -> Dims:
+              input_norm=True, sigma_cond=False, pe_L=0, objects=False) -> Dims:
     levels = len(widths) if levels is None else levels
     c = (ctypes.c_int * 4)(*(list(widths) + [0] * (4 - len(widths))))
     return Dims(H, W, K, levels, c, t_hidden, 1 if pool == "mean" else 0,
-                1 if r_takes_ld else 0, 1 if input_norm else 0, 1 if sigma_cond else 0, int(pe_L))
+                1 if r_takes_ld else 0, 1 if input_norm else 0, 1 if sigma_cond else 0, int(pe_L),
+                1 if objects else 0)
 
 
 def dims_from_cfg(cfg, H=None, W=None, **kw) -> Dims:
     kw.setdefault("sigma_cond", bool(getattr(cfg, "extra", {}).get("sigma_cond", False)))
     kw.setdefault("pe_L", int(getattr(cfg, "extra", {}).get("pe_L", 0)))
+    kw.setdefault("objects", bool(getattr(cfg, "extra", {}).get("objects", False)))
     return make_dims(cfg.height if H is None else H, cfg.width if W is None else W,
                      cfg.k_slots, cfg.widths, cfg.t_hidden, cfg.levels, pool=cfg.pool, **kw)
 
@@ -195,7 +200,11 @@ def split_weights(d: Dims, weights):
         p += n
 
     pe = 2 * d.pe_L + 1
-    take("T1.W", (h, 11 * pe + (c[0] if d.sigma_cond else 0))); take("T1.b", (h,)); take("T2.W", (h, h)); take("T2.b", (h,))
+    if d.objects:   # N4: h's layers are 3x3 convolutions (OHWI)
+        take("T1.W", (h, 3, 3, 11)); take("T1.b", (h,)); take("T2.W", (h, 3, 3, h)); take("T2.b", (h,))
+    else:
+        take("T1.W", (h, 11 * pe + (c[0] if d.sigma_cond else 0))); take("T1.b", (h,)); take("T2.W", (h, h))
+        take("T2.b", (h,))
     cin = 15 * pe
     for l in range(L):
         take(f"F{l}.W", (c[l], 3, 3, cin)); take(f"F{l}.b", (c[l],)); cin = c[l]
@@ -247,3 +256,38 @@ def posenc(v, L):
     out = np.zeros(v.size * (2 * L + 1))
     lib().og_posenc(_ptr(v), int(v.size), int(L), _ptr(out))
     return out
+
+
+def objects_from_slots(tbuf, tcount, K):
+    """N4's synthetic object buffers: object k holds slot k of every pixel, covered where k < n
+    (the pixel-major frame's information, object-major).  tbuf [H][W][K][11], tcount [H][W]."""
+    objs = [np.ascontiguousarray(tbuf[:, :, k, :]) for k in range(K)]
+    covs = [np.ascontiguousarray((np.asarray(tcount).astype(np.int64) > k).astype(np.uint8)) for k in range(K)]
+    return objs, covs
+
+
+def forward_objects(d: Dims, weights, gbuf, direct, objs, covers, dump=False):
+    """N4: one frame from t object buffers objs[i] [H][W][11] and coverage covers[i] [H][W]."""
+    H, W = d.H, d.W
+    w = _c64(weights)
+    assert d.objects and w.size == weight_count(d), (w.size, weight_count(d))
+    g, dr = _c64(gbuf), _c64(direct)
+    ob = [_c64(o) for o in objs]
+    cv = [np.ascontiguousarray(c, dtype=np.uint8) for c in covers]
+    t = len(ob)
+    for o, c in zip(ob, cv):
+        assert o.shape == (H, W, 11) and c.shape == (H, W)
+    optr = (_P * max(t, 1))(*[_ptr(o) for o in ob])
+    u8p = ctypes.POINTER(ctypes.c_uint8)
+    cptr = (u8p * max(t, 1))(*[c.ctypes.data_as(u8p) for c in cv])
+    out = np.zeros((H, W, 3))
+    arrays, dm = {}, None
+    if dump:
+        arrays["tau"] = np.zeros((H, W, d.h + 1))
+        dm = Dump()
+        dm.tau = _ptr(arrays["tau"])
+    rc = lib().og_forward_objects(ctypes.byref(d), _ptr(w), _ptr(g), _ptr(dr), t, optr, cptr, _ptr(out),
+                                  ctypes.byref(dm) if dm is not None else None)
+    if rc != 0:
+        raise RuntimeError(f"og_forward_objects failed rc={rc}")
+    return (out, arrays) if dump else out

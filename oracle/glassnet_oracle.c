@@ -44,6 +44,7 @@ typedef struct {
   int input_norm;  /* 1: power-of-two input normalisation (R9)    */
   int sigma_cond;  /* 1: h(b, sigma), sigma = e0 at the pixel (N1) */
   int pe_L;        /* N2: positional encoding with L_pe frequencies (0 = off)              */
+  int objects;     /* N4: object-major buffers, h a 3x3 CNN (og_forward_objects)            */
 } og_dims;
 
 typedef struct {        /* optional per-layer dumps (any pointer may be NULL) */
@@ -85,8 +86,9 @@ size_t og_weight_count(const og_dims* d) {
   size_t n = 0;
   int h = d->h;
   const int pe = 2 * d->pe_L + 1;          /* N2: channels per encoded input channel */
-  n += (size_t)h * (11 * pe + (d->sigma_cond ? d->c[0] : 0)) + h;   /* T1 */
-  n += (size_t)h * h + h;                  /* T2 */
+  const int taps = d->objects ? 9 : 1;     /* N4: h's layers are 3x3 convolutions */
+  n += (size_t)h * taps * (11 * pe + (d->sigma_cond ? d->c[0] : 0)) + h;   /* T1 */
+  n += (size_t)h * taps * h + h;           /* T2 */
   int cin = 15 * pe;
   for (int l = 0; l < d->L; ++l) { n += (size_t)d->c[l] * 9 * cin + d->c[l]; cin = d->c[l]; }
   n += (size_t)d->c[0] * (d->c[0] + h + 1) + d->c[0];   /* B */
@@ -190,20 +192,38 @@ void og_T_pixel(const og_dims* d, const double* W1, const double* b1, const doub
   free(a2); free(a1); free(col);
 }
 
-/* One frame. gbuf [H][W][12], direct [H][W][3], tbuf [H][W][K][11], tcount [H][W].
- * out [H][W][3] in [0,1].  Returns 0 on success. */
-int og_forward(const og_dims* d, const double* wts, const double* gbuf, const double* direct,
-               const double* tbuf, const uint8_t* tcount, double* out, const og_dump* dump) {
+/* N4 -- object-major transparency buffers with a spatial h (PAPER.md P:257-258
+ * "a set of buffers with a size of (w, h, c*(t+1))" -- one full-frame buffer per transparent
+ * object; "other networks use multi-layer CNN without down-sampling"; streaming,
+ * "the model can operate on a single buffer of each transparent object, and then add
+ * it to the summed latent representation").  DESIGN.md reading N4:
+ *   x_i   = cover_i ? b_i' : 0        b_i' = b_i with depth x 2^-7 (R9); 11 ch per pixel
+ *   a_i   = ReLU(conv3x3(ReLU(conv3x3(x_i; T1)); T2))      h, zero padding, no down-sampling
+ *   tau   = [ sum_{i covering the pixel} a_i , n ]      n = number of covering objects
+ * (the per-channel sum taken over the values sorted ascending: a function of the multiset of
+ * objects, so object order cannot change a bit); B, F, R and the output as og_forward.
+ * T1.W [h][3][3][11], T2.W [h][3][3][h] (OHWI) replace the MLP weights in the blob. */
+typedef struct {
+  int t;                      /* number of objects              */
+  const double* const* buf;   /* t x [H][W][11]                 */
+  const uint8_t* const* cover;/* t x [H][W], nonzero = covered  */
+} og_objects;
+
+static int og_forward_impl(const og_dims* d, const double* wts, const double* gbuf, const double* direct,
+                           const double* tbuf, const uint8_t* tcount, const og_objects* ob, double* out,
+                           const og_dump* dump) {
   const int H = d->H, W = d->W, K = d->K, L = d->L, h = d->h;
   const int* c = d->c;
   const size_t P = (size_t)H * W;
   if (L < 2 || L > 4 || K < 1 || H < 1 || W < 1 || d->pe_L < 0 || d->pe_L > 10) return 1;
+  if ((ob != 0) != (d->objects != 0) || (ob && (d->pe_L || d->sigma_cond))) return 1;
+  const int taps = ob ? 9 : 1;
   const int pe = 2 * d->pe_L + 1, nx = 15 * pe;          /* N2: encoded input width */
 
   /* ---- unpack the weight blob (SURVEY.md §8(b) order) ---- */
   const double* p = wts;
-  const double *T1W = p; p += (size_t)h * (11 * pe + (d->sigma_cond ? c[0] : 0)); const double* T1b = p; p += h;
-  const double *T2W = p; p += (size_t)h * h;  const double* T2b = p; p += h;
+  const double *T1W = p; p += (size_t)h * taps * (11 * pe + (d->sigma_cond ? c[0] : 0)); const double* T1b = p; p += h;
+  const double *T2W = p; p += (size_t)h * taps * h;  const double* T2b = p; p += h;
   const double *FW[4], *Fb[4];
   int cin = nx;
   for (int l = 0; l < L; ++l) { FW[l] = p; p += (size_t)c[l] * 9 * cin; Fb[l] = p; p += c[l]; cin = c[l]; }
@@ -239,9 +259,47 @@ int og_forward(const og_dims* d, const double* wts, const double* gbuf, const do
   }
   /* ---- 3. T ---- */
   double* tau = (double*)malloc(sizeof(double) * P * (h + 1));
-  for (size_t q = 0; q < P; ++q)
-    og_T_pixel(d, T1W, T1b, T2W, T2b, tbuf + q * (size_t)K * 11, (int)tcount[q], e[0] + q * c[0],
-               tau + q * (h + 1));
+  if (!ob) {
+    for (size_t q = 0; q < P; ++q)
+      og_T_pixel(d, T1W, T1b, T2W, T2b, tbuf + q * (size_t)K * 11, (int)tcount[q], e[0] + q * c[0],
+                 tau + q * (h + 1));
+  } else {   /* N4: one object buffer at a time through the spatial h */
+    const int t = ob->t;
+    double* vals = (double*)malloc(sizeof(double) * P * (size_t)(t > 0 ? t : 1) * h);
+    int* cnt = (int*)calloc(P, sizeof(int));
+    double* xi = (double*)malloc(sizeof(double) * P * 11);
+    double* h1 = (double*)malloc(sizeof(double) * P * h);
+    double* a2 = (double*)malloc(sizeof(double) * P * h);
+    double* col = (double*)malloc(sizeof(double) * (size_t)(t > 0 ? t : 1));
+    for (int i = 0; i < t; ++i) {
+      for (size_t q = 0; q < P; ++q)
+        for (int j = 0; j < 11; ++j) {
+          double v = ob->cover[i][q] ? ob->buf[i][q * 11 + j] : 0.0;
+          if (j == 7 && d->input_norm) v = v * 0x1p-7;
+          xi[q * 11 + j] = v;
+        }
+      og_conv3x3(xi, H, W, 11, T1W, T1b, h, 1, 1, h1);
+      og_conv3x3(h1, H, W, h, T2W, T2b, h, 1, 1, a2);
+      for (size_t q = 0; q < P; ++q)
+        if (ob->cover[i][q]) {
+          for (int j = 0; j < h; ++j) vals[(q * t + cnt[q]) * h + j] = a2[q * h + j];
+          cnt[q] += 1;
+        }
+    }
+    for (size_t q = 0; q < P; ++q) {
+      const int m = cnt[q];
+      for (int j = 0; j < h; ++j) {
+        for (int k = 0; k < m; ++k) col[k] = vals[(q * t + k) * h + j];
+        qsort(col, (size_t)m, sizeof(double), cmp_double);
+        double sm = 0.0;
+        for (int k = 0; k < m; ++k) sm += col[k];
+        if (d->pool == 1) sm = m > 0 ? sm / (double)m : 0.0;
+        tau[q * (h + 1) + j] = sm;
+      }
+      tau[q * (h + 1) + h] = (double)m;
+    }
+    free(vals); free(cnt); free(xi); free(h1); free(a2); free(col);
+  }
   /* ---- 4. B ---- */
   double* phi = (double*)malloc(sizeof(double) * P * c[0]);
   for (size_t q = 0; q < P; ++q)
@@ -345,4 +403,18 @@ int og_supersample(int H, int W, int s, int input_norm, const double* wts, const
     }
   free(x); free(u); free(s1); free(s2);
   return 0;
+}
+
+/* One frame. gbuf [H][W][12], direct [H][W][3], tbuf [H][W][K][11], tcount [H][W].
+ * out [H][W][3] in [0,1].  Returns 0 on success. */
+int og_forward(const og_dims* d, const double* wts, const double* gbuf, const double* direct,
+               const double* tbuf, const uint8_t* tcount, double* out, const og_dump* dump) {
+  return og_forward_impl(d, wts, gbuf, direct, tbuf, tcount, 0, out, dump);
+}
+
+/* N4: one frame from t object buffers (obj[i] [H][W][11], cover[i] [H][W]); d->objects = 1. */
+int og_forward_objects(const og_dims* d, const double* wts, const double* gbuf, const double* direct, int t,
+                       const double* const* obj, const uint8_t* const* cover, double* out, const og_dump* dump) {
+  og_objects ob = {t, obj, cover};
+  return og_forward_impl(d, wts, gbuf, direct, 0, 0, &ob, out, dump);
 }

@@ -160,7 +160,7 @@ CONFIGS = {
 
 
 # --------------------------------------------------------------------------- weights
-def layer_shapes(widths, levels, t_hidden, r_takes_ld=True, sigma_cond=False, pe_L=0):
+def layer_shapes(widths, levels, t_hidden, r_takes_ld=True, sigma_cond=False, pe_L=0, objects=False):
     """(name, W shape, fan_in) in blob order (SURVEY.md §8(b) 'Weights blob').  sigma_cond
     (SURVEY §8(f) N1): h's first layer also takes sigma = e0 at the pixel, T1.W [h][11 + c0].
     pe_L (N2): the inputs are positionally encoded, 11 -> 11(2L+1), 15 -> 15(2L+1) channels."""
@@ -168,7 +168,10 @@ def layer_shapes(widths, levels, t_hidden, r_takes_ld=True, sigma_cond=False, pe
     h = t_hidden
     pe = 2 * pe_L + 1
     n1 = 11 * pe + (c[0] if sigma_cond else 0)
-    out = [("T1", (h, n1), n1), ("T2", (h, h), h)]
+    if objects:   # N4: h's layers are 3x3 convolutions (OHWI)
+        out = [("T1", (h, 3, 3, 11), 99), ("T2", (h, 3, 3, h), 9 * h)]
+    else:
+        out = [("T1", (h, n1), n1), ("T2", (h, h), h)]
     cin = 15 * pe
     for lv in range(levels):
         out.append((f"F{lv}", (c[lv], 3, 3, cin), 9 * cin))
@@ -181,18 +184,19 @@ def layer_shapes(widths, levels, t_hidden, r_takes_ld=True, sigma_cond=False, pe
     return out
 
 
-def weight_count(widths, levels, t_hidden, r_takes_ld=True, sigma_cond=False, pe_L=0):
+def weight_count(widths, levels, t_hidden, r_takes_ld=True, sigma_cond=False, pe_L=0, objects=False):
     n = 0
-    for _, shp, _ in layer_shapes(widths, levels, t_hidden, r_takes_ld, sigma_cond, pe_L):
+    for _, shp, _ in layer_shapes(widths, levels, t_hidden, r_takes_ld, sigma_cond, pe_L, objects):
         n += int(np.prod(shp)) + shp[0]
     return n
 
 
-def make_weights(widths, levels, t_hidden, seed=0, r_takes_ld=True, bf16_weights=False, sigma_cond=False, pe_L=0):
+def make_weights(widths, levels, t_hidden, seed=0, r_takes_ld=True, bf16_weights=False, sigma_cond=False, pe_L=0,
+                 objects=False):
     """Flat little-endian fp32 blob.  If bf16_weights, every W tensor (not the biases)
     is rounded RNE to a bf16-representable fp32 (SURVEY.md §8(c) preamble)."""
     parts = []
-    for li, (_, shp, fan_in) in enumerate(layer_shapes(widths, levels, t_hidden, r_takes_ld, sigma_cond, pe_L)):
+    for li, (_, shp, fan_in) in enumerate(layer_shapes(widths, levels, t_hidden, r_takes_ld, sigma_cond, pe_L, objects)):
         key = splitmix64_int((seed * 4096 + 1000 + li) & MASK64)
         nW = int(np.prod(shp))
         idx = np.arange(nW, dtype=np.uint64)
