@@ -247,7 +247,51 @@ def run_extras(net, cfg, g, d, t, n, args):
         net2.close()
         del g2, d2, t2, n2, o2
     res["n3_supersample_c3"] = run_supersample(cfg, out, args)
+    res["n4_objects_c3"] = run_objects(cfg, g, d, t, n, args)
     return res
+
+
+def run_objects(cfg, g, d, t, n, args, nf=8):
+    """N4: the object-major path with a spatial h on nf c3 frames, the K slots as
+    K full-frame object buffers (object k = slot k, covered where k < n): begin + K adds + finish,
+    tensor-core family; per-stage times."""
+    import torch
+    from paper_2405_19056_b200 import GlassNet, make_dims
+    H, W, K = cfg.height, cfg.width, cfg.k_slots
+    w = synth.make_weights(cfg.widths, cfg.levels, cfg.t_hidden, seed=0, bf16_weights=True, objects=True)
+    net = GlassNet(w, make_dims(H, W, K, cfg.widths, cfg.t_hidden, cfg.levels, max_batch=nf, objects=True))
+    objs = [t[:nf, :, :, k, :].contiguous() for k in range(K)]
+    covs = [(n[:nf] > k).to(torch.uint8).contiguous() for k in range(K)]
+    gg, dd = g[:nf], d[:nf]
+    o = torch.empty((nf, H, W, 3), dtype=torch.float32, device="cuda")
+
+    def run():
+        net.objects_begin(nf)
+        for k in range(K):
+            net.objects_add(objs[k], covs[k])
+        net.objects_finish(gg, dd, o)
+    steps = max(3, args.steps // 2)
+    ms = _time_forward(run, steps, 2)
+    net.profile_begin((4 * K + 24) * steps + 4)
+    for _ in range(steps):
+        run()
+    st = net.profile_end()
+    torch.cuda.synchronize()
+    P = H * W
+    h = cfg.t_hidden
+    fl = {"obj_h1": 2 * 9 * 11 * h * P, "obj_h2_accum": 2 * 9 * h * h * P}   # per object and frame
+    stages = {}
+    for k, (tot, cnt) in st.items():
+        per = tot / cnt
+        e = {"ms_per_launch": per, "launches_per_call": cnt / steps}
+        if k in fl:
+            e["alg_TFLOPs"] = fl[k] * nf / (per / 1000.0) / 1e12
+        stages[k] = e
+    net.close()
+    del objs, covs, o
+    return {"workload": f"N4: {nf} frames {W}x{H}, {K} object buffers (object k = slot k), h = 2 conv3x3 "
+                        f"(11->{h}->{h}), bf16 tensor cores", "ms_per_call": ms, "ms_per_frame": ms / nf,
+            "frames_per_s": nf * 1000.0 / ms, "stages": stages}
 
 
 def run_supersample(cfg, img, args, nf=8):

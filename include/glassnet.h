@@ -32,6 +32,7 @@
  * Weights: one little-endian fp32 host blob, in this order (conv weights OHWI,
  * cross-correlation, tap (ky,kx) reads offset (ky-1,kx-1)):
  *   (with GLASSNET_FLAG_POSENC(L): every "11" below is 11(2L+1) and F0's "15" is 15(2L+1))
+ *   (with GLASSNET_FLAG_OBJECTS: T1.W[h][3][3][11], T2.W[h][3][3][h] -- h's two 3x3 convolutions)
  *   T1.W[h][11] T1.b[h] T2.W[h][h] T2.b[h]   (GLASSNET_FLAG_SIGMA_COND: T1.W[h][11 + c0] --
  *                                             the paper's h(b_i, sigma), Eq. eq:SymmetricNN
  *                                             P:308-316, layer 1 over [record ; e0 at the
@@ -68,7 +69,8 @@ enum { GLASSNET_POOL_SUM = 0, GLASSNET_POOL_MEAN = 1 };  /* g of Eq. eq:Symmetri
 enum { GLASSNET_FLAG_R_TAKES_LD = 1u << 0,               /* reading R15, default on     */
        GLASSNET_FLAG_INPUT_NORM = 1u << 1,               /* reading R9, default on      */
        GLASSNET_FLAG_SIGMA_COND = 1u << 2,               /* N1, default off: h(b, sigma) */
-       GLASSNET_FLAG_SUPERSAMPLE = 1u << 3 };            /* N3, default off: the x2 super-sampler S */
+       GLASSNET_FLAG_SUPERSAMPLE = 1u << 3,              /* N3, default off: the x2 super-sampler S */
+       GLASSNET_FLAG_OBJECTS = 1u << 4 };                /* N4, default off: object-major T (below) */
 /* N2 (default off): positional encoding with L_pe = 1..10 frequencies of every input channel
  * (§3.4 P:373-375 "All the inputs use positional encoding by Mildenhall et al.";
  * SPEC.md S:395-403): gamma(v) = (v, sin(2^0 pi v), cos(2^0 pi v), ..., sin(2^(L-1) pi v),
@@ -165,6 +167,28 @@ int glassnet_debug_psi(glassnet_t net, float* dst, int32_t batch, glassnet_strea
  * the flag). */
 int glassnet_supersample(glassnet_t net, const float* img, const void* gbuf_hi, float* out_hi, int32_t batch,
                          glassnet_stream_t stream);
+
+/* N4 -- object-major transparency buffers with a spatial h, streamed one object at a time
+ * (one (w, h, c) buffer per transparent object; P:366-368:
+ * T is a "multi-layer CNN without down-sampling"; "the model can operate on a single
+ * buffer of each transparent object, and then add it to the summed latent representation" --
+ * constant memory in the number of objects).  Needs a handle created with GLASSNET_FLAG_OBJECTS
+ * (not combinable with SIGMA_COND or POSENC; glassnet_forward then returns UNSUPPORTED):
+ *   a_i = ReLU(conv3x3(ReLU(conv3x3(x_i; T1)); T2)),  x_i = cover_i ? b_i' : 0 (b_i' = R9-normalised)
+ *   tau = [ sum over covering objects of a_i , number of covering objects ]
+ * accumulated as an exact fixed-point integer sum (round(a_i * 2^12) in bf16 mode, 2^20 in fp32
+ * check mode; uint32 per channel), so the order of the objects cannot change a bit.
+ *   begin:  tau := 0 for `batch` frames.
+ *   add:    obj [B][H][W][11] (element type = dims.precision; uncovered pixels may hold any bits),
+ *           cover [B][H][W] uint8 (nonzero = the object covers the pixel); adds this object.
+ *   finish: gbuf, direct, out as glassnet_forward; runs F, B (over tau), R and the output.
+ * All device pointers, enqueued on `stream`, no allocation.  Calls on one handle must be ordered
+ * begin, add*, finish on one stream. */
+int glassnet_objects_begin(glassnet_t net, int32_t batch, glassnet_stream_t stream);
+int glassnet_objects_add(glassnet_t net, const void* obj, const uint8_t* cover, int32_t batch,
+                         glassnet_stream_t stream);
+int glassnet_objects_finish(glassnet_t net, const void* gbuf, const void* direct, float* out, int32_t batch,
+                            glassnet_stream_t stream);
 
 /* ---- row-tile sharding (one process per GPU, NCCL point-to-point halos) ---- */
 

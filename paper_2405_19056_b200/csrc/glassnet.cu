@@ -67,8 +67,10 @@ static int validate_dims(const glassnet_dims* d) {
   if (d->t_hidden != 16 && d->t_hidden != 32 && d->t_hidden != 64)
     return gn_fail(GLASSNET_ERR_UNSUPPORTED, "t_hidden must be 16, 32 or 64");
   if (gn_pe_L(*d) > 10) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "positional encoding L_pe must be <= 10");
-  if (d->flags & ~(0xFu | (0xFu << 8)))
-    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "unknown flag bits 0x%x", d->flags & ~(0xFu | (0xFu << 8)));
+  if (d->flags & ~(0x1Fu | (0xFu << 8)))
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "unknown flag bits 0x%x", d->flags & ~(0x1Fu | (0xFu << 8)));
+  if ((d->flags & GLASSNET_FLAG_OBJECTS) && ((d->flags & GLASSNET_FLAG_SIGMA_COND) || gn_pe_L(*d)))
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "GLASSNET_FLAG_OBJECTS with SIGMA_COND or POSENC is not implemented");
   return GLASSNET_OK;
 }
 
@@ -77,7 +79,8 @@ extern "C" size_t glassnet_weight_count(const glassnet_dims* d) {
   const int h = d->t_hidden, L = d->levels;
   const int* c = d->widths;
   const int nin = gn_rec_in(*d) + ((d->flags & GLASSNET_FLAG_SIGMA_COND) ? d->widths[0] : 0);   // N1: [record ; e0]
-  size_t n = (size_t)h * nin + h + (size_t)h * h + h;
+  const int taps = (d->flags & GLASSNET_FLAG_OBJECTS) ? 9 : 1;   // N4: h's layers are 3x3 convs
+  size_t n = (size_t)h * taps * nin + h + (size_t)h * taps * h + h;
   int cin = gn_x_in(*d);   // N2: 15 (2 L_pe + 1)
   for (int l = 0; l < L; ++l) { n += (size_t)c[l] * 9 * cin + c[l]; cin = c[l]; }
   n += (size_t)c[0] * (c[0] + h + 1) + c[0];
@@ -141,8 +144,10 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   std::vector<const float*> FW(L), Fb(L), RW(L), Rb(L);
   const bool sig = (d.flags & GLASSNET_FLAG_SIGMA_COND) != 0;
   const int nin = gn_rec_in(d) + (sig ? c[0] : 0);
-  const float *T1W = p; p += (size_t)h * nin; const float* T1b = p; p += h;
-  const float *T2W = p; p += (size_t)h * h; const float* T2b = p; p += h;
+  const bool objm = (d.flags & GLASSNET_FLAG_OBJECTS) != 0;
+  const int taps = objm ? 9 : 1;   // N4: T1.W [h][3][3][11], T2.W [h][3][3][h]
+  const float *T1W = p; p += (size_t)h * taps * nin; const float* T1b = p; p += h;
+  const float *T2W = p; p += (size_t)h * taps * h; const float* T2b = p; p += h;
   const int XIN = gn_x_in(d), XC = gn_x_ch(d);   // N2: F0's input channels (real, stored)
   int cin = XIN;
   for (int l = 0; l < L; ++l) { FW[l] = p; p += (size_t)c[l] * 9 * cin; Fb[l] = p; p += c[l]; cin = c[l]; }
@@ -161,10 +166,11 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
 
   // ---- SIMT packs ----
   std::vector<float> tb;
-  for (int i = 0; i < h * nin; ++i) tb.push_back(W(T1W[i]));
+  for (int i = 0; i < h * taps * nin; ++i) tb.push_back(W(T1W[i]));
   for (int i = 0; i < h; ++i) tb.push_back(T1b[i]);
-  for (int i = 0; i < h * h; ++i) tb.push_back(W(T2W[i]));
+  for (int i = 0; i < h * taps * h; ++i) tb.push_back(W(T2W[i]));
   for (int i = 0; i < h; ++i) tb.push_back(T2b[i]);
+  net->wb_off = tb.size();
   for (int i = 0; i < c[0] * NB; ++i) tb.push_back(W(BW[i]));
   for (int i = 0; i < c[0]; ++i) tb.push_back(Bb[i]);
   for (int i = 0; i < 3 * NO; ++i) tb.push_back(W(OW[i]));
@@ -197,6 +203,19 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   for (int o = 0; o < 3; ++o)
     for (int i = 0; i < c[0]; ++i) wz[(size_t)o * c[0] + i] = W(OW[(size_t)o * NO + i]);
   if ((rc = dev_upload(&net->wz, wz, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+  if (objm) {   // N4: h's convs for the SIMT family (T1 over the 16-channel object input)
+    pack_conv(T1W, h, 11, 16, tmp);
+    if ((rc = dev_upload(&net->objW[0], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    pack_conv(T2W, h, h, h, tmp);
+    if ((rc = dev_upload(&net->objW[1], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
+    std::vector<float> b1(T1b, T1b + h), b2(T2b, T2b + h);
+    if ((rc = dev_upload(&net->objB[0], b1, &net->w_bytes)) || (rc = dev_upload(&net->objB[1], b2, &net->w_bytes))) {
+      glassnet_destroy(net);
+      return rc;
+    }
+    net->qscale = bf ? 4096.f : 1048576.f;   // 2^12 (R5's format) / 2^20 (fp32 check mode)
+    net->qsat = bf ? 2048.f : 256.f;
+  }
   if (ss) {
     pack_conv(S1W, c[0], 15, 16, tmp);
     if ((rc = dev_upload(&net->ssW[0], tmp, &net->w_bytes))) { glassnet_destroy(net); return rc; }
@@ -229,6 +248,11 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
   for (int l = 1; l < L - 1 && !rc; ++l) rc = alloc(&net->dd[l], B * Hl[l] * Wl[l] * c[l] * es);
   if (!rc) rc = alloc((void**)&net->z, B * Hl[1] * Wl[1] * 3 * sizeof(float));
   if (ss && !rc) rc = alloc(&net->ss_s1, B * 4 * P0 * c[0] * es);
+  if (objm && !rc) rc = alloc(&net->obj_x, B * P0 * 16 * es);
+  if (objm && !rc) rc = alloc(&net->obj_h1, B * P0 * h * es);
+  if (objm && !rc) rc = alloc(&net->obj_a2, B * P0 * h * es);
+  if (objm && !rc) rc = alloc((void**)&net->tau_q, B * P0 * h * sizeof(uint32_t));
+  if (objm && !rc) rc = alloc((void**)&net->tau_n, B * P0 * sizeof(uint32_t));
   if (ss && !rc) rc = alloc(&net->ss_x, B * 4 * P0 * 16 * es);      // SIMT family only: x and r stored
   if (ss && !rc) rc = alloc((void**)&net->ss_r, B * 4 * P0 * 3 * sizeof(float));
   if (rc) { glassnet_destroy(net); return rc; }
@@ -239,6 +263,7 @@ extern "C" int glassnet_create(const float* weights, size_t n_weights, const gla
     if (!rc) rc = gn::tc_setup_convs(net, FW, RW);
     if (!rc) rc = gn::tc_setup_full_geom(net);
     if (!rc && ss) rc = gn::tc_setup_ss(net, S1W, S2W);
+    if (!rc && objm) rc = gn::tc_setup_objects(net, T1W, T2W);
     if (rc) { glassnet_destroy(net); return rc; }
   }
   net->tc = bf && gn::tc_supported(d);
@@ -251,7 +276,8 @@ extern "C" void glassnet_destroy(glassnet_t net) {
   cudaSetDevice(net->dev);
   void* ptrs[] = {net->w_tb, net->wz, net->x16, net->psi, net->z, net->st_g, net->st_d, net->st_t,
                   net->st_n, net->st_o, net->ssW[0], net->ssW[1], net->ssB[0], net->ssB[1], net->ss_wz,
-                  net->ss_s1, net->ss_x, net->ss_r};
+                  net->ss_s1, net->ss_x, net->ss_r, net->objW[0], net->objW[1], net->objB[0], net->objB[1],
+                  net->obj_x, net->obj_h1, net->obj_a2, net->tau_q, net->tau_n};
   for (void* q : ptrs) if (q) cudaFree(q);
   if (net->st_in) cudaStreamDestroy(net->st_in);
   if (net->st_out) cudaStreamDestroy(net->st_out);
@@ -329,6 +355,26 @@ static void launch_tb_simt(glassnet* net, const T* tbuf, const uint8_t* tcount, 
 #undef TB_LAUNCH
 }
 
+// N4: B + psi from tau_q / tau_n (kernels_simt.cuh k_b_psi), both families.
+template <typename T>
+static void launch_b_psi(glassnet* net, const T* e0, const T* direct, float* psi, long P0, cudaStream_t st) {
+  const glassnet_dims& d = net->d;
+  const int h = d.t_hidden, c0 = d.widths[0];
+  const int ld = (d.flags & GLASSNET_FLAG_R_TAKES_LD) ? 1 : 0;
+  const float* wb = net->w_tb + net->wb_off;
+  const unsigned g = nblk(P0, 128);
+  const float iq = 1.f / net->qscale;
+#define BP_LAUNCH(HH, CC) \
+  gn::k_b_psi<T, HH, CC><<<g, 128, 0, st>>>(e0, net->tau_q, net->tau_n, direct, wb, psi, P0, d.pool, ld, iq);
+  if (h == 64 && c0 == 32) BP_LAUNCH(64, 32)
+  else if (h == 64 && c0 == 16) BP_LAUNCH(64, 16)
+  else if (h == 32 && c0 == 32) BP_LAUNCH(32, 32)
+  else if (h == 32 && c0 == 16) BP_LAUNCH(32, 16)
+  else if (h == 16 && c0 == 32) BP_LAUNCH(16, 32)
+  else BP_LAUNCH(16, 16)
+#undef BP_LAUNCH
+}
+
 template <typename T>
 static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* tbuf, const uint8_t* tcount,
                         float* out, int B, cudaStream_t st) {
@@ -371,7 +417,10 @@ static int forward_simt(glassnet* net, const T* gbuf, const T* direct, const T* 
   for (int l = 0; l < L; ++l) e[l] = (T*)net->e[l];
   conv(x16, 0, XC, 0, c[0], 1, e[0], 0);
   for (int l = 1; l < L; ++l) conv(e[l - 1], l - 1, c[l - 1], l, c[l], 2, e[l], 0);
-  launch_tb_simt<T>(net, tbuf, tcount, e[0], direct, net->psi, P0, st);
+  if (d.flags & GLASSNET_FLAG_OBJECTS)   // N4: B + psi over the streamed latent
+    launch_b_psi<T>(net, e[0], direct, net->psi, P0, st);
+  else
+    launch_tb_simt<T>(net, tbuf, tcount, e[0], direct, net->psi, P0, st);
   net->prof.mark("T_B_psi", st);
   // R: d_{L-1} = e_{L-1}
   const T* dcur = e[L - 1];
@@ -456,6 +505,14 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
   typedef __nv_bfloat16 bf;
   switch (sp.kind) {
     case ST_PREP: {
+      if (d.flags & GLASSNET_FLAG_OBJECTS) {   // N4: no records to sort; F0 reads the G-buffer
+        if (!tile) return 0;
+        bf* x = (bf*)G.x16 + (size_t)h * G.W[0] * 16;
+        const dim3 grid((unsigned)((G.W[0] + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
+        ew::k_prep_x<<<grid, 256, 0, st>>>((const bf*)gbuf, (const bf*)direct, x, G.W[0], G.rows[0], 0);
+        net->prof.mark("prep_x", st);
+        return 0;
+      }
       if (gn_pe_L(d)) {   // N2: x = gamma([G', L_d]) stored (XC channels) for F0's TMA halo; T runs SIMT
         const int XC = gn_x_ch(d);
         bf* x = (bf*)G.x16 + (size_t)h * G.W[0] * XC;
@@ -485,6 +542,12 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
     }
     case ST_TB: {
       const bf* e0 = (const bf*)G.e[0] + (size_t)h * G.W[0] * c[0];
+      if (d.flags & GLASSNET_FLAG_OBJECTS) {   // N4: B + psi over the streamed latent
+        if (tile) return gn_fail(GLASSNET_ERR_UNSUPPORTED, "row tiles with GLASSNET_FLAG_OBJECTS");
+        launch_b_psi<bf>(net, e0, (const bf*)direct, G.psi, P0, st);
+        net->prof.mark("T_B_psi", st);
+        return 0;
+      }
       if (gn_pe_L(d)) {   // N2: T over the encoded records on the SIMT kernel (same stream order)
         launch_tb_simt<bf>(net, (const bf*)tbuf, tcount, e0, (const bf*)direct, G.psi, P0, st);
         net->prof.mark("T_B_psi", st);
@@ -527,7 +590,7 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       g.rows_f = G.rows[0]; g.rows_f_buf = G.rows[0] + 2 * h; g.grow0_f = G.grow0[0];
       g.rows_c_buf = G.rows[1] + 2 * h; g.grow0_c = G.grow0[1]; g.Hc_full = G.Hfull[1]; g.halo = h;
       const dim3 grid((unsigned)((G.W[0] / 2 + 255) / 256), (unsigned)G.rows[0], (unsigned)B);
-      if (tile && !gn_pe_L(d)) cudaStreamWaitEvent(st, s->ev_tb, 0);   // psi from T's stream
+      if (tile && !gn_pe_L(d) && !(d.flags & GLASSNET_FLAG_OBJECTS)) cudaStreamWaitEvent(st, s->ev_tb, 0);   // psi from T's stream
       ew::k_output<<<grid, 256, 0, st>>>(G.z, G.W[1], G.psi, out, G.W[0], g);
       net->prof.mark("output", st);
       return 0;
@@ -568,6 +631,8 @@ extern "C" int glassnet_forward(glassnet_t net, const void* gbuf, const void* di
   if (!tcount) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "tcount is NULL");
   if (batch < 1 || batch > net->d.max_batch)
     return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "batch=%d outside [1, max_batch=%d]", batch, net->d.max_batch);
+  if (net->d.flags & GLASSNET_FLAG_OBJECTS)
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "GLASSNET_FLAG_OBJECTS handle: use glassnet_objects_begin/add/finish");
   CUDA_TRY(cudaSetDevice(net->dev));
   cudaStream_t st = (cudaStream_t)stream;
   if (net->d.precision == GLASSNET_FP32)
@@ -662,6 +727,88 @@ extern "C" int glassnet_forward_host(glassnet_t net, const void* gbuf, const voi
   if (rc) return rc;
   CUDA_TRY(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3);
   return GLASSNET_OK;
+}
+
+// ------------------------------------------------------------------------ N4 object-major T
+static int objects_check(glassnet* net, int32_t batch) {
+  if (!net) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "net is NULL");
+  if (!(net->d.flags & GLASSNET_FLAG_OBJECTS))
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "the handle was created without GLASSNET_FLAG_OBJECTS");
+  if (batch < 1 || batch > net->d.max_batch)
+    return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "batch=%d outside [1, max_batch=%d]", batch, net->d.max_batch);
+  CUDA_TRY(cudaSetDevice(net->dev));
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_objects_begin(glassnet_t net, int32_t batch, glassnet_stream_t stream) {
+  int rc = objects_check(net, batch);
+  if (rc) return rc;
+  const size_t P = (size_t)batch * net->d.height * net->d.width;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(net->tau_q, 0, P * net->d.t_hidden * sizeof(uint32_t), st));
+  CUDA_TRY(cudaMemsetAsync(net->tau_n, 0, P * sizeof(uint32_t), st));
+  return GLASSNET_OK;
+}
+
+template <typename T>
+static int objects_add_simt(glassnet* net, const T* obj, const uint8_t* cover, int B, cudaStream_t st) {
+  const glassnet_dims& d = net->d;
+  const int H = d.height, W = d.width, h = d.t_hidden;
+  const long P = (long)B * H * W;
+  T* x = (T*)net->obj_x;
+  T* h1 = (T*)net->obj_h1;
+  T* a2 = (T*)net->obj_a2;
+  net->prof.mark(nullptr, st);
+  gn::k_obj_prep<T><<<nblk(P, 256), 256, 0, st>>>(obj, cover, x, P, (d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
+  net->prof.mark("obj_prep", st);
+  const int nj = h >= 32 ? 32 : 16;
+  const dim3 grid(nblk(P, 128), h / nj);
+  if (nj == 32) {
+    gn::k_conv3x3_simt<T, 32, 0><<<grid, 128, 0, st>>>(x, H, W, 16, net->objW[0], net->objB[0], h, 1, h1, H, W, P, nullptr, nullptr);
+    gn::k_conv3x3_simt<T, 32, 0><<<grid, 128, 0, st>>>(h1, H, W, h, net->objW[1], net->objB[1], h, 1, a2, H, W, P, nullptr, nullptr);
+  } else {
+    gn::k_conv3x3_simt<T, 16, 0><<<grid, 128, 0, st>>>(x, H, W, 16, net->objW[0], net->objB[0], h, 1, h1, H, W, P, nullptr, nullptr);
+    gn::k_conv3x3_simt<T, 16, 0><<<grid, 128, 0, st>>>(h1, H, W, h, net->objW[1], net->objB[1], h, 1, a2, H, W, P, nullptr, nullptr);
+  }
+  net->prof.mark("obj_h", st);
+  gn::k_obj_accum<T><<<nblk(P, 256), 256, 0, st>>>(a2, cover, net->tau_q, net->tau_n, P, h, net->qscale, net->qsat);
+  net->prof.mark("obj_accum", st);
+  CUDA_TRY(cudaGetLastError());
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_objects_add(glassnet_t net, const void* obj, const uint8_t* cover, int32_t batch,
+                                    glassnet_stream_t stream) {
+  int rc = objects_check(net, batch);
+  if (rc) return rc;
+  if ((rc = check_ptr(obj, "obj"))) return rc;
+  if (!cover) return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "cover is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (net->d.precision == GLASSNET_FP32) return objects_add_simt<float>(net, (const float*)obj, cover, batch, st);
+  if (!net->tc) return objects_add_simt<__nv_bfloat16>(net, (const __nv_bfloat16*)obj, cover, batch, st);
+  const long P = (long)batch * net->d.height * net->d.width;
+  net->prof.mark(nullptr, st);
+  gn::k_obj_prep<__nv_bfloat16><<<nblk(P, 256), 256, 0, st>>>((const __nv_bfloat16*)obj, cover,
+                                                              (__nv_bfloat16*)net->obj_x, P,
+                                                              (net->d.flags & GLASSNET_FLAG_INPUT_NORM) ? 1 : 0);
+  net->prof.mark("obj_prep", st);
+  rc = gn::tc_objects_convs(net, cover, batch, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaGetLastError());
+  return GLASSNET_OK;
+}
+
+extern "C" int glassnet_objects_finish(glassnet_t net, const void* gbuf, const void* direct, float* out, int32_t batch,
+                                       glassnet_stream_t stream) {
+  int rc = objects_check(net, batch);
+  if (rc) return rc;
+  if ((rc = check_ptr(gbuf, "gbuf")) || (rc = check_ptr(direct, "direct")) || (rc = check_ptr(out, "out"))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (net->d.precision == GLASSNET_FP32)
+    return forward_simt<float>(net, (const float*)gbuf, (const float*)direct, nullptr, nullptr, out, batch, st);
+  if (net->tc) return forward_tc(net, gbuf, direct, nullptr, nullptr, out, batch, st);
+  return forward_simt<__nv_bfloat16>(net, (const __nv_bfloat16*)gbuf, (const __nv_bfloat16*)direct, nullptr, nullptr,
+                                     out, batch, st);
 }
 
 // ------------------------------------------------------------------------ N3 super-sampler

@@ -82,6 +82,13 @@ struct ConvArgs {
   // N3 super-sampler S (GB = 2 / EPI = 2, full frame): the low-res image [B][Ho/2][Wo/2][3] fp32
   const float* img;      // GB = 2: channels 12..14 of the halo = bf16(img at the covering coarse pixel)
   float b3[3];           // EPI = 2: out = clamp(img(coarse) + S3.W s2 + b3, 0, 1) -> zout
+  // N4 object-major T (EPI = 3): a2 = ReLU(acc + b2) of one object, added where it covers the
+  // pixel into the exact fixed-point latent tau_q += round(min(a2, qsat) * qscale) (uint32; integer
+  // adds commute, so the object order cannot change a bit) and the count tau_n += 1
+  const uint8_t* cover;  // [B][Ho][Wo]
+  uint32_t* tau_q;       // [B][Ho][Wo][Cout]
+  uint32_t* tau_n;       // [B][Ho][Wo]
+  float qscale, qsat;
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
@@ -139,7 +146,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
   }
   for (int i = tid; i < NS; i += blockDim.x) sBias[i] = a.bias[split * NS + i];
-  if (EPI >= 1)   // the z projection's weights (EPI 1, 2 run unsplit: NS = Cout)
+  if (EPI == 1 || EPI == 2)   // the z projection's weights (EPI 1, 2 run unsplit: NS = Cout)
     for (int i = tid; i < 3 * NS; i += blockDim.x) sBias[NS + i] = a.wz[i];
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) { tc::mbar_init(full + i, GB ? GB_PRODUCERS : 1); tc::mbar_init(empty + i, 1); }
@@ -316,6 +323,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           __syncwarp();
         }
         float z0 = 0.f, z1 = 0.f, z2 = 0.f;
+        const bool cov = EPI == 3 && valid && __ldg(a.cover + opix) != 0;
 #pragma unroll 1
         for (int c = 0; c < NS / 16; ++c) {
           uint32_t v[16];
@@ -340,6 +348,19 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
               dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
             }
+          } else if (EPI == 3) {
+            if (cov) {   // this thread's pixel, 16 channels: read-modify-write (one writer per pixel)
+              uint4* tq = reinterpret_cast<uint4*>(a.tau_q + opix * a.Cout + co0 + c * 16);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 u = tq[j];
+                u.x += __float2uint_rn(fminf(y[4 * j], a.qsat) * a.qscale);
+                u.y += __float2uint_rn(fminf(y[4 * j + 1], a.qsat) * a.qscale);
+                u.z += __float2uint_rn(fminf(y[4 * j + 2], a.qsat) * a.qscale);
+                u.w += __float2uint_rn(fminf(y[4 * j + 3], a.qsat) * a.qscale);
+                tq[j] = u;
+              }
+            }
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -353,6 +374,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (EPI == 1 && valid) {
           a.zout[opix * 3 + 0] = z0; a.zout[opix * 3 + 1] = z1; a.zout[opix * 3 + 2] = z2;
         }
+        if (EPI == 3 && cov && split == 0) a.tau_n[opix] += 1u;
         if (EPI == 2 && valid) {   // N3: residual onto the nearest-upsampled image, clamped
           const long pc = ((long)b * (a.out_rows_buf >> 1) + ((oy + a.out_row_off) >> 1)) * (a.Wo >> 1) + (px >> 1);
           const float* im = a.img + pc * 3;

@@ -142,6 +142,96 @@ __global__ void k_ss_out(const float* __restrict__ img, const float* __restrict_
   for (int c = 0; c < 3; ++c) out[p * 3 + c] = fminf(fmaxf(img[pc * 3 + c] + (r[p * 3 + c] + bb[c]), 0.f), 1.f);
 }
 
+// N4 object-major T (reading N4), SIMT side.  x = cover ? [b (depth x 2^-7 with R9), 0 x 5]
+// : 0 (16 channels, T) -- the conv input of h's first 3x3 layer.  One thread per pixel.
+template <typename T>
+__global__ void k_obj_prep(const T* __restrict__ obj, const uint8_t* __restrict__ cover, T* __restrict__ x, long P,
+                           int norm) {
+  const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  float v[16];
+  const bool c = cover[p] != 0;
+#pragma unroll
+  for (int i = 0; i < 11; ++i) v[i] = c ? to_f(obj[p * 11 + i]) : 0.f;   // select: garbage never read into math
+#pragma unroll
+  for (int i = 11; i < 16; ++i) v[i] = 0.f;
+  if (norm) v[7] *= 0.0078125f;
+  store8(x + p * 16, v);
+  store8(x + p * 16 + 8, v + 8);
+}
+
+// N4, SIMT family: tau_q += round(min(a2, qsat) qscale) and tau_n += 1 where the object covers
+// (a2 from k_conv3x3_simt; the same exact fixed-point sum as the tensor-core epilogue).
+template <typename T>
+__global__ void k_obj_accum(const T* __restrict__ a2, const uint8_t* __restrict__ cover, uint32_t* __restrict__ tau_q,
+                            uint32_t* __restrict__ tau_n, long P, int H, float qscale, float qsat) {
+  const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P || cover[p] == 0) return;
+  for (int j = 0; j < H; j += 8) {
+    float v[8];
+    load8(a2 + p * H + j, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tau_q[p * H + j + i] += __float2uint_rn(fminf(v[i], qsat) * qscale);
+  }
+  tau_n[p] += 1u;
+}
+
+// N4: B + psi from the accumulated latent (both families): tau = tau_q / qscale (mean: / n),
+// phi = ReLU(W_B [e0; tau; n] + b_B), psi = W_O[:, :c0] phi + W_O[:, c0:] L_d + b_O (R15).
+// wb: WB[C0][C0+H+1] bB[C0] WO[3][NO] bO[3] (fp32).
+template <typename T, int H, int C0>
+__global__ void __launch_bounds__(128) k_b_psi(const T* __restrict__ e0, const uint32_t* __restrict__ tau_q,
+                                               const uint32_t* __restrict__ tau_n, const T* __restrict__ direct,
+                                               const float* __restrict__ wb, float* __restrict__ psi, long P, int pool,
+                                               int r_takes_ld, float inv_qscale) {
+  const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0);
+  __shared__ __align__(16) float sw[C0 * (C0 + H + 1) + C0 + 3 * (C0 + 3) + 3];   // the B / output weights
+  const int nw = C0 * NB + C0 + 3 * NO + 3;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) sw[i] = wb[i];
+  __syncthreads();
+  const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float* WB = sw;
+  const float* bB = WB + C0 * NB;
+  const float* WO = bB + C0;
+  const float* bO = WO + 3 * NO;
+  const float m = (float)tau_n[p];
+  float s[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    s[j] = (float)tau_q[p * H + j] * inv_qscale;
+    if (pool == 1) s[j] = m > 0.f ? __fdiv_rn(s[j], m) : 0.f;
+  }
+  float ev[C0];
+#pragma unroll
+  for (int i = 0; i < C0; i += 8) load8(e0 + p * C0 + i, ev + i);
+  float ps0 = bO[0], ps1 = bO[1], ps2 = bO[2];
+  if (r_takes_ld) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float l = to_f(direct[p * 3 + i]);
+      ps0 = fmaf(WO[0 * NO + C0 + i], l, ps0);
+      ps1 = fmaf(WO[1 * NO + C0 + i], l, ps1);
+      ps2 = fmaf(WO[2 * NO + C0 + i], l, ps2);
+    }
+  }
+#pragma unroll 2
+  for (int o = 0; o < C0; ++o) {
+    const float* w = WB + o * NB;
+    float a = bB[o];
+#pragma unroll
+    for (int i = 0; i < C0; ++i) a = fmaf(w[i], ev[i], a);
+#pragma unroll
+    for (int j = 0; j < H; ++j) a = fmaf(w[C0 + j], s[j], a);
+    a = fmaf(w[C0 + H], m, a);
+    const float phi = relu(a);
+    ps0 = fmaf(WO[0 * NO + o], phi, ps0);
+    ps1 = fmaf(WO[1 * NO + o], phi, ps1);
+    ps2 = fmaf(WO[2 * NO + o], phi, ps2);
+  }
+  psi[p * 3 + 0] = ps0; psi[p * 3 + 1] = ps1; psi[p * 3 + 2] = ps2;
+}
+
 // conv3x3 (cross-correlation, zero pad 1), NHWC.  w: [9][Cin][Cout] fp32.  One thread =
 // one output pixel x NJ output channels.  EPI 0: bias + ReLU -> T.  EPI 1 (R_1 only):
 // bias + ReLU -> z = Wz y (3 fp32), the projection of reading R15.

@@ -64,6 +64,8 @@ struct TcState {
   Geom* tile = nullptr;         // row-tile geometry (forward_sharded)
   TcConv ssconv[2];             // N3 super-sampler: S1 (GB = 2), S2 (EPI = 2)
   ConvGeom ssg[2];
+  TcConv objconv[2];            // N4 object-major h: T1 (16 -> h), T2 (h -> h, EPI = 3 accumulate)
+  ConvGeom objg[2];
   int* sched = nullptr;         // T kernel's dynamic tile counter
   uint32_t* perm = nullptr;     // T kernel's count-sorted pixel order (k_tb_sort), one entry per pixel
   long perm_cap = 0;
@@ -430,7 +432,7 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
 template <int S, int NS, int EPI, int WS, int OST, int RR, int GB = 0>
 static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
                           const void* gbuf = nullptr, const void* direct = nullptr, const float* img = nullptr,
-                          const float* b3 = nullptr) {
+                          const float* b3 = nullptr, const uint8_t* cover = nullptr) {
   auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST, RR, GB>;
   static int smem_set = -1;   // the attribute is set once per instantiation and size (not per launch)
   if (smem_set < (int)L.smem) {
@@ -441,6 +443,7 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
   a.wimg = L.wimg; a.bias = L.bias; a.out = G.out; a.wz = L.wz ? L.wz : net->wz; a.zout = G.zout;
   a.img = img;
   for (int i = 0; i < 3; ++i) a.b3[i] = b3 ? b3[i] : 0.f;
+  a.cover = cover; a.tau_q = net->tau_q; a.tau_n = net->tau_n; a.qscale = net->qscale; a.qsat = net->qsat;
   a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
   a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
   a.in_rows_buf = G.Hi_buf;
@@ -454,7 +457,17 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
                        const void* gbuf = nullptr, const void* direct = nullptr, const float* img = nullptr,
-                       const float* b3 = nullptr) {
+                       const float* b3 = nullptr, const uint8_t* cover = nullptr) {
+  if (L.epi == 3) {   // N4: h's second conv, accumulated into the fixed-point latent where covered
+#define CONV_E3(NS_, RR_)                                                                                \
+    if (L.S == 1 && L.NS == NS_ && L.ws == 0 && L.ost == 0 && L.rr == RR_) {                            \
+      launch_conv_k<1, NS_, 3, 0, 0, RR_>(net, L, G, B, st, nullptr, nullptr, nullptr, nullptr, cover); \
+      return 0;                                                                                         \
+    }
+    CONV_E3(32, 1) CONV_E3(32, 2) CONV_E3(32, 4) CONV_E3(64, 1) CONV_E3(64, 2) CONV_E3(64, 4)
+#undef CONV_E3
+    return gn_fail(GLASSNET_ERR_UNSUPPORTED, "object conv: NS=%d rr=%d", L.NS, L.rr);
+  }
   if (gbuf && img) {   // N3 S1: the hi-res G-buffer + the nearest-upsampled image
 #define CONV_GB2(NS_, OST_, RR_)                                                                         \
     if (L.S == 1 && L.NS == NS_ && L.epi == 0 && L.ws == 0 && L.ost == OST_ && L.rr == RR_) {           \
@@ -515,6 +528,36 @@ inline int tc_supersample(glassnet* net, const float* img, const void* gbuf_hi, 
   g.zout = out_hi;
   rc = launch_conv(net, s->ssconv[1], g, B, st, nullptr, nullptr, img, net->ss_b3);
   net->prof.mark("ss_S2", st);
+  return rc;
+}
+
+// N4 object-major h on the tensor cores: T1 = k_conv_tc over the 16-channel object input (x built
+// by k_obj_prep), T2 = k_conv_tc EPI = 3 whose epilogue adds ReLU(acc + b2) into the exact
+// fixed-point latent tau_q where the object covers (a2 never reaches HBM).
+inline int tc_setup_objects(glassnet* net, const float* T1W, const float* T2W) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  const glassnet_dims& d = net->d;
+  const int h = d.t_hidden;
+  int rc = setup_conv(net, s->objconv[0], 1, T1W, net->objB[0], 11, 16, h, 0);
+  if (!rc) rc = setup_conv(net, s->objconv[1], 1, T2W, net->objB[1], h, h, h, 3);
+  for (int i = 0; i < 2 && !rc; ++i) {
+    ConvGeom& g = s->objg[i];
+    g.Hi_buf = d.height; g.Wi = d.width; g.Ho = d.height; g.Wo = d.width;
+    g.in_row_off = 0; g.out_row_off = 0; g.out_rows_buf = d.height;
+    g.out = i == 0 ? reinterpret_cast<uint16_t*>(net->obj_h1) : nullptr;
+    g.zout = nullptr;
+    rc = make_halo_maps(1, g, i == 0 ? net->obj_x : net->obj_h1, d.max_batch, i == 0 ? 16 : h, s->objconv[i].rr);
+  }
+  return rc;
+}
+
+inline int tc_objects_convs(glassnet* net, const uint8_t* cover, int B, cudaStream_t st) {
+  TcState* s = reinterpret_cast<TcState*>(net->tc_state);
+  int rc = launch_conv(net, s->objconv[0], s->objg[0], B, st);
+  net->prof.mark("obj_h1", st);
+  if (rc) return rc;
+  rc = launch_conv(net, s->objconv[1], s->objg[1], B, st, nullptr, nullptr, nullptr, nullptr, cover);
+  net->prof.mark("obj_h2_accum", st);
   return rc;
 }
 

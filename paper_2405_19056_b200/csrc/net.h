@@ -83,6 +83,16 @@ struct glassnet {
   void* ss_s1 = nullptr;    // [B][2H][2W][c0]
   void* ss_x = nullptr;     // [B][2H][2W][16]  (SIMT family)
   float* ss_r = nullptr;    // [B][2H][2W][3]   (SIMT family)
+  // N4 object-major T (GLASSNET_FLAG_OBJECTS)
+  float* objW[2] = {};      // SIMT conv packs of T1 (16 -> h), T2 (h -> h), [tap][ci][co]
+  float* objB[2] = {};
+  void* obj_x = nullptr;    // [B][H][W][16]   an object's conv input
+  void* obj_h1 = nullptr;   // [B][H][W][h]    its first layer
+  void* obj_a2 = nullptr;   // [B][H][W][h]    its second layer (SIMT family only)
+  uint32_t* tau_q = nullptr;   // [B][H][W][h] fixed-point latent
+  uint32_t* tau_n = nullptr;   // [B][H][W]    covering objects
+  size_t wb_off = 0;        // offset of W_B in w_tb
+  float qscale = 4096.f, qsat = 2048.f;
   size_t ws_bytes = 0, w_bytes = 0;
   // staging for glassnet_forward_host
   void *st_g = nullptr, *st_d = nullptr, *st_t = nullptr, *st_n = nullptr;

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("GN_LIB", os.path.join(_HERE, "libglassnet.so"))   # G
 GLASSNET_ABI_VERSION = 1
 BF16, FP32 = 0, 1
 POOL_SUM, POOL_MEAN = 0, 1
-FLAG_R_TAKES_LD, FLAG_INPUT_NORM, FLAG_SIGMA_COND, FLAG_SUPERSAMPLE = 1, 2, 4, 8
+FLAG_R_TAKES_LD, FLAG_INPUT_NORM, FLAG_SIGMA_COND, FLAG_SUPERSAMPLE, FLAG_OBJECTS = 1, 2, 4, 8, 16
 ERRORS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CUDA", 4: "NCCL", 5: "OUT_OF_MEMORY"}
 
 EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glassnet_forward_host",
@@ -25,7 +25,8 @@ EXPORTS = ["glassnet_weight_count", "glassnet_create", "glassnet_forward", "glas
            "glassnet_set_kernel_family", "glassnet_get_unique_id", "glassnet_comm_create",
            "glassnet_comm_destroy", "glassnet_tile_rows", "glassnet_forward_sharded",
            "glassnet_destroy", "glassnet_last_error", "glassnet_profile_begin", "glassnet_profile_end",
-           "glassnet_forward_sharded_local", "glassnet_debug_psi", "glassnet_supersample"]
+           "glassnet_forward_sharded_local", "glassnet_debug_psi", "glassnet_supersample",
+           "glassnet_objects_begin", "glassnet_objects_add", "glassnet_objects_finish"]
 
 
 class GlassNetError(RuntimeError):
@@ -83,6 +84,12 @@ def lib():
         L.glassnet_profile_end.argtypes = [vp, i32, vp, vp, vp, vp]
         L.glassnet_forward_sharded_local.restype = ctypes.c_int
         L.glassnet_forward_sharded_local.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+        L.glassnet_objects_begin.restype = ctypes.c_int
+        L.glassnet_objects_begin.argtypes = [vp, i32, vp]
+        L.glassnet_objects_add.restype = ctypes.c_int
+        L.glassnet_objects_add.argtypes = [vp, vp, vp, i32, vp]
+        L.glassnet_objects_finish.restype = ctypes.c_int
+        L.glassnet_objects_finish.argtypes = [vp, vp, vp, vp, i32, vp]
         L.glassnet_supersample.restype = ctypes.c_int
         L.glassnet_supersample.argtypes = [vp, vp, vp, vp, i32, vp]
         L.glassnet_debug_psi.restype = ctypes.c_int
@@ -101,12 +108,13 @@ def _check(rc):
 
 
 def make_dims(height, width, k_slots, widths, t_hidden, levels=None, precision="bf16", max_batch=1,
-              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False, supersample=False, pe_L=0) -> Dims:
+              pool="sum", r_takes_ld=True, input_norm=True, sigma_cond=False, supersample=False, pe_L=0,
+              objects=False) -> Dims:
     levels = len(widths) if levels is None else levels
     w = (ctypes.c_int32 * 4)(*(list(widths)[:levels] + [0] * (4 - levels)))
     flags = ((FLAG_R_TAKES_LD if r_takes_ld else 0) | (FLAG_INPUT_NORM if input_norm else 0)
              | (FLAG_SIGMA_COND if sigma_cond else 0) | (FLAG_SUPERSAMPLE if supersample else 0)
-             | (int(pe_L) << 8))   # N2: GLASSNET_FLAG_POSENC(L)
+             | (FLAG_OBJECTS if objects else 0) | (int(pe_L) << 8))   # N2: GLASSNET_FLAG_POSENC(L)
     return Dims(GLASSNET_ABI_VERSION, height, width, max_batch, k_slots, levels, w, t_hidden,
                 BF16 if precision == "bf16" else FP32, POOL_MEAN if pool == "mean" else POOL_SUM, flags)
 
@@ -181,6 +189,30 @@ class GlassNet:
     def forward_sharded(self, comm, gbuf, direct, tbuf, tcount, out, stream=None):
         _check(lib().glassnet_forward_sharded(self._h, comm._h, _ptr(gbuf), _ptr(direct), _ptr(tbuf),
                                               _ptr(tcount), _ptr(out), _stream(stream)))
+        return out
+
+    # -- N4 object-major T (include/glassnet.h glassnet_objects_*) -------------------------
+    def objects_begin(self, batch, stream=None):
+        _check(lib().glassnet_objects_begin(self._h, batch, _stream(stream)))
+
+    def objects_add(self, obj, cover, stream=None):
+        """obj [B][H][W][11] (dims precision), cover [B][H][W] uint8, both on the device."""
+        import torch
+        d = self.dims
+        B = obj.shape[0]
+        dt = torch.bfloat16 if d.precision == BF16 else torch.float32
+        if tuple(obj.shape) != (B, d.height, d.width, 11) or obj.dtype != dt or not obj.is_contiguous():
+            raise ValueError(f"obj: want {(B, d.height, d.width, 11)} {dt}, got {tuple(obj.shape)} {obj.dtype}")
+        if tuple(cover.shape) != (B, d.height, d.width) or cover.dtype != torch.uint8 or not cover.is_contiguous():
+            raise ValueError(f"cover: want {(B, d.height, d.width)} uint8, got {tuple(cover.shape)} {cover.dtype}")
+        _check(lib().glassnet_objects_add(self._h, _ptr(obj), _ptr(cover), B, _stream(stream)))
+
+    def objects_finish(self, gbuf, direct, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(gbuf.shape[:3] + (3,), dtype=torch.float32, device=gbuf.device)
+        _check(lib().glassnet_objects_finish(self._h, _ptr(gbuf), _ptr(direct), _ptr(out), gbuf.shape[0],
+                                             _stream(stream)))
         return out
 
     def supersample(self, img, gbuf_hi, out=None, stream=None):
