@@ -324,10 +324,22 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         float z0 = 0.f, z1 = 0.f, z2 = 0.f;
         const bool cov = EPI == 3 && valid && __ldg(a.cover + opix) != 0;
+        uint4 tcur[4], tnext[4];   // EPI 3: this and the next chunk's latent (loads one chunk ahead)
+        uint4* tq0 = EPI == 3 ? reinterpret_cast<uint4*>(a.tau_q + opix * a.Cout + co0) : nullptr;
+        if (EPI == 3 && cov)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tnext[j] = tq0[j];
 #pragma unroll 1
         for (int c = 0; c < NS / 16; ++c) {
           uint32_t v[16];
           tc::tmem_ld16(taddr + c * 16, v);
+          if (EPI == 3 && cov) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tcur[j] = tnext[j];
+            if (c + 1 < NS / 16)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) tnext[j] = tq0[4 * (c + 1) + j];
+          }
           tc::tmem_ld_wait();
           float y[16];
 #pragma unroll
@@ -350,10 +362,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
           } else if (EPI == 3) {
             if (cov) {   // this thread's pixel, 16 channels: read-modify-write (one writer per pixel)
-              uint4* tq = reinterpret_cast<uint4*>(a.tau_q + opix * a.Cout + co0 + c * 16);
+              uint4* tq = tq0 + 4 * c;
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                uint4 u = tq[j];
+                uint4 u = tcur[j];
                 u.x += __float2uint_rn(fminf(y[4 * j], a.qsat) * a.qscale);
                 u.y += __float2uint_rn(fminf(y[4 * j + 1], a.qsat) * a.qscale);
                 u.z += __float2uint_rn(fminf(y[4 * j + 2], a.qsat) * a.qscale);

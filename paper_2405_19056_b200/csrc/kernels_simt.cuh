@@ -185,14 +185,15 @@ __global__ void __launch_bounds__(128) k_b_psi(const T* __restrict__ e0, const u
                                                const float* __restrict__ wb, float* __restrict__ psi, long P, int pool,
                                                int r_takes_ld, float inv_qscale) {
   const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0);
-  __shared__ __align__(16) float sw[C0 * (C0 + H + 1) + C0 + 3 * (C0 + 3) + 3];   // the B / output weights
-  const int nw = C0 * NB + C0 + 3 * NO + 3;
-  for (int i = threadIdx.x; i < nw; i += blockDim.x) sw[i] = wb[i];
+  constexpr int NBP = (C0 + H + 1 + 3) / 4 * 4;   // W_B rows padded to 16 bytes: vector weight loads
+  __shared__ __align__(16) float sWB[C0 * NBP];
+  __shared__ float sRest[C0 + 3 * (C0 + 3) + 3];   // b_B, W_O, b_O
+  for (int i = threadIdx.x; i < C0 * NB; i += blockDim.x) sWB[(i / NB) * NBP + i % NB] = wb[i];
+  for (int i = threadIdx.x; i < C0 + 3 * NO + 3; i += blockDim.x) sRest[i] = wb[C0 * NB + i];
   __syncthreads();
   const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
-  const float* WB = sw;
-  const float* bB = WB + C0 * NB;
+  const float* bB = sRest;
   const float* WO = bB + C0;
   const float* bO = WO + 3 * NO;
   const float m = (float)tau_n[p];
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(128) k_b_psi(const T* __restrict__ e0, const u
   }
 #pragma unroll 2
   for (int o = 0; o < C0; ++o) {
-    const float* w = WB + o * NB;
+    const float* w = sWB + o * NBP;
     float a = bB[o];
 #pragma unroll
     for (int i = 0; i < C0; ++i) a = fmaf(w[i], ev[i], a);
