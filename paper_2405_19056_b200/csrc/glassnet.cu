@@ -341,10 +341,9 @@ static void launch_tb_simt(glassnet* net, const T* tbuf, const uint8_t* tcount, 
   const unsigned g = nblk(P0, 128);
 #define TB_LAUNCH(HH, CC)                                                                                      \
   {                                                                                                            \
-    auto kfn = gn::k_tb_simt<T, HH, CC>;                                                                       \
+    auto kfn = sig ? gn::k_tb_simt<T, HH, CC, true> : gn::k_tb_simt<T, HH, CC, false>;                        \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
-    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e0, direct, net->w_tb, psi, P0, K, d.pool, ld, norm, sig ? 1 : 0, \
-                              gn_pe_L(d));                                                                     \
+    kfn<<<g, 128, smem, st>>>(tbuf, tcount, e0, direct, net->w_tb, psi, P0, K, d.pool, ld, norm, gn_pe_L(d)); \
   }
   if (h == 64 && c[0] == 32) TB_LAUNCH(64, 32)
   else if (h == 64 && c[0] == 16) TB_LAUNCH(64, 16)

@@ -320,11 +320,14 @@ __device__ __forceinline__ bool rec_less(const T* a, const T* b) {
 // wts (fp32): W1[H][NIN] b1[H] W2[H][H] b2[H] WB[C0][C0+H+1] bB[C0] WO[3][NO] bO[3],
 // NIN = NR (+ C0 with sigma, N1: h's layer 1 over [record ; e0 at the pixel]); NR = 11, or
 // 11 (2 pe_L + 1) with N2's positional encoding of the record (computed here, per fragment)
-template <typename T, int H, int C0>
+// SIG (N1) is a template parameter so that without it neither the shared layer-1 part u1 nor e0 is
+// live across the fragment loop (register pressure; e0 is loaded for B after the loop).
+template <typename T, int H, int C0, bool SIG>
 __global__ void __launch_bounds__(128) k_tb_simt(
     const T* __restrict__ tbuf, const uint8_t* __restrict__ tcount, const T* __restrict__ e0,
     const T* __restrict__ direct, const float* __restrict__ wts, float* __restrict__ psi,
-    long P, int K, int pool, int r_takes_ld, int norm, int sigma, int pe_L) {
+    long P, int K, int pool, int r_takes_ld, int norm, int pe_L) {
+  constexpr bool sigma = SIG;
   extern __shared__ float sw[];
   const int PE = 2 * pe_L + 1, NR = 11 * PE;
   const int NB = C0 + H + 1, NO = C0 + (r_takes_ld ? 3 : 0), NIN = NR + (sigma ? C0 : 0);
@@ -358,18 +361,19 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     idx[j] = k;
   }
   float ev[C0];
+  if (SIG)
 #pragma unroll
-  for (int i = 0; i < C0; i += 8) load8(e0 + p * C0 + i, ev + i);
+    for (int i = 0; i < C0; i += 8) load8(e0 + p * C0 + i, ev + i);
   // the layer-1 part every fragment of the pixel shares: b1 (+ W1,sigma e0 with N1)
   float u1[H];
+  if (SIG)
 #pragma unroll
-  for (int o = 0; o < H; ++o) {
-    float a = b1[o];
-    if (sigma)
+    for (int o = 0; o < H; ++o) {
+      float a = b1[o];
 #pragma unroll
       for (int j = 0; j < C0; ++j) a = fmaf(W1[o * NIN + NR + j], ev[j], a);
-    u1[o] = a;
-  }
+      u1[o] = a;
+    }
   float s[H];
 #pragma unroll
   for (int o = 0; o < H; ++o) s[o] = 0.f;
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     if (pe_L == 0) {
 #pragma unroll
       for (int o = 0; o < H; ++o) {
-        float a = u1[o];
+        float a = SIG ? u1[o] : b1[o];
 #pragma unroll
         for (int i = 0; i < 11; ++i) a = fmaf(W1[o * NIN + i], x[i], a);
         a1[o] = relu(a);
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(128) k_tb_simt(
     } else {   // N2: layer 1 over gamma(record), channel by channel (features in index order)
       const float* w1t = sw + ((nw + 3) & ~3);   // [NIN][H]
 #pragma unroll
-      for (int o = 0; o < H; ++o) a1[o] = u1[o];
+      for (int o = 0; o < H; ++o) a1[o] = SIG ? u1[o] : b1[o];
 #pragma unroll 1
       for (int i = 0; i < 11; ++i) {
         const float v = x[i];
@@ -434,6 +438,9 @@ __global__ void __launch_bounds__(128) k_tb_simt(
 #pragma unroll
     for (int o = 0; o < H; ++o) s[o] = __fdiv_rn(s[o], (float)m);
   }
+  if (!SIG)   // B's e0 input, loaded only now (not live across the fragment loop)
+#pragma unroll
+    for (int i = 0; i < C0; i += 8) load8(e0 + p * C0 + i, ev + i);
   float ld[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) ld[i] = to_f(direct[p * 3 + i]);

@@ -127,3 +127,48 @@ def test_objects_handle_refuses_pixel_major_forward(cuda_ok):
     with pytest.raises(gb.GlassNetError, match="OBJECTS"):
         net.forward(g, d, t, n)
     net.close()
+
+
+def test_objects_rerun_bitwise_and_guard_bands(cuda_ok):
+    """Hazard check: 20 begin/add/finish sequences give the same bits (the latent's read-modify-
+    write has one writer per pixel and launch), and the output's NaN guard bands stay untouched."""
+    import torch
+    K = 8
+    cfg, w, net, fr = _setup(24, 136, 2, K, "bf16", C1NET, seed=9)
+    g, d, t, n = to_torch(fr)
+    objs = [t[:, :, :, k, :].contiguous() for k in range(K)]
+    covs = [(n > k).to(torch.uint8).contiguous() for k in range(K)]
+    N = 2 * 24 * 136 * 3
+    G = 4096
+    buf = torch.full((N + 2 * G,), float("nan"), device="cuda")
+    out = buf[G:G + N].view(2, 24, 136, 3)
+
+    def run():
+        net.objects_begin(2)
+        for k in range(K):
+            net.objects_add(objs[k], covs[k])
+        net.objects_finish(g, d, out)
+        torch.cuda.synchronize()
+        return out.cpu().numpy().copy()
+    first = run()
+    assert torch.isnan(buf[:G]).all() and torch.isnan(buf[G + N:]).all() and not np.isnan(first).any()
+    for _ in range(20):
+        assert np.array_equal(first.view(np.uint32), run().view(np.uint32))
+    net.close()
+
+
+@pytest.mark.parametrize("family", ["tc", "simt"])
+def test_objects_empty_set(cuda_ok, family):
+    """No object added (the empty set of Eq. eq:SymmetricNN): tau = 0 and n = 0 everywhere, as the
+    oracle's t = 0 forward."""
+    cfg, w, net, fr = _setup(16, 136, 1, 4, "bf16", C1NET, seed=10)
+    net.set_kernel_family(family == "tc")
+    g, d, t, n = to_torch(fr)
+    net.objects_begin(1)
+    out = net.objects_finish(g, d).cpu().numpy()
+    g64, d64, _, _ = fr.as64()
+    dims = oracle.make_dims(16, 136, 4, C1NET["widths"], C1NET["t_hidden"], 4, objects=True)
+    ref = oracle.forward_objects(dims, w.astype(np.float64), g64[0], d64[0], [], [])
+    mx, mn = errs(out[0], ref)
+    assert mx <= BF16_TOL[0] and mn <= BF16_TOL[1]
+    net.close()

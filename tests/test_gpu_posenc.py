@@ -36,7 +36,8 @@ def _run(cfg, fr, family=None):
 
 
 @pytest.mark.parametrize("family", ["tc", "simt"])
-@pytest.mark.parametrize("H,W,K,pe_L,sigma", [(48, 136, 8, 6, False), (32, 64, 5, 3, False), (16, 264, 8, 6, True)])
+@pytest.mark.parametrize("H,W,K,pe_L,sigma", [(48, 136, 8, 6, False), (32, 64, 5, 3, False), (16, 264, 8, 6, True),
+                                              (16, 136, 4, 1, False), (16, 136, 4, 10, False)])
 def test_pe_bf16_parity(cuda_ok, family, H, W, K, pe_L, sigma):
     cfg = _cfg(H, W, 1, K, "bf16", C1NET, pe_L, sigma)
     fr = synth.gen_frames(cfg, seed=3)
@@ -47,8 +48,9 @@ def test_pe_bf16_parity(cuda_ok, family, H, W, K, pe_L, sigma):
     net.close()
 
 
-def test_pe_fp32_check_mode(cuda_ok):
-    cfg = _cfg(32, 48, 1, 4, "fp32", C0NET, 6)
+@pytest.mark.parametrize("pe_L", [6, 10])
+def test_pe_fp32_check_mode(cuda_ok, pe_L):
+    cfg = _cfg(32, 48, 1, 4, "fp32", C0NET, pe_L)
     fr = synth.gen_frames(cfg, seed=4)
     out, net = _run(cfg, fr)
     mx, _ = errs(out[0], oracle_full(cfg, weights_for(cfg), fr))

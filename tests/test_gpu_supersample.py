@@ -144,3 +144,27 @@ def test_forward_then_supersample(cuda_ok):
     mx, mn = errs(out[0], ref)
     assert mx <= BF16_TOL[0] and mn <= BF16_TOL[1]
     net.close()
+
+
+def test_ss_output_guard_bands_and_rerun_bitwise(cuda_ok):
+    """Hazard check (compute-sanitizer is closed on this pool, profiles/r2_hazard_checks.md): S's
+    epilogue writes exactly out_hi -- NaN guard bands before and after it stay untouched on a
+    ragged frame (hi-res width 272 = 2 x 128 + 16) -- and 20 reruns give the same bits."""
+    import torch
+    H, W, B = 24, 136, 2
+    net, _ = _net(H, W, B, "bf16", C1NET)
+    img, img_t, g_t, _ = _inputs(H, W, B, "bf16")
+    n = B * 2 * H * 2 * W * 3
+    G = 4096
+    buf = torch.full((n + 2 * G,), float("nan"), device="cuda")
+    out = buf[G:G + n].view(B, 2 * H, 2 * W, 3)
+    net.supersample(img_t, g_t, out)
+    torch.cuda.synchronize()
+    first = out.cpu().numpy().copy()
+    assert torch.isnan(buf[:G]).all() and torch.isnan(buf[G + n:]).all()
+    assert not np.isnan(first).any()
+    for _ in range(20):
+        net.supersample(img_t, g_t, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(first.view(np.uint32), out.cpu().numpy().view(np.uint32))
+    net.close()
