@@ -411,6 +411,8 @@ def run_ours(args):
     # per-stage times (events after every launch, same stream; a second pass of K steps)
     # (a row tile also builds x16 for its halo exchange: one more launch than the full frame)
     launches = net.launches_per_forward(B) + (1 if tiles_mode and args.family == "tc" else 0)
+    if tiles_mode and args.family == "tc" and world > 1:   # boundary rows first: each exchanged conv / up2 runs as two launches
+        launches += 4 if cfg.levels >= 3 else 3 * cfg.levels - 3   # the splits at levels 0 and 1 (default policy)
     net.profile_begin((launches + 3) * args.steps + 2)   # + start marks (a row tile restarts around T's stream)
     for _ in range(args.steps):
         run()

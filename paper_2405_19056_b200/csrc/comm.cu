@@ -11,6 +11,8 @@
 struct glassnet_comm {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  cudaStream_t cs = nullptr;                  // halo exchanges run here, beside the interior rows
+  cudaEvent_t ev_b = nullptr, ev_x = nullptr;  // boundary rows written / exchange done
 };
 
 extern "C" int glassnet_get_unique_id(uint8_t id[128]) {
@@ -37,6 +39,12 @@ extern "C" int glassnet_comm_create(const uint8_t id[128], int32_t nranks, int32
   }
   c->nranks = nranks;
   c->rank = rank;
+  if (cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming) != cudaSuccess) {
+    glassnet_comm_destroy(c);
+    return gn_fail(GLASSNET_ERR_CUDA, "comm stream / events");
+  }
   *out = c;
   return GLASSNET_OK;
 }
@@ -44,23 +52,49 @@ extern "C" int glassnet_comm_create(const uint8_t id[128], int32_t nranks, int32
 extern "C" void glassnet_comm_destroy(glassnet_comm_t c) {
   if (!c) return;
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->ev_x) cudaEventDestroy(c->ev_x);
   delete c;
 }
 
 // Row-tile forward: the tensor-core step list with halo rows exchanged at EXCH steps.
 // Rank r sends its first interior row up (to r-1) and its last interior row down (to
 // r+1) and receives the neighbours' rows into its halo rows; frame-edge halos stay zero.
-static int run_tile_steps(glassnet_t net, int nranks, int rank, const void* gbuf, const void* direct,
-                          const void* tbuf, const uint8_t* tcount, float* out, cudaStream_t st,
+// Boundary rows first (gn::tc_steps, tile order): a producer's first/last rows are computed,
+// the exchange of them runs on the comm stream (after an event on the main stream), and the
+// producer's other rows run on the main stream meanwhile; the next step that reads the
+// exchanged rows (anything but an edge-2 step or T) first waits for the exchange's event.  The
+// exchange writes only the halo rows and reads only the boundary rows, which the edge-2 launch
+// neither reads nor writes.
+static int run_tile_steps(glassnet_t net, glassnet_comm* c, const void* gbuf, const void* direct, const void* tbuf,
+                          const uint8_t* tcount, float* out, cudaStream_t st,
                           int (*exch)(void*, glassnet_t, int, cudaStream_t), void* ctx) {
-  gn::Step steps[64];
-  const int n = gn::tc_steps(net, steps, 64, true);
+  gn::Step steps[96];
+  const int n = gn::tc_steps(net, steps, 96, true);
+  if (n > 96) return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tile step list");
   net->prof.mark(nullptr, st);
+  bool pending = false;
   for (int i = 0; i < n; ++i) {
-    int rc = steps[i].kind == gn::ST_EXCH ? exch(ctx, net, steps[i].idx, st)
-                                          : gn::tc_run_step(net, true, steps[i], gbuf, direct, tbuf, tcount, out, 1, st);
+    const gn::Step& sp = steps[i];
+    int rc;
+    if (sp.kind == gn::ST_EXCH) {
+      if (pending && cudaStreamWaitEvent(c->cs, c->ev_x, 0) != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "wait");
+      if (cudaEventRecord(c->ev_b, st) != cudaSuccess || cudaStreamWaitEvent(c->cs, c->ev_b, 0) != cudaSuccess)
+        return gn_fail(GLASSNET_ERR_CUDA, "exchange event");
+      rc = exch(ctx, net, sp.idx, c->cs);
+      if (!rc && cudaEventRecord(c->ev_x, c->cs) != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "exchange event");
+      pending = true;
+    } else {
+      if (pending && sp.edge != 2 && sp.kind != gn::ST_TB) {
+        if (cudaStreamWaitEvent(st, c->ev_x, 0) != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "exchange wait");
+        pending = false;
+      }
+      rc = gn::tc_run_step(net, true, sp, gbuf, direct, tbuf, tcount, out, 1, st);
+    }
     if (rc) return rc;
   }
+  if (pending && cudaStreamWaitEvent(st, c->ev_x, 0) != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "exchange wait");
   return GLASSNET_OK;
 }
 
@@ -105,8 +139,7 @@ extern "C" int glassnet_forward_sharded(glassnet_t net, glassnet_comm_t comm, co
   int row0, rows;
   int rc = check_tile_args(net, comm->nranks, comm->rank, &row0, &rows);
   if (rc) return rc;
-  rc = run_tile_steps(net, comm->nranks, comm->rank, gbuf, direct, tbuf, tcount, out, (cudaStream_t)stream,
-                      nccl_exch, comm);
+  rc = run_tile_steps(net, comm, gbuf, direct, tbuf, tcount, out, (cudaStream_t)stream, nccl_exch, comm);
   if (rc) return rc;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return gn_fail(GLASSNET_ERR_CUDA, "forward_sharded: %s", cudaGetErrorString(e));
@@ -128,8 +161,9 @@ extern "C" int glassnet_forward_sharded_local(glassnet_t* nets, int32_t nranks, 
     if (nets[r]->dev != nets[0]->dev)
       return gn_fail(GLASSNET_ERR_INVALID_ARGUMENT, "forward_sharded_local needs all handles on one device");
   }
-  gn::Step steps[64];
-  const int n = gn::tc_steps(nets[0], steps, 64, true);
+  gn::Step steps[96];
+  const int n = gn::tc_steps(nets[0], steps, 96, true);
+  if (n > 96) return gn_fail(GLASSNET_ERR_UNSUPPORTED, "tile step list");
   for (int r = 0; r < nranks; ++r) nets[r]->prof.mark(nullptr, st);
   for (int i = 0; i < n; ++i) {
     if (steps[i].kind != gn::ST_EXCH) {

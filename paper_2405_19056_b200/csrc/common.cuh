@@ -35,6 +35,7 @@ struct Up2Rows {
   int rows_f, rows_f_buf, grow0_f;   // fine level (skip, d, psi, out)
   int rows_c_buf, grow0_c, Hc_full;  // coarse level (y or z)
   int halo;
+  int yoff = 0, ystep = 1;           // fine row of grid row j = j * ystep + yoff (row tiles: edge rows first)
 };
 
 }  // namespace gn

@@ -446,7 +446,35 @@ namespace gn {
 int tc_steps(const glassnet* net, Step* out, int max, bool tile) {
   const int L = net->d.levels;
   int n = 0;
-  auto push = [&](int kind, int idx) { if (n < max) out[n] = Step{kind, idx}; ++n; };
+  auto push = [&](int kind, int idx, int edge = 0) { if (n < max) out[n] = Step{kind, idx, edge}; ++n; };
+  if (tile) {
+    // Row tile, boundary rows first: every CONV / UP whose output is exchanged runs as
+    // [first/last rows; EXCH of its output (comm stream); the other rows], so the halo transfer
+    // overlaps the interior; T (no halo) runs on its own stream once e0 is complete.
+    // Only producers at the two finest levels are split: their interior runs long enough to cover
+    // an exchange, while at the coarse levels the extra launch costs more than the latency it
+    // hides (tools/tile_times.py: splitting all nine costs 0.65 -> 0.78 ms of rank compute at N = 8).
+    // One rank alone has no neighbour to exchange with: no split.  GN_TILE_SPLIT=0 / 2 (env): none / all.
+    const TcState* ts = reinterpret_cast<const TcState*>(net->tc_state);
+    static const int pol = getenv("GN_TILE_SPLIT") ? atoi(getenv("GN_TILE_SPLIT")) : 1;
+    const bool multi = ts && ts->tile_nranks > 1;
+    auto split = [&](int kind, int idx, int tensor, int out_level) {
+      if (!multi || pol == 0 || (pol == 1 && out_level > 1)) { push(kind, idx); push(ST_EXCH, tensor); return; }
+      push(kind, idx, 1); push(ST_EXCH, tensor); push(kind, idx, 2);
+    };
+    push(ST_PREP, 0);
+    push(ST_EXCH, TEN_X);
+    split(ST_CONV, 0, TEN_E + 0, 0);
+    push(ST_TB, 0);
+    for (int l = 1; l < L; ++l) split(ST_CONV, l, TEN_E + l, l);
+    split(ST_CONV, 4 + L - 1, L - 1 >= 2 ? TEN_Y + L - 1 : TEN_Z, L - 1);
+    for (int l = L - 1; l >= 2; --l) {
+      split(ST_UP, l, TEN_D + l - 1, l - 1);
+      split(ST_CONV, 4 + l - 1, l - 1 >= 2 ? TEN_Y + l - 1 : TEN_Z, l - 1);
+    }
+    push(ST_OUT, 0);
+    return n;
+  }
   push(ST_PREP, 0);
   push(ST_EXCH, TEN_X);
   push(ST_CONV, 0);
@@ -534,8 +562,10 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       return 0;
     }
     case ST_CONV: {
-      int rc = (!tile && sp.idx == 0 && !gn_pe_L(d)) ? launch_conv(net, s->conv[0], G.cg[0], B, st, gbuf, direct)
-                                      : launch_conv(net, s->conv[sp.idx], G.cg[sp.idx], B, st);
+      int rc = (!tile && sp.idx == 0 && !gn_pe_L(d))
+                   ? launch_conv(net, s->conv[0], G.cg[0], B, st, gbuf, direct)
+                   : launch_conv(net, s->conv[sp.idx], G.cg[sp.idx], B, st, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                 sp.edge);
       net->prof.mark(kConvNames[sp.idx], st);
       return rc;
     }
@@ -578,7 +608,12 @@ int tc_run_step(glassnet* net, bool tile, const Step& sp, const void* gbuf, cons
       g.rows_f = G.rows[l - 1]; g.rows_f_buf = G.rows[l - 1] + 2 * h; g.grow0_f = G.grow0[l - 1];
       g.rows_c_buf = G.rows[l] + 2 * h; g.grow0_c = G.grow0[l]; g.Hc_full = G.Hfull[l]; g.halo = h;
       const int cv = c[l - 1] / 8, lcv = __builtin_ctz((unsigned)cv);
-      const dim3 grid((unsigned)(((long)(G.W[l - 1] / 2) * cv + 255) / 256), (unsigned)G.rows[l - 1], (unsigned)B);
+      const int rf = G.rows[l - 1];
+      int ny = rf;   // edge 1: rows 0 and rf-1; edge 2: rows 1..rf-2
+      if (sp.edge == 1) { ny = rf < 2 ? rf : 2; g.yoff = 0; g.ystep = rf > 1 ? rf - 1 : 1; }
+      if (sp.edge == 2) { ny = rf > 2 ? rf - 2 : 0; g.yoff = 1; g.ystep = 1; }
+      if (ny == 0) return 0;
+      const dim3 grid((unsigned)(((long)(G.W[l - 1] / 2) * cv + 255) / 256), (unsigned)ny, (unsigned)B);
       ew::k_up2add<<<grid, 256, 0, st>>>((const bf*)G.y[l], G.W[l], (const bf*)G.e[l - 1], (bf*)G.dd[l - 1],
                                          G.W[l - 1], c[l - 1], lcv, g);
       net->prof.mark("up2add", st);

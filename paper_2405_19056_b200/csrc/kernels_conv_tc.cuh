@@ -89,7 +89,18 @@ struct ConvArgs {
   uint32_t* tau_q;       // [B][Ho][Wo][Cout]
   uint32_t* tau_n;       // [B][Ho][Wo]
   float qscale, qsat;
+  // row tiles (forward_sharded, boundary rows first): 0 = every row tile of the frame, 1 = only the
+  // first and the last row tile (the rows the next halo exchange sends), 2 = only the others
+  int edge;
 };
+
+// Row tile `i` of the `nrt` a launch covers in edge mode `edge` -> the frame's row-tile index.
+__device__ __forceinline__ int edge_row_tile(int i, int nry, int edge) {
+  return edge == 0 ? i : edge == 1 ? (i == 0 ? 0 : nry - 1) : 1 + i;
+}
+__host__ __device__ __forceinline__ int edge_row_tiles(int nry, int edge) {
+  return edge == 0 ? nry : edge == 1 ? (nry < 2 ? nry : 2) : (nry > 2 ? nry - 2 : 0);
+}
 
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
@@ -162,7 +173,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
   const int ntx = (a.Wo + TILE_M - 1) / TILE_M;
   const int nry = (a.Ho + RR - 1) / RR;             // row tiles per frame
-  const long ntiles = (long)a.B * nry * ntx;
+  const int nrt = edge_row_tiles(nry, a.edge);      // row tiles this launch covers
+  const long ntiles = (long)a.B * nrt * ntx;
   const int cta = blockIdx.x / a.nsplit, ncta = gridDim.x / a.nsplit;
   const int nchunk = Cin / 16;
 
@@ -174,8 +186,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (long t = cta; t < ntiles; t += ncta) {
       const int xt = (int)(t % ntx);
       const long r = t / ntx;
-      const int oy = (int)(r % nry) * RR;
-      const int b = (int)(r / nry);
+      const int oy = edge_row_tile((int)(r % nrt), nry, a.edge) * RR;
+      const int b = (int)(r / nrt);
       const int x0 = xt * TILE_M;
       if (lane == 0) tc::mbar_wait(empty + stage, ph ^ 1);
       __syncwarp();
@@ -228,8 +240,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (long t = cta; t < ntiles; t += ncta) {
         const int xt = (int)(t % ntx);
         const long r = t / ntx;
-        const int oy = (int)(r % nry) * RR;
-        const int b = (int)(r / nry);
+        const int oy = edge_row_tile((int)(r % nrt), nry, a.edge) * RR;
+        const int b = (int)(r / nrt);
         const int x0 = xt * TILE_M;
         for (int c = 0; c < nchunk; ++c) {
           tc::mbar_wait(empty + stage, ph ^ 1);
@@ -263,7 +275,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         bool skip_top = false;
         if (S == 2) {
           const long r = t / ntx;
-          skip_top = (int)(r % nry) == 0 && a.in_row_off == 0;
+          skip_top = edge_row_tile((int)(r % nrt), nry, a.edge) == 0 && a.in_row_off == 0;
         }
         bool first = true;
         for (int c = 0; c < nchunk; ++c) {
@@ -304,8 +316,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (long t = cta; t < ntiles; t += ncta) {
       const int xt = (int)(t % ntx);
       const long r = t / ntx;
-      const int oy0 = (int)(r % nry) * RR;
-      const int b = (int)(r / nry);
+      const int oy0 = edge_row_tile((int)(r % nrt), nry, a.edge) * RR;
+      const int b = (int)(r / nrt);
       const int px = xt * TILE_M + m;
       const bool pvalid = px < a.Wo;
       tc::mbar_wait(tfull + acc, aph);

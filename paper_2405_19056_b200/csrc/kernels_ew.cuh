@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_up2add(const __nv_bfloat16* __restrict_
   const int i = t >> lcv;
   if (2 * i >= W2) return;
   const int c8 = (t & ((1 << lcv) - 1)) * 8;
-  const int Y = blockIdx.y;
+  const int Y = blockIdx.y * g.ystep + g.yoff;
   const long b = blockIdx.z;
   int ya, yb;
   float wya, wyb;

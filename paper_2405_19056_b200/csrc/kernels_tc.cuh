@@ -432,8 +432,10 @@ inline int tc_setup_tile_geom(glassnet* net, int nranks, int rank, int row0, int
 template <int S, int NS, int EPI, int WS, int OST, int RR, int GB = 0>
 static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
                           const void* gbuf = nullptr, const void* direct = nullptr, const float* img = nullptr,
-                          const float* b3 = nullptr, const uint8_t* cover = nullptr) {
+                          const float* b3 = nullptr, const uint8_t* cover = nullptr, int edge = 0) {
   auto kfn = conv::k_conv_tc<S, NS, EPI, WS, OST, RR, GB>;
+  const long ntiles = (long)B * conv::edge_row_tiles((G.Ho + RR - 1) / RR, edge) * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
+  if (ntiles == 0) return;   // edge mode 2 of a tile with <= 2 row tiles: nothing inside
   static int smem_set = -1;   // the attribute is set once per instantiation and size (not per launch)
   if (smem_set < (int)L.smem) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
@@ -444,11 +446,11 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
   a.img = img;
   for (int i = 0; i < 3; ++i) a.b3[i] = b3 ? b3[i] : 0.f;
   a.cover = cover; a.tau_q = net->tau_q; a.tau_n = net->tau_n; a.qscale = net->qscale; a.qsat = net->qsat;
+  a.edge = edge;
   a.Cin = L.Cin; a.Cout = L.Cout; a.Ho = G.Ho; a.Wo = G.Wo; a.B = B; a.nsplit = L.nsplit; a.nstage = L.nstage;
   a.in_row_off = G.in_row_off; a.out_row_off = G.out_row_off; a.out_rows_buf = G.out_rows_buf;
   a.in_rows_buf = G.Hi_buf;
   a.gbuf = reinterpret_cast<const uint16_t*>(gbuf); a.direct = reinterpret_cast<const uint16_t*>(direct); a.Wi = G.Wi;
-  const long ntiles = (long)B * ((G.Ho + RR - 1) / RR) * ((G.Wo + conv::TILE_M - 1) / conv::TILE_M);
   long per_split = (long)net->num_sms * L.ctas_per_sm / L.nsplit;
   if (per_split > ntiles) per_split = ntiles;
   if (per_split < 1) per_split = 1;
@@ -457,7 +459,7 @@ static void launch_conv_k(glassnet* net, const TcConv& L, const ConvGeom& G, int
 
 static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B, cudaStream_t st,
                        const void* gbuf = nullptr, const void* direct = nullptr, const float* img = nullptr,
-                       const float* b3 = nullptr, const uint8_t* cover = nullptr) {
+                       const float* b3 = nullptr, const uint8_t* cover = nullptr, int edge = 0) {
   if (L.epi == 3) {   // N4: h's second conv, accumulated into the fixed-point latent where covered
 #define CONV_E3(NS_, RR_)                                                                                \
     if (L.S == 1 && L.NS == NS_ && L.ws == 0 && L.ost == 0 && L.rr == RR_) {                            \
@@ -502,7 +504,8 @@ static int launch_conv(glassnet* net, const TcConv& L, const ConvGeom& G, int B,
   }
 #define CONV_K(S_, NS_, E_, WS_, OST_, RR_)                                                              \
   if (L.S == S_ && L.NS == NS_ && L.epi == E_ && L.ws == WS_ && L.ost == OST_ && L.rr == RR_) {         \
-    launch_conv_k<S_, NS_, E_, WS_, OST_, RR_>(net, L, G, B, st);                                       \
+    launch_conv_k<S_, NS_, E_, WS_, OST_, RR_>(net, L, G, B, st, nullptr, nullptr, nullptr, nullptr,     \
+                                               nullptr, edge);                                          \
     return 0;                                                                                           \
   }
 #define CONV_S1(NS_, RR_) CONV_K(1, NS_, 0, 0, 0, RR_) CONV_K(1, NS_, 0, 0, 1, RR_) CONV_K(1, NS_, 1, 0, 0, RR_)

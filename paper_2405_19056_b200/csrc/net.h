@@ -47,7 +47,10 @@ namespace gn {
 // back to back; a row tile (forward_sharded, comm.cu) exchanges halo rows at EXCH steps.
 enum StepKind { ST_PREP = 0, ST_CONV = 1, ST_TB = 2, ST_UP = 3, ST_OUT = 4, ST_EXCH = 5 };
 enum TensorId { TEN_X = 0, TEN_E = 1, TEN_Y = 5, TEN_D = 9, TEN_Z = 13 };   // TEN_E + l, ...
-struct Step { int kind; int idx; };   // CONV: conv slot (l = F_l, 4+l = R_l); UP: level; EXCH: tensor
+// CONV: conv slot (l = F_l, 4+l = R_l); UP: level; EXCH: tensor.  edge (row tiles, boundary rows
+// first): 0 = every row, 1 = only the first / last rows (what the next EXCH sends), 2 = the rest
+// (runs while that EXCH is in flight).
+struct Step { int kind; int idx; int edge = 0; };
 // tile = true: the row-tile order (T right after F0, on its own stream; see tc_run_step)
 int tc_steps(const struct ::glassnet* net, Step* out, int max, bool tile = false);
 int tc_prepare_tile(struct ::glassnet* net, int nranks, int rank, int row0, int rows);

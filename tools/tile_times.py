@@ -52,13 +52,20 @@ for N in (1, 2, 4, 8):
     rank_ms = all_ms * max_rows / H
     if N == 1:
         t1 = all_ms
-    # exchange model: 12 grouped send/recv phases per frame (x16, e0..e2, decoder y/d, z), each
+    # exchange model: 10 grouped send/recv phases per frame (x16, e0..e3, y3, d2, y2, d1, z), each
     # ~15 us of NCCL latency on NVLink at these 0.1-0.5 MB sizes (bandwidth time < 1 us at 770 GB/s)
-    exch_ms = 0.0 if N == 1 else 12 * 0.015
+    exch_ms = 0.0 if N == 1 else 10 * 0.015
     pred = rank_ms + exch_ms
+    # boundary rows first (the tile step list, GN_TILE_SPLIT policy): the exchanges of split producers
+    # run beside their interior rows (counted hidden); the others stay exposed
+    pol = int(os.environ.get("GN_TILE_SPLIT", "1"))
+    nsplit = 0 if pol == 0 else (4 if pol == 1 else 9)
+    pred_bf = rank_ms + (0.0 if N == 1 else (10 - nsplit) * 0.015)
     res["N"][str(N)] = {"all_tiles_ms": all_ms, "max_rank_rows": max_rows, "rank_compute_ms": rank_ms,
                         "exchange_model_ms": exch_ms, "predicted_frame_ms": pred,
-                        "predicted_efficiency": t1 / (N * pred), "compute_only_efficiency": t1 / (N * rank_ms)}
+                        "predicted_efficiency": t1 / (N * pred), "compute_only_efficiency": t1 / (N * rank_ms),
+                        "predicted_frame_ms_boundary_first": pred_bf,
+                        "predicted_efficiency_boundary_first": t1 / (N * pred_bf)}
     print(N, json.dumps(res["N"][str(N)]), flush=True)
     for x in nets:
         x.close()
