@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -322,6 +323,22 @@ static gn::Up2Rows full_rows(int rows_f, int rows_c) {
   return g;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size, not per launch.
+static void smem_attr_once(const void* kfn, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& e : done)
+    if (e.first == kfn) {
+      if (e.second >= smem) return;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e.second = smem;
+      return;
+    }
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done.emplace_back(kfn, smem);
+}
+
 // T + B + psi on the SIMT kernel (FFMA): the fp32 check mode, the SIMT family, and -- with N2's
 // positional encoding -- the tensor-core family's T stage (h's layer 1 over 11 (2L+1) encoded
 // features per record has no tensor-core kernel here).
@@ -342,7 +359,7 @@ static void launch_tb_simt(glassnet* net, const T* tbuf, const uint8_t* tcount, 
 #define TB_LAUNCH(HH, CC)                                                                                      \
   {                                                                                                            \
     auto kfn = sig ? gn::k_tb_simt<T, HH, CC, true> : gn::k_tb_simt<T, HH, CC, false>;                        \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
+    smem_attr_once((const void*)kfn, (int)smem);                                                              \
     kfn<<<g, 128, smem, st>>>(tbuf, tcount, e0, direct, net->w_tb, psi, P0, K, d.pool, ld, norm, gn_pe_L(d)); \
   }
   if (h == 64 && c[0] == 32) TB_LAUNCH(64, 32)
