@@ -1,5 +1,5 @@
-"""A/B timing of the F0 / S1 G-buffer producers (GN_LIB selects the library): per-stage CUDA-event
-times of conv_F0 in a c3 forward of 8 frames and of ss_S1 in an 8-frame super-sample."""
+"""A/B timing of conv variants (GN_LIB selects the library): per-stage CUDA-event times of the convs
+in a c3 forward of 8 frames and of an 8-frame super-sample (ss_S1, ss_S2)."""
 import os
 import sys
 
@@ -29,5 +29,6 @@ for _ in range(R):
     net.forward(g, d, t, n, img)
     net.supersample(img, gh, o)
 st = net.profile_end()
-print(os.path.basename(os.environ.get("GN_LIB", "libglassnet.so")),
-      " ".join(f"{k} {v[0] / v[1]:.4f}" for k, v in st.items() if k in ("conv_F0", "ss_S1", "ss_S2", "T_B_psi")))
+conv = sum(v[0] for k, v in st.items() if k.startswith("conv_")) / R
+print(os.path.basename(os.environ.get("GN_LIB", "libglassnet.so")), f"convs {conv:.4f}",
+      " ".join(f"{k} {v[0] / v[1]:.4f}" for k, v in st.items() if k.startswith(("conv_", "ss_", "up2")) or k == "T_B_psi"))
