@@ -156,3 +156,17 @@ def test_gloo_row_tiles_with_halo_exchange_equal_full_frame():
     cfg = synth.Config("g", H, W, 1, K, 3, (16, 32, 64), 32, "fp32")
     full = oracle_full(cfg, synth.make_weights((16, 32, 64), 3, 32), synth.gen_frames(cfg, seed=5))
     assert np.array_equal(got, full)
+
+
+def test_halo_bench_harness_gloo():
+    """tools/halo_bench.py (the §8(e) halo microbenchmark) at world size 2 with gloo on CPU: the
+    neighbour exchange pattern completes and each halo row holds the neighbour's data."""
+    import json as _json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", "tools/halo_bench.py", "--cpu",
+           "--iters", "5", "--warmup", "2"]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = [l for l in res.stdout.splitlines() if l.startswith("{")][-1]
+    d = _json.loads(line)
+    assert d["world"] == 2 and all(p["ok"] for p in d["phases"].values())
