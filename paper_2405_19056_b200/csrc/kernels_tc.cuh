@@ -260,6 +260,7 @@ static int setup_conv(glassnet* net, TcConv& L, int S, const float* W, const flo
       if (2 * rr * NS <= 512 && conv_smem(S, Cin, NS, 2, L.ws, 0, rr, epi) <= LIMIT) { L.rr = rr; break; }
   if (const char* e = getenv("GN_CONV_RR")) if (S == 1) L.rr = atoi(e);
   L.nstage = 4;
+  if (const char* e = getenv("GN_CONV_NSTAGE")) L.nstage = atoi(e);   // diagnostic: pipeline depth cap
   while (L.nstage > 2 && conv_smem(S, Cin, NS, L.nstage, L.ws, 0, L.rr, epi) > LIMIT) --L.nstage;
   // staged (bulk-copied) output when it fits without giving up pipeline depth
   L.ost = (epi == 0 && !L.ws && conv_smem(S, Cin, NS, L.nstage, L.ws, 1, L.rr, epi) <= LIMIT && !getenv("GN_CONV_NO_OST"))
