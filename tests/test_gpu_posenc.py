@@ -102,3 +102,29 @@ def test_pe_row_tiles_bitwise(cuda_ok):
     torch.cuda.synchronize()
     out = torch.cat([tl[4] for tl in tiles], dim=1)
     assert np.array_equal(ref.cpu().numpy().view(np.uint32), out.cpu().numpy().view(np.uint32))
+
+
+def test_pe_c3_geometry_windows(cuda_ok):
+    """N2 in the bench's launch configuration (c3 1920x1080, K=8, pe_L=6, tensor-core family; 4
+    frames here): 16x32 windows at the corners and centre of frames 0 and 3 against the windowed
+    oracle (margin 64; the encoding adds no receptive field)."""
+    import torch
+    from helpers import window_oracle
+    from synth import device
+    c3 = synth.CONFIGS["c3"]
+    cfg = synth.Config("c3pe", c3.height, c3.width, 4, c3.k_slots, c3.levels, c3.widths, c3.t_hidden, "bf16",
+                       extra={"pe_L": 6})
+    net = net_for(cfg)
+    g, d, t, n = device.alloc_and_fill(cfg, nframes=4, seed=1)
+    out = net.forward(g, d, t, n)
+    torch.cuda.synchronize()
+    w = weights_for(cfg)
+    H, W = cfg.height, cfg.width
+    for b in (0, 3):
+        for r0, c0 in ((0, 0), (H // 2, W // 2 - 16), (H - 16, W - 32)):
+            rows, cols = (r0, r0 + 16), (c0, c0 + 32)
+            ref = window_oracle(cfg, w, b, rows, cols, margin=64)
+            mx, mn = errs(out[b, rows[0]:rows[1], cols[0]:cols[1]].cpu().numpy(), ref)
+            print(f"PE c3 frame {b} window {rows}x{cols}: max {mx:.3e} mean {mn:.3e}")
+            assert mx <= BF16_TOL[0] and mn <= BF16_TOL[1]
+    net.close()
