@@ -100,8 +100,11 @@ struct TbParams {
 // two 16-bit fields per word and prefix-summed across the block in one pass; the sorted
 // superblock is staged in shared memory and written with 16-byte stores.  The order inside
 // a bin is deterministic but irrelevant (every MMA row is independent).
+#ifndef GN_SORT_MINB
+#define GN_SORT_MINB 2   // two blocks per SM (<= 64 registers): the sort is latency-bound per block
+#endif
 template <int K>
-__global__ void __launch_bounds__(TB_SBP / 8) k_tb_sort(const uint8_t* __restrict__ tcount, uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(TB_SBP / 8, GN_SORT_MINB) k_tb_sort(const uint8_t* __restrict__ tcount, uint32_t* __restrict__ perm,
                                                         long P) {
   constexpr int NT = TB_SBP / 8, NW = NT / 32;   // threads x 8 pixels; per-bin totals <= TB_SBP < 2^16
   static_assert(NT % 32 == 0 && TB_SBP < 65536, "sort block");
